@@ -1,0 +1,167 @@
+/*
+ * palu_b200.h -- C ABI of the B200-native Palu latent-KV RoPE decode path.
+ *
+ * The reference (Palu, pkg/src/palu) has no FFI: its boundary is the Python
+ * API of palu.attention (attention.py:392-448 palu_decode_step_rope and the
+ * functions it calls).  Each entry point below replaces one numpy stage of
+ * that function; the Python host mirror (paper_2407_21118_b200/attention.py)
+ * binds them with ctypes exactly as INTEGRATION.md shows.
+ *
+ * Conventions
+ *   - plain pointers and sizes only; all pointers are DEVICE pointers unless
+ *     named *_host; memory is owned by the caller (torch on the Python side);
+ *   - every call is stream-ordered on `stream` (a cudaStream_t, may be NULL);
+ *   - the decode position lives on the device (`t_dev`: rows cached BEFORE
+ *     this step) so a whole step can be captured once in a CUDA graph;
+ *   - return 0 on success, negative PALU_E* codes otherwise (the host shim
+ *     maps PALU_EVALIDATION to palu.errors.ValidationError); no C++
+ *     exceptions cross this boundary.
+ *
+ * Cache layout in HBM (one layer):
+ *   latent rows  [B][G][T_cap][row]   row = R_pad elements of the storage
+ *                                     dtype (bits==16) or R_pad*bits/8 bytes
+ *                                     of little-endian packed codes (bits<16,
+ *                                     quant.py:156-169 order inside a row)
+ *   scales       [B][G][T_cap] float  (quantised sides only)
+ *   zero points  [B][G][T_cap] float  (quantised sides only; integral values,
+ *                                     exact below 2^24; exact fp64 scales and
+ *                                     int64 zero points go to optional export
+ *                                     arrays so quantized_latent() stays
+ *                                     bit-exact)
+ * Columns >= rank(g) are zero (raw) / code 0 (quantised) and meet zero rows
+ * of the padded factors, so they never contribute.
+ */
+#ifndef PALU_B200_H
+#define PALU_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PALU_OK 0
+#define PALU_EVALIDATION (-1)
+#define PALU_ECUDA (-2)
+#define PALU_EUNSUPPORTED (-3)
+
+#define PALU_DTYPE_F32 0
+#define PALU_DTYPE_BF16 1
+
+/* Library identity and the device check (fails on anything but sm_100). */
+const char* palu_version(void);
+int palu_device_check(int device);
+const char* palu_last_error(void);
+
+/*
+ * y[b][n] (+)= sum_k W[n][k] * x[b][k]   W row-major N x K in `dtype`.
+ * Replaces the numpy projections of the step: x @ W_q[:, head]
+ * (attention.py:430), x @ A_g (attention.py:343-347, _append_latents) and
+ * ctx @ wo_fused (attention.py:361, _value_output).
+ */
+int palu_gemv(int dtype, const void* W, int N, int K, const float* x, int B, int ldx,
+              float* y, int ldy, int accumulate, void* stream);
+
+/*
+ * Append row t (= *t_dev) of every group's latent store from fp32 latents
+ * lat[b][lat_off[g] + c], c < ranks[g] (ranks/lat_off: device int arrays).
+ * bits==16 stores raw `dtype` values (attention.py:249-251); bits in
+ * {2,3,4,8} quantises per token in fp64 with quant.py:87-99's operation
+ * order (round half away from zero, range floor 1e-8) and packs the codes.
+ * Replaces _GroupStore.append (attention.py:248-255).
+ */
+int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat, int G,
+                       const int* ranks, const int* lat_off, void* rows, float* scales,
+                       float* zps, double* scales64, int64_t* zps64, int R_pad, int T_cap,
+                       const int* t_dev, void* stream);
+
+/*
+ * Bit-exact per-token quantiser on fp64 rows (quant.py:87-99): codes (uint8,
+ * one per element), scales (fp64) and zero points (int64).  The cache uses
+ * the same device function; this entry point exposes it for parity tests.
+ */
+int palu_quantize_rows(const double* x, int rows, int cols, int bits, uint8_t* codes,
+                       double* scales, int64_t* zps, void* stream);
+
+/* LE bit-packing of `rows` x `cols` codes, one byte-aligned packed row each
+ * (quant.py:156-169 order); cols*bits must be a multiple of 8. */
+int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* packed,
+                   void* stream);
+
+/*
+ * Query absorption for the RoPE score (attention.py:428-444 restated):
+ *   q_rot = RoPE(q, t) per head with fp64 angles, then per head p of key
+ *   group g and pair j < d_h/2:
+ *     u_j = scale * (q_rot[j]   * B_g[:, p*d_h+j] + q_rot[j+h] * B_g[:, p*d_h+j+h])
+ *     w_j = scale * (q_rot[j+h] * B_g[:, p*d_h+j] - q_rot[j]   * B_g[:, p*d_h+j+h])
+ *   so that  q_rot . RoPE_t'(h B_g[:, head]) = sum_j cos(t' th_j) h.u_j + sin(t' th_j) h.w_j.
+ * bk: [G][R_pad][s_k*d_h] in `dtype` (rows >= rank zero).
+ * layout 0: uw fp32 [B][n][R_pad][d_h]  (cols j < h: u_j, j >= h: w_{j-h})
+ * layout 1: uw bf16 [B][G][s_k*d_h][R_pad] (K-major rows, tcgen05 B operand)
+ */
+int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, int head_dim,
+                      int s_k, const void* bk, int R_pad, const double* theta, float scale,
+                      const int* t_dev, void* uw, int layout, void* stream);
+
+/*
+ * RoPE score over the latent key cache (attention.py:433-444):
+ *   logits[b][i][t'] = q_rot_i . RoPE_t'( H_k[g(i)][t'] @ B_g[:, head i] ) / sqrt(d_h)
+ * for t' in [0, *t_dev], via the absorbed uw (layout 0).  bits 16 reads raw
+ * rows; bits < 16 dequantises (code - z) * s on load (attention.py:265-268).
+ * logits: [B][n][ld_logits] fp32.
+ */
+int palu_rope_score(int dtype, int bits, const void* hk, const float* scales, const float* zps,
+                    int B, int n_heads, int head_dim, int s_k, int G, int R_pad, int T_cap,
+                    const void* uw, const double* theta, const int* t_dev, float* logits,
+                    int ld_logits, void* stream);
+
+/*
+ * tcgen05 (sm_100a) RoPE score kernel, bf16 raw latents or 4/2-bit codes.
+ * Same contract as palu_rope_score with uw in layout 1.  Requires d_h 128,
+ * s_k*d_h a multiple of 256 and R_pad a multiple of 64 (<= 256);
+ * returns PALU_EUNSUPPORTED otherwise.
+ */
+int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
+                       int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
+                       const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
+                       void* stream);
+
+/* cos/sin tables for palu_rope_score_tc: [T_cap/128 + 1][64 pairs] tile bases
+ * (fp64-reduced) followed by [128][64] in-tile offsets, float2 each. */
+int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, void* stream);
+size_t palu_rope_table_floats(int half, int T_cap);
+
+/*
+ * Softmax + fused value path (attention.py:445-446, _value_output :350-362
+ * up to the wo_fused product):  ctx[b][o_off[i] + c] = sum_t' p_i[t'] H_v[g(i)][t'][c]
+ * with p_i = softmax(logits[b][i][0..*t_dev]), split over n_chunks token
+ * chunks per (b, group) and merged in a fixed order (deterministic).
+ * workspace: palu_softmax_value_workspace() bytes.
+ */
+size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks);
+int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales,
+                       const float* zps, int B, int n_heads, int s_v, int G, int R_pad,
+                       const int* ranks_v, const int* o_off, int T_cap, const float* logits,
+                       int ld_logits, const int* t_dev, int n_chunks, void* workspace,
+                       float* ctx, int ld_ctx, void* stream);
+
+/* *t_dev += 1 (cache.t += 1, attention.py:447) -- the last node of a step. */
+int palu_advance(int* t_dev, void* stream);
+
+/*
+ * Uncompressed baseline (K0; semantics of reference_decode,
+ * attention.py:133-168): append post-RoPE k and v rows at t, then per head
+ * softmax(K q / sqrt(d_h)) V.  kc/vc: [B][n][T_cap][d_h] in `dtype`;
+ * qkv: fp32 [B][3*d] (q | k | v, pre-RoPE); out: fp32 [B][d] attention
+ * context (before W_o).
+ */
+int palu_dense_decode(int dtype, const float* qkv, int B, int n_heads, int head_dim,
+                      void* kc, void* vc, int T_cap, const double* theta, const int* t_dev,
+                      int n_chunks, void* workspace, float* attn, void* stream);
+size_t palu_dense_workspace(int B, int n_heads, int head_dim, int n_chunks);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PALU_B200_H */

@@ -1,0 +1,92 @@
+// Shared helpers for the Palu B200 kernels (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "palu_b200.h"
+
+namespace palu {
+
+void set_error(const char* fmt, ...);
+
+#define PALU_CK(x)                                                                   \
+  do {                                                                               \
+    cudaError_t e_ = (x);                                                            \
+    if (e_ != cudaSuccess) {                                                         \
+      ::palu::set_error("%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_)); \
+      return PALU_ECUDA;                                                             \
+    }                                                                                \
+  } while (0)
+
+#define PALU_REQUIRE(cond, ...)               \
+  do {                                        \
+    if (!(cond)) {                            \
+      ::palu::set_error(__VA_ARGS__);         \
+      return PALU_EVALIDATION;                \
+    }                                         \
+  } while (0)
+
+#define PALU_LAUNCHED() PALU_CK(cudaGetLastError())
+
+typedef __nv_bfloat16 bf16;
+
+__device__ __forceinline__ float to_f(float v) { return v; }
+__device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
+template <typename T> __device__ __forceinline__ T from_f(float v);
+template <> __device__ __forceinline__ float from_f<float>(float v) { return v; }
+template <> __device__ __forceinline__ bf16 from_f<bf16>(float v) { return __float2bfloat16_rn(v); }
+
+// 16-byte vector of storage elements -> fp32
+template <typename T> struct Vec16;
+template <> struct Vec16<float> {
+  static constexpr int N = 4;
+  static __device__ __forceinline__ void unpack(const uint4& v, float* f) {
+    f[0] = __uint_as_float(v.x); f[1] = __uint_as_float(v.y);
+    f[2] = __uint_as_float(v.z); f[3] = __uint_as_float(v.w);
+  }
+};
+template <> struct Vec16<bf16> {
+  static constexpr int N = 8;
+  static __device__ __forceinline__ void unpack(const uint4& v, float* f) {
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      f[2 * i] = __uint_as_float(w[i] << 16);
+      f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+    }
+  }
+};
+
+__device__ __forceinline__ uint4 ldg_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+template <typename F>
+__device__ __forceinline__ float warp_reduce(float v, F op) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = op(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Extract code `k` from a little-endian packed row (quant.py:156-169 order).
+__device__ __forceinline__ uint32_t packed_code(const uint8_t* row, int row_bytes, int k, int bits) {
+  const int bit = k * bits;
+  const int byte = bit >> 3;
+  uint32_t v = row[byte];
+  if (byte + 1 < row_bytes) v |= uint32_t(row[byte + 1]) << 8;
+  return (v >> (bit & 7)) & ((1u << bits) - 1u);
+}
+
+// Round half away from zero (quant.py:31-32), no contraction.
+__device__ __forceinline__ double round_half_away(double x) {
+  return x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5));
+}
+
+}  // namespace palu

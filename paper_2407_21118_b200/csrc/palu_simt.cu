@@ -1,0 +1,1009 @@
+// Palu latent-KV RoPE decode: CUDA-core kernels + the C ABI (sm_100a).
+//
+// Each kernel restates one stage of palu_decode_step_rope
+// (/root/reference/pkg/src/palu/attention.py:392-448); see include/palu_b200.h
+// for the contracts and DESIGN.md for the HBM layout and rooflines.
+#include <math.h>
+#include <string.h>
+
+#include "palu_common.cuh"
+
+namespace palu {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// GEMV:  y[b][n] (+)= sum_k W[n][k] x[b][k].  Weight-streaming (HBM-bound):
+// one warp per 2 output rows, 16-byte non-allocating loads, 4 in flight per
+// lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
+// ---------------------------------------------------------------------------
+constexpr int GEMV_WARPS = 8;
+constexpr int GEMV_ROWS_PER_WARP = 2;
+
+template <typename T, int MAXB>
+__global__ void __launch_bounds__(GEMV_WARPS * 32)
+gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, int B, int ldx,
+            float* __restrict__ y, int ldy, int accumulate, int KC) {
+  extern __shared__ float xs[];  // [MAXB][KC]
+  using V = Vec16<T>;
+  constexpr int VEC = V::N;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row0 = (blockIdx.x * GEMV_WARPS + warp) * GEMV_ROWS_PER_WARP;
+  float acc[GEMV_ROWS_PER_WARP][MAXB];
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r)
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b) acc[r][b] = 0.f;
+
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    const int kc = min(KC, K - k0);
+    __syncthreads();
+    for (int i = threadIdx.x; i < B * kc; i += blockDim.x) {
+      const int b = i / kc, k = i - b * kc;
+      xs[b * KC + k] = x[(size_t)b * ldx + k0 + k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r) {
+      const int row = row0 + r;
+      if (row >= N) break;
+      const T* wr = W + (size_t)row * K + k0;
+      int k = lane * VEC;
+      for (; k + 3 * 32 * VEC < kc; k += 4 * 32 * VEC) {
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = ldg_stream(wr + k + u * 32 * VEC);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          float wf[VEC];
+          V::unpack(v[u], wf);
+          const int kk = k + u * 32 * VEC;
+#pragma unroll
+          for (int b = 0; b < MAXB; ++b) {
+            if (b < B) {
+#pragma unroll
+              for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xs[b * KC + kk + e], acc[r][b]);
+            }
+          }
+        }
+      }
+      for (; k < kc; k += 32 * VEC) {
+        uint4 v = ldg_stream(wr + k);
+        float wf[VEC];
+        V::unpack(v, wf);
+#pragma unroll
+        for (int b = 0; b < MAXB; ++b) {
+          if (b < B) {
+#pragma unroll
+            for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xs[b * KC + k + e], acc[r][b]);
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r) {
+    const int row = row0 + r;
+#pragma unroll
+    for (int b = 0; b < MAXB; ++b) {
+      float v = warp_reduce(acc[r][b], [](float a, float c) { return a + c; });
+      if (lane == 0 && row < N && b < B) {
+        float* dst = y + (size_t)b * ldy + row;
+        *dst = accumulate ? *dst + v : v;
+      }
+    }
+  }
+}
+
+template <typename T, int MAXB>
+static int launch_gemv(const T* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
+                       int acc, cudaStream_t st) {
+  int KC = K;
+  const int cap = (48 * 1024) / (4 * MAXB);
+  if (KC > cap) KC = (cap / 256) * 256;
+  const size_t smem = (size_t)MAXB * KC * sizeof(float);
+  const int rows_per_cta = GEMV_WARPS * GEMV_ROWS_PER_WARP;
+  dim3 grid((N + rows_per_cta - 1) / rows_per_cta);
+  gemv_kernel<T, MAXB><<<grid, GEMV_WARPS * 32, smem, st>>>(W, N, K, x, B, ldx, y, ldy, acc, KC);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+template <typename T>
+static int gemv_dispatch(const T* W, int N, int K, const float* x, int B, int ldx, float* y,
+                         int ldy, int acc, cudaStream_t st) {
+  for (int b0 = 0; b0 < B; b0 += 8) {
+    const int nb = B - b0 < 8 ? B - b0 : 8;
+    const float* xb = x + (size_t)b0 * ldx;
+    float* yb = y + (size_t)b0 * ldy;
+    int rc;
+    if (nb == 1) rc = launch_gemv<T, 1>(W, N, K, xb, nb, ldx, yb, ldy, acc, st);
+    else if (nb == 2) rc = launch_gemv<T, 2>(W, N, K, xb, nb, ldx, yb, ldy, acc, st);
+    else if (nb <= 4) rc = launch_gemv<T, 4>(W, N, K, xb, nb, ldx, yb, ldy, acc, st);
+    else rc = launch_gemv<T, 8>(W, N, K, xb, nb, ldx, yb, ldy, acc, st);
+    if (rc) return rc;
+  }
+  return PALU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Latent append (attention.py:343-347 + _GroupStore.append :248-255).
+// One CTA per (group, batch row).  Quantised sides run quant.py:87-99 in fp64.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void append_raw_kernel(const float* __restrict__ lat, int ld_lat, int G,
+                                  const int* __restrict__ ranks, const int* __restrict__ lat_off,
+                                  T* __restrict__ rows, int R_pad, int T_cap,
+                                  const int* __restrict__ t_dev) {
+  const int g = blockIdx.x, b = blockIdx.y;
+  const int t = *t_dev;
+  if (t >= T_cap) return;
+  const int r = ranks[g];
+  const float* src = lat + (size_t)b * ld_lat + lat_off[g];
+  T* dst = rows + (((size_t)b * G + g) * T_cap + t) * R_pad;
+  for (int c = threadIdx.x; c < R_pad; c += blockDim.x) dst[c] = from_f<T>(c < r ? src[c] : 0.f);
+}
+
+// Quantise one row held in shared memory (fp64).  Mirrors quant.py:93-98.
+__device__ void quantize_row_dev(const double* xrow, int cols, int bits, uint8_t* codes_out,
+                                 double* s_out, int64_t* z_out, double* red /*[64]*/) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double lo = INFINITY, hi = -INFINITY;
+  for (int c = tid; c < cols; c += nt) {
+    lo = fmin(lo, xrow[c]);
+    hi = fmax(hi, xrow[c]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const int warp = tid >> 5, lane = tid & 31, nw = (nt + 31) >> 5;
+  if (lane == 0) { red[warp] = lo; red[32 + warp] = hi; }
+  __syncthreads();
+  if (tid == 0) {
+    double l = red[0], h = red[32];
+    for (int w = 1; w < nw; ++w) { l = fmin(l, red[w]); h = fmax(h, red[32 + w]); }
+    red[0] = l; red[32] = h;
+  }
+  __syncthreads();
+  lo = red[0];
+  hi = red[32];
+  const double qmax = double((1 << bits) - 1);
+  // scales = max(hi - lo, 1e-8) / qmax ;  zps = rha(-lo / scales)
+  const double s = __ddiv_rn(fmax(__dsub_rn(hi, lo), 1e-8), qmax);
+  const double z = round_half_away(__ddiv_rn(-lo, s));
+  for (int c = tid; c < cols; c += nt) {
+    double q = __dadd_rn(round_half_away(__ddiv_rn(xrow[c], s)), z);
+    q = fmin(fmax(q, 0.0), qmax);
+    codes_out[c] = (uint8_t)q;
+  }
+  if (tid == 0) { *s_out = s; *z_out = (int64_t)z; }
+  __syncthreads();
+}
+
+__device__ void pack_row_dev(const uint8_t* codes, int cols, int bits, uint8_t* out) {
+  const int nbytes = cols * bits / 8;
+  for (int j = threadIdx.x; j < nbytes; j += blockDim.x) {
+    uint32_t byte = 0;
+    if (bits == 8) {
+      byte = codes[j];
+    } else if (bits == 4) {
+      byte = codes[2 * j] | (codes[2 * j + 1] << 4);
+    } else if (bits == 2) {
+      byte = codes[4 * j] | (codes[4 * j + 1] << 2) | (codes[4 * j + 2] << 4) | (codes[4 * j + 3] << 6);
+    } else {
+      for (int p = 0; p < 8; ++p) {
+        const int bit = 8 * j + p;
+        byte |= ((codes[bit / bits] >> (bit % bits)) & 1u) << p;
+      }
+    }
+    out[j] = (uint8_t)byte;
+  }
+}
+
+__global__ void append_quant_kernel(const float* __restrict__ lat, int ld_lat, int G, int bits,
+                                    const int* __restrict__ ranks, const int* __restrict__ lat_off,
+                                    uint8_t* __restrict__ rows, float* __restrict__ scales,
+                                    float* __restrict__ zps, double* __restrict__ scales64,
+                                    int64_t* __restrict__ zps64, int R_pad, int T_cap,
+                                    const int* __restrict__ t_dev) {
+  extern __shared__ double qsm[];  // [R_pad] values, 64 reduction slots, then codes
+  double* xrow = qsm;
+  double* red = qsm + R_pad;
+  uint8_t* codes = reinterpret_cast<uint8_t*>(red + 64);
+  __shared__ double s_sh;
+  __shared__ int64_t z_sh;
+  const int g = blockIdx.x, b = blockIdx.y;
+  const int t = *t_dev;
+  if (t >= T_cap) return;
+  const int r = ranks[g];
+  const float* src = lat + (size_t)b * ld_lat + lat_off[g];
+  for (int c = threadIdx.x; c < r; c += blockDim.x) xrow[c] = (double)src[c];
+  __syncthreads();
+  quantize_row_dev(xrow, r, bits, codes, &s_sh, &z_sh, red);
+  for (int c = r + threadIdx.x; c < R_pad; c += blockDim.x) codes[c] = 0;
+  __syncthreads();
+  const size_t tok = ((size_t)b * G + g) * T_cap + t;
+  pack_row_dev(codes, R_pad, bits, rows + tok * (size_t)(R_pad * bits / 8));
+  if (threadIdx.x == 0) {
+    scales[tok] = (float)s_sh;
+    zps[tok] = (float)z_sh;
+    if (scales64) scales64[tok] = s_sh;
+    if (zps64) zps64[tok] = z_sh;
+  }
+}
+
+__global__ void quantize_rows_kernel(const double* __restrict__ x, int cols, int bits,
+                                     uint8_t* __restrict__ codes, double* __restrict__ scales,
+                                     int64_t* __restrict__ zps) {
+  extern __shared__ double qsm[];
+  double* xrow = qsm;
+  double* red = qsm + cols;
+  __shared__ double s_sh;
+  __shared__ int64_t z_sh;
+  const int row = blockIdx.x;
+  for (int c = threadIdx.x; c < cols; c += blockDim.x) xrow[c] = x[(size_t)row * cols + c];
+  __syncthreads();
+  quantize_row_dev(xrow, cols, bits, codes + (size_t)row * cols, &s_sh, &z_sh, red);
+  if (threadIdx.x == 0) { scales[row] = s_sh; zps[row] = z_sh; }
+}
+
+__global__ void pack_rows_kernel(const uint8_t* __restrict__ codes, int cols, int bits,
+                                 uint8_t* __restrict__ packed) {
+  const int row = blockIdx.x;
+  pack_row_dev(codes + (size_t)row * cols, cols, bits, packed + (size_t)row * (cols * bits / 8));
+}
+
+// ---------------------------------------------------------------------------
+// Query absorption (attention.py:428-431 queries, folded into the key factor).
+// grid (n_heads, B); fp64 RoPE of q at t, then u/w columns per rank row k.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n_heads, int dh,
+                                    int s_k, const T* __restrict__ bk, int R_pad,
+                                    const double* __restrict__ theta, float scale,
+                                    const int* __restrict__ t_dev, void* __restrict__ uw,
+                                    int layout) {
+  extern __shared__ float qr[];  // [dh] rotated query
+  const int i = blockIdx.x, b = blockIdx.y;
+  const int half = dh / 2;
+  const int g = i / s_k, p = i - g * s_k;
+  const double pos = (double)(*t_dev);
+  const float* qh = q + (size_t)b * ld_q + (size_t)i * dh;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    double sn, cs;
+    sincos(pos * theta[j], &sn, &cs);  // attention.py:108-112 (fp64 angles)
+    const double lo = qh[j], hi = qh[j + half];
+    qr[j] = (float)(lo * cs - hi * sn);
+    qr[j + half] = (float)(lo * sn + hi * cs);
+  }
+  __syncthreads();
+  const int width = s_k * dh;
+  const T* bg = bk + (size_t)g * R_pad * width + (size_t)p * dh;
+  if (layout == 0) {
+    float* out = reinterpret_cast<float*>(uw) + ((size_t)b * n_heads + i) * R_pad * dh;
+    const int lanes_j = half < (int)blockDim.x ? half : (int)blockDim.x;
+    const int kstep = blockDim.x / lanes_j;
+    const int j0 = threadIdx.x % lanes_j, kk = threadIdx.x / lanes_j;
+    if (kk >= kstep) return;
+    for (int k = kk; k < R_pad; k += kstep) {
+      for (int j = j0; j < half; j += lanes_j) {
+        const float b1 = to_f(bg[(size_t)k * width + j]);
+        const float b2 = to_f(bg[(size_t)k * width + j + half]);
+        out[(size_t)k * dh + j] = scale * (qr[j] * b1 + qr[j + half] * b2);
+        out[(size_t)k * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
+      }
+    }
+  } else {
+    // bf16 [B][G][s_k*dh][R_pad]: row n = p*dh + c, c < half -> u_c, else w_{c-half}
+    bf16* out = reinterpret_cast<bf16*>(uw) + (((size_t)b * (n_heads / s_k) + g) * width +
+                                              (size_t)p * dh) * R_pad;
+    for (int idx = threadIdx.x; idx < half * R_pad; idx += blockDim.x) {
+      const int j = idx / R_pad, k = idx - j * R_pad;
+      const float b1 = to_f(bg[(size_t)k * width + j]);
+      const float b2 = to_f(bg[(size_t)k * width + j + half]);
+      out[(size_t)j * R_pad + k] = __float2bfloat16_rn(scale * (qr[j] * b1 + qr[j + half] * b2));
+      out[(size_t)(j + half) * R_pad + k] =
+          __float2bfloat16_rn(scale * (qr[j + half] * b1 - qr[j] * b2));
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// RoPE score, CUDA-core path.  logits[b][i][t'] = sum_j cos(t' th_j) (h.u_j)
+// + sin(t' th_j) (h.w_j) -- algebraically q_rot . RoPE_t'(h B) (see
+// palu_query_absorb).  Tiled for d_h = 128: a CTA owns (b, group) and walks
+// 64-token tiles; per head a 64 x 128 x R GEMM in registers, then the cos/sin
+// epilogue.  cos/sin come from fp64 angles per tile (attention.py:108-110).
+// ---------------------------------------------------------------------------
+constexpr int SC_TT = 64;  // tokens per tile
+constexpr int SC_KC = 32;  // rank rows per chunk
+
+template <typename T, int BITS>
+__device__ __forceinline__ float load_latent(const void* rows, const float* scales,
+                                             const float* zps, size_t tok, int R_pad, int k) {
+  if constexpr (BITS == 16) {
+    return to_f(reinterpret_cast<const T*>(rows)[tok * R_pad + k]);
+  } else {
+    const int rb = R_pad * BITS / 8;
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(rows) + tok * rb;
+    const float code = (float)packed_code(row, rb, k, BITS);
+    return (code - zps[tok]) * scales[tok];
+  }
+}
+
+template <typename T, int BITS>
+__global__ void __launch_bounds__(256)
+rope_score_tiled_kernel(const void* __restrict__ hk, const float* __restrict__ scales,
+                        const float* __restrict__ zps, int n_heads, int s_k, int G, int R_pad,
+                        int T_cap, const float* __restrict__ uw, const double* __restrict__ theta,
+                        const int* __restrict__ t_dev, float* __restrict__ logits, int ld_logits) {
+  constexpr int DH = 128, HALF = 64, HS = SC_TT + 4;
+  extern __shared__ __align__(16) float sc_sm[];
+  float (*Hs)[HS] = reinterpret_cast<float (*)[HS]>(sc_sm);                  // [SC_KC][HS]
+  float (*Us)[DH] = reinterpret_cast<float (*)[DH]>(sc_sm + SC_KC * HS);     // [SC_KC][DH]
+  float2 (*CSs)[HALF] = reinterpret_cast<float2 (*)[HALF]>(sc_sm + SC_KC * HS + SC_KC * DH);
+  const int g = blockIdx.y, b = blockIdx.z;
+  const int T_rows = *t_dev + 1;
+  const int n_tiles = (T_rows + SC_TT - 1) / SC_TT;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const size_t tok_base = ((size_t)b * G + g) * T_cap;
+  for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int t0 = tile * SC_TT;
+    __syncthreads();
+    for (int idx = tid; idx < SC_TT * HALF; idx += blockDim.x) {
+      const int tt = idx / HALF, j = idx - tt * HALF;
+      double sn, cs;
+      sincos((double)(t0 + tt) * theta[j], &sn, &cs);
+      CSs[tt][j] = make_float2((float)cs, (float)sn);
+    }
+    for (int p = 0; p < s_k; ++p) {
+      const int head = g * s_k + p;
+      const float* uwh = uw + ((size_t)b * n_heads + head) * R_pad * DH;
+      float acc[4][8];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[a][c] = 0.f;
+      for (int k0 = 0; k0 < R_pad; k0 += SC_KC) {
+        __syncthreads();
+        for (int idx = tid; idx < SC_KC * SC_TT; idx += blockDim.x) {
+          const int tt = idx / SC_KC, kk = idx - tt * SC_KC;
+          const int t = t0 + tt;
+          Hs[kk][tt] = (t < T_rows) ? load_latent<T, BITS>(hk, scales, zps, tok_base + t, R_pad, k0 + kk)
+                                    : 0.f;
+        }
+        for (int idx = tid; idx < SC_KC * DH / 4; idx += blockDim.x) {
+          const int kk = idx / (DH / 4), c4 = idx - kk * (DH / 4);
+          reinterpret_cast<float4*>(&Us[kk][0])[c4] =
+              reinterpret_cast<const float4*>(uwh + (size_t)(k0 + kk) * DH)[c4];
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int kk = 0; kk < SC_KC; ++kk) {
+          const float4 a = reinterpret_cast<const float4*>(&Hs[kk][0])[ty];
+          const float4 u = reinterpret_cast<const float4*>(&Us[kk][0])[tx];
+          const float4 w = reinterpret_cast<const float4*>(&Us[kk][HALF])[tx];
+          const float av[4] = {a.x, a.y, a.z, a.w};
+          const float bv[8] = {u.x, u.y, u.z, u.w, w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+#pragma unroll
+            for (int c = 0; c < 8; ++c) acc[r][c] = fmaf(av[r], bv[c], acc[r][c]);
+        }
+      }
+      // epilogue: sum_j cos_j * h.u_j + sin_j * h.w_j over this thread's 4 pairs
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int tt = ty * 4 + r;
+        float v = 0.f;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const float2 cs = CSs[tt][tx * 4 + c];
+          v = fmaf(cs.x, acc[r][c], v);
+          v = fmaf(cs.y, acc[r][c + 4], v);
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        const int t = t0 + tt;
+        if (tx == 0 && t < T_rows) logits[((size_t)b * n_heads + head) * ld_logits + t] = v;
+      }
+    }
+  }
+}
+
+// Generic (any even d_h) score: one thread per (token, head).  Used for the
+// small reference-test shapes; the tiled/tcgen05 kernels cover d_h = 128.
+template <typename T, int BITS>
+__global__ void rope_score_generic_kernel(const void* __restrict__ hk, const float* __restrict__ scales,
+                                          const float* __restrict__ zps, int n_heads, int dh,
+                                          int s_k, int G, int R_pad, int T_cap,
+                                          const float* __restrict__ uw,
+                                          const double* __restrict__ theta,
+                                          const int* __restrict__ t_dev, float* __restrict__ logits,
+                                          int ld_logits) {
+  const int b = blockIdx.z, head = blockIdx.y;
+  const int g = head / s_k;
+  const int T_rows = *t_dev + 1;
+  const int half = dh / 2;
+  const float* uwh = uw + ((size_t)b * n_heads + head) * R_pad * dh;
+  const size_t tok_base = ((size_t)b * G + g) * T_cap;
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < T_rows; t += gridDim.x * blockDim.x) {
+    float v = 0.f;
+    for (int j = 0; j < half; ++j) {
+      float a = 0.f, w = 0.f;
+      for (int k = 0; k < R_pad; ++k) {
+        const float h = load_latent<T, BITS>(hk, scales, zps, tok_base + t, R_pad, k);
+        a = fmaf(h, uwh[(size_t)k * dh + j], a);
+        w = fmaf(h, uwh[(size_t)k * dh + j + half], w);
+      }
+      double sn, cs;
+      sincos((double)t * theta[j], &sn, &cs);
+      v += (float)cs * a + (float)sn * w;
+    }
+    logits[((size_t)b * n_heads + head) * ld_logits + t] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Softmax + value (attention.py:445-446, 350-362).  Split-T partials, then a
+// fixed-order merge (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int SV_THREADS = 256;
+constexpr int SV_HP = 4;           // heads per pass
+constexpr int SV_MAX_CHUNK = 4096;  // tokens per chunk cap (smem)
+
+struct SvPartial {
+  float* m;    // [B][n][NC]
+  float* l;    // [B][n][NC]
+  float* ctx;  // [B][n][NC][R_pad]
+};
+
+__host__ __device__ inline SvPartial sv_carve(void* ws, int B, int n, int R_pad, int NC) {
+  SvPartial p;
+  float* f = reinterpret_cast<float*>(ws);
+  p.m = f;
+  p.l = f + (size_t)B * n * NC;
+  p.ctx = f + 2 * (size_t)B * n * NC;
+  return p;
+}
+
+template <typename T, int BITS>
+__global__ void __launch_bounds__(SV_THREADS)
+softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restrict__ scales,
+                             const float* __restrict__ zps, int n_heads, int s_v, int G, int R_pad,
+                             int T_cap, const float* __restrict__ logits, int ld_logits,
+                             const int* __restrict__ t_dev, int NC, SvPartial part) {
+  extern __shared__ float sv_sm[];  // ps[SV_HP][chunk] then red[...]
+  const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
+  const int T_rows = *t_dev + 1;
+  int clen = (T_rows + NC - 1) / NC;
+  clen = (clen + 7) & ~7;
+  const int c0 = c * clen;
+  const int c1 = min(T_rows, c0 + clen);
+  const int tid = threadIdx.x;
+  float* ps = sv_sm;                       // [SV_HP][clen]
+  float* red = sv_sm + SV_HP * clen;       // [SV_THREADS/32 * 2]
+  const size_t tok_base = ((size_t)b * G + g) * T_cap;
+
+  // thread -> (row lane group, column segment): COLV columns per thread
+  constexpr int COLV = (BITS == 16) ? Vec16<T>::N : 8;
+  const int tpr = R_pad / COLV;               // threads per token row
+  const int rows_par = SV_THREADS / tpr;      // token rows in parallel (>= 1)
+  const int my_row = tid / tpr, my_seg = tid - my_row * tpr;
+  float* accred = red + 2 * (SV_THREADS / 32);  // [rows_par][SV_HP][R_pad]
+
+  for (int p0 = 0; p0 < s_v; p0 += SV_HP) {
+    const int hp = min(SV_HP, s_v - p0);
+    __syncthreads();
+    // (1) per-head chunk max and exp, sums
+    for (int hh = 0; hh < hp; ++hh) {
+      const int head = g * s_v + p0 + hh;
+      const float* lg = logits + ((size_t)b * n_heads + head) * ld_logits;
+      float m = -INFINITY;
+      for (int t = c0 + tid; t < c1; t += SV_THREADS) m = fmaxf(m, lg[t]);
+      m = warp_reduce(m, [](float a, float d) { return fmaxf(a, d); });
+      if ((tid & 31) == 0) red[tid >> 5] = m;
+      __syncthreads();
+      if (tid == 0) {
+        float mm = red[0];
+        for (int w = 1; w < SV_THREADS / 32; ++w) mm = fmaxf(mm, red[w]);
+        red[SV_THREADS / 32] = mm;
+      }
+      __syncthreads();
+      m = red[SV_THREADS / 32];
+      float l = 0.f;
+      for (int t = c0 + tid; t < c1; t += SV_THREADS) {
+        const float e = expf(lg[t] - m);
+        ps[hh * clen + (t - c0)] = e;
+        l += e;
+      }
+      l = warp_reduce(l, [](float a, float d) { return a + d; });
+      __syncthreads();
+      if ((tid & 31) == 0) red[tid >> 5] = l;
+      __syncthreads();
+      if (tid == 0) {
+        float ll = 0.f;
+        for (int w = 0; w < SV_THREADS / 32; ++w) ll += red[w];
+        const size_t pi = ((size_t)b * n_heads + head) * NC + c;
+        part.m[pi] = (c0 < c1) ? m : -INFINITY;
+        part.l[pi] = (c0 < c1) ? ll : 0.f;
+      }
+      __syncthreads();
+    }
+    // (2) ctx partial: acc[h][e] = sum_t p_h[t] * H_v[t][seg*COLV + e]
+    float acc[SV_HP][COLV];
+#pragma unroll
+    for (int h = 0; h < SV_HP; ++h)
+#pragma unroll
+      for (int e = 0; e < COLV; ++e) acc[h][e] = 0.f;
+    if (my_row < rows_par) {
+      for (int t = c0 + my_row; t < c1; t += rows_par) {
+        float hvv[COLV];
+        const size_t tok = tok_base + t;
+        if constexpr (BITS == 16) {
+          const T* row = reinterpret_cast<const T*>(hv) + tok * R_pad + my_seg * COLV;
+          Vec16<T>::unpack(ldg_stream(row), hvv);
+        } else {
+          const int rb = R_pad * BITS / 8;
+          const uint8_t* row = reinterpret_cast<const uint8_t*>(hv) + tok * rb + my_seg * BITS;
+          uint64_t bitsv = 0;
+#pragma unroll
+          for (int q = 0; q < BITS; ++q) bitsv |= uint64_t(row[q]) << (8 * q);
+          const float s = scales[tok], z = zps[tok];
+#pragma unroll
+          for (int e = 0; e < COLV; ++e)
+            hvv[e] = ((float)((bitsv >> (e * BITS)) & ((1u << BITS) - 1u)) - z) * s;
+        }
+#pragma unroll
+        for (int h = 0; h < SV_HP; ++h) {
+          if (h < hp) {
+            const float pv = ps[h * clen + (t - c0)];
+#pragma unroll
+            for (int e = 0; e < COLV; ++e) acc[h][e] = fmaf(pv, hvv[e], acc[h][e]);
+          }
+        }
+      }
+    }
+    // reduce the rows_par partial sums
+    if (my_row < rows_par) {
+      for (int h = 0; h < hp; ++h)
+        for (int e = 0; e < COLV; ++e)
+          accred[((size_t)my_row * SV_HP + h) * R_pad + my_seg * COLV + e] = acc[h][e];
+    }
+    __syncthreads();
+    for (int idx = tid; idx < hp * R_pad; idx += SV_THREADS) {
+      const int h = idx / R_pad, col = idx - h * R_pad;
+      float v = 0.f;
+      for (int r = 0; r < rows_par; ++r) v += accred[((size_t)r * SV_HP + h) * R_pad + col];
+      const int head = g * s_v + p0 + h;
+      part.ctx[(((size_t)b * n_heads + head) * NC + c) * R_pad + col] = v;
+    }
+  }
+}
+
+__global__ void softmax_value_combine_kernel(int n_heads, int s_v, int R_pad,
+                                             const int* __restrict__ ranks_v,
+                                             const int* __restrict__ o_off, int NC, SvPartial part,
+                                             float* __restrict__ ctx, int ld_ctx) {
+  extern __shared__ float wsm[];  // [NC] weights
+  const int head = blockIdx.x, b = blockIdx.y;
+  const size_t base = ((size_t)b * n_heads + head) * NC;
+  __shared__ float Msh, Lsh;
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+    for (int c = 0; c < NC; ++c) M = fmaxf(M, part.m[base + c]);
+    float L = 0.f;
+    for (int c = 0; c < NC; ++c) {
+      const float w = (part.l[base + c] > 0.f) ? expf(part.m[base + c] - M) : 0.f;
+      wsm[c] = w;
+      L += w * part.l[base + c];
+    }
+    Msh = M;
+    Lsh = L;
+  }
+  __syncthreads();
+  const float invL = 1.f / Lsh;
+  const int r = ranks_v[head / s_v];
+  float* dst = ctx + (size_t)b * ld_ctx + o_off[head];
+  for (int col = threadIdx.x; col < r; col += blockDim.x) {
+    float v = 0.f;
+    for (int c = 0; c < NC; ++c) {
+      const float w = wsm[c];
+      if (w != 0.f) v = fmaf(w, part.ctx[(base + c) * R_pad + col], v);
+    }
+    dst[col] = v * invL;
+  }
+}
+
+__global__ void advance_kernel(int* t_dev) { *t_dev += 1; }
+
+// ---------------------------------------------------------------------------
+// Uncompressed baseline K0 (reference_decode, attention.py:133-168)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void dense_append_kernel(const float* __restrict__ qkv, int n_heads, int dh,
+                                    T* __restrict__ kc, T* __restrict__ vc, int T_cap,
+                                    const double* __restrict__ theta, const int* __restrict__ t_dev,
+                                    float* __restrict__ qrot) {
+  const int i = blockIdx.x, b = blockIdx.y;
+  const int d = n_heads * dh, half = dh / 2;
+  const int t = *t_dev;
+  const float* q = qkv + (size_t)b * 3 * d + (size_t)i * dh;
+  const float* k = q + d;
+  const float* v = q + 2 * d;
+  const size_t row = (((size_t)b * n_heads + i) * T_cap + t) * dh;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    double sn, cs;
+    sincos((double)t * theta[j], &sn, &cs);
+    const double klo = k[j], khi = k[j + half], qlo = q[j], qhi = q[j + half];
+    kc[row + j] = from_f<T>((float)(klo * cs - khi * sn));
+    kc[row + j + half] = from_f<T>((float)(klo * sn + khi * cs));
+    float* qo = qrot + ((size_t)b * n_heads + i) * dh;
+    qo[j] = (float)(qlo * cs - qhi * sn);
+    qo[j + half] = (float)(qlo * sn + qhi * cs);
+  }
+  for (int j = threadIdx.x; j < dh; j += blockDim.x) vc[row + j] = from_f<T>(v[j]);
+}
+
+// one warp per token: logit = k . q / sqrt(dh); chunk partials like K3
+template <typename T>
+__global__ void __launch_bounds__(256)
+dense_partial_kernel(int n_heads, int dh, const T* __restrict__ kc, const T* __restrict__ vc,
+                     int T_cap, const int* __restrict__ t_dev, const float* __restrict__ qrot,
+                     int NC, SvPartial part) {
+  extern __shared__ float dsm[];  // q[dh], lg[clen], acc[8][dh], red
+  const int c = blockIdx.x, i = blockIdx.y, b = blockIdx.z;
+  const int T_rows = *t_dev + 1;
+  int clen = (T_rows + NC - 1) / NC;
+  clen = (clen + 7) & ~7;
+  const int c0 = c * clen, c1 = min(T_rows, c0 + clen);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* qs = dsm;
+  float* lg = dsm + dh;
+  float* accs = lg + clen;  // [8][dh]
+  float* red = accs + 8 * dh;
+  const float scale = rsqrtf((float)dh);
+  for (int j = tid; j < dh; j += blockDim.x) qs[j] = qrot[((size_t)b * n_heads + i) * dh + j];
+  __syncthreads();
+  const size_t base = ((size_t)b * n_heads + i) * T_cap;
+  float m = -INFINITY;
+  for (int t = c0 + warp; t < c1; t += 8) {
+    const T* kr = kc + (base + t) * dh;
+    float s = 0.f;
+    for (int j = lane; j < dh; j += 32) s = fmaf(to_f(kr[j]), qs[j], s);
+    s = warp_reduce(s, [](float a, float e) { return a + e; });
+    s *= scale;
+    if (lane == 0) lg[t - c0] = s;
+    m = fmaxf(m, s);
+  }
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = red[0];
+  for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+  float l = 0.f;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int t = c0 + warp; t < c1; t += 8) {
+    const float p = expf(lg[t - c0] - m);
+    l += p;
+    const T* vr = vc + (base + t) * dh;
+    for (int j = lane, q = 0; j < dh && q < 4; j += 32, ++q) acc[q] = fmaf(p, to_f(vr[j]), acc[q]);
+  }
+  for (int j = lane, q = 0; j < dh && q < 4; j += 32, ++q) accs[warp * dh + j] = acc[q];
+  __syncthreads();
+  if (lane == 0) red[8 + warp] = l;
+  __syncthreads();
+  const size_t pi = ((size_t)b * n_heads + i) * NC + c;
+  if (tid == 0) {
+    float ll = 0.f;
+    for (int w = 0; w < 8; ++w) ll += red[8 + w];
+    part.m[pi] = (c0 < c1) ? m : -INFINITY;
+    part.l[pi] = (c0 < c1) ? ll : 0.f;
+  }
+  for (int j = tid; j < dh; j += blockDim.x) {
+    float v = 0.f;
+    for (int w = 0; w < 8; ++w) v += accs[w * dh + j];
+    part.ctx[pi * dh + j] = v;
+  }
+}
+
+__global__ void dense_combine_kernel(int n_heads, int dh, int NC, SvPartial part,
+                                     float* __restrict__ attn) {
+  const int i = blockIdx.x, b = blockIdx.y;
+  const size_t base = ((size_t)b * n_heads + i) * NC;
+  float M = -INFINITY;
+  for (int c = 0; c < NC; ++c) M = fmaxf(M, part.m[base + c]);
+  float L = 0.f;
+  for (int c = 0; c < NC; ++c)
+    if (part.l[base + c] > 0.f) L += expf(part.m[base + c] - M) * part.l[base + c];
+  for (int j = threadIdx.x; j < dh; j += blockDim.x) {
+    float v = 0.f;
+    for (int c = 0; c < NC; ++c)
+      if (part.l[base + c] > 0.f) v = fmaf(expf(part.m[base + c] - M), part.ctx[(base + c) * dh + j], v);
+    attn[(size_t)b * n_heads * dh + (size_t)i * dh + j] = v / L;
+  }
+}
+
+}  // namespace palu
+
+namespace palu {
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename T, int BITS>
+static void launch_score(const void* hk, const float* scales, const float* zps, int B,
+                         int n_heads, int head_dim, int s_k, int G, int R_pad, int T_cap,
+                         const float* uw, const double* theta, const int* t_dev, float* logits,
+                         int ld_logits, cudaStream_t st) {
+  if (head_dim == 128 && R_pad % SC_KC == 0) {
+    const int tiles = (T_cap + SC_TT - 1) / SC_TT;
+    int px = (2 * sm_count() + G * B - 1) / (G * B);
+    px = px < 1 ? 1 : (px > tiles ? tiles : px);
+    dim3 grid(px, G, B);
+    const size_t smem = sizeof(float) * (SC_KC * (SC_TT + 4) + SC_KC * 128 + 2 * SC_TT * 64);
+    static bool attr_set = false;
+    if (!attr_set) {
+      cudaFuncSetAttribute(rope_score_tiled_kernel<T, BITS>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_set = true;
+    }
+    rope_score_tiled_kernel<T, BITS><<<grid, 256, smem, st>>>(hk, scales, zps, n_heads, s_k, G, R_pad,
+                                                           T_cap, uw, theta, t_dev, logits,
+                                                           ld_logits);
+  } else {
+    const int blocks = (T_cap + 127) / 128;
+    dim3 grid(blocks < 64 ? blocks : 64, n_heads, B);
+    rope_score_generic_kernel<T, BITS><<<grid, 128, 0, st>>>(hk, scales, zps, n_heads, head_dim,
+                                                             s_k, G, R_pad, T_cap, uw, theta,
+                                                             t_dev, logits, ld_logits);
+  }
+}
+
+template <typename T, int BITS>
+static int launch_sv(const void* hv, const float* scales, const float* zps, int B, int n_heads,
+                     int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
+                     const float* logits, int ld_logits, const int* t_dev, int NC, SvPartial part,
+                     float* ctx, int ld_ctx, cudaStream_t st) {
+  constexpr int COLV = (BITS == 16) ? Vec16<T>::N : 8;
+  PALU_REQUIRE(R_pad % COLV == 0 && R_pad / COLV <= SV_THREADS,
+               "palu_softmax_value: R_pad=%d unsupported", R_pad);
+  int clen = (T_cap + NC - 1) / NC;
+  clen = (clen + 7) & ~7;
+  PALU_REQUIRE(clen <= SV_MAX_CHUNK, "palu_softmax_value: raise n_chunks (chunk %d > %d)", clen,
+               SV_MAX_CHUNK);
+  const int rows_par = SV_THREADS / (R_pad / COLV);
+  const size_t smem = sizeof(float) * ((size_t)SV_HP * clen + 2 * (SV_THREADS / 32) +
+                                       (size_t)rows_par * SV_HP * R_pad);
+  PALU_CK(cudaFuncSetAttribute(softmax_value_partial_kernel<T, BITS>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dim3 grid(NC, G, B);
+  softmax_value_partial_kernel<T, BITS><<<grid, SV_THREADS, smem, st>>>(
+      hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, t_dev, NC, part);
+  PALU_LAUNCHED();
+  softmax_value_combine_kernel<<<dim3(n_heads, B), 128, NC * sizeof(float), st>>>(
+      n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+}  // namespace palu
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+using namespace palu;
+
+extern "C" {
+
+const char* palu_version(void) { return "palu_b200 0.1.0 (sm_100a)"; }
+const char* palu_last_error(void) { return g_err; }
+
+int palu_device_check(int device) {
+  cudaDeviceProp prop;
+  PALU_CK(cudaGetDeviceProperties(&prop, device));
+  PALU_REQUIRE(prop.major == 10 && prop.minor == 0,
+               "palu_b200 is built for sm_100a only; device %d is sm_%d%d (%s)", device,
+               prop.major, prop.minor, prop.name);
+  return PALU_OK;
+}
+
+int palu_gemv(int dtype, const void* W, int N, int K, const float* x, int B, int ldx, float* y,
+              int ldy, int accumulate, void* stream) {
+  PALU_REQUIRE(N > 0 && K > 0 && B > 0, "palu_gemv: bad sizes N=%d K=%d B=%d", N, K, B);
+  const int vec = dtype == PALU_DTYPE_BF16 ? 8 : 4;
+  PALU_REQUIRE(K % vec == 0, "palu_gemv: K=%d must be a multiple of %d", K, vec);
+  PALU_REQUIRE(((uintptr_t)W & 15) == 0, "palu_gemv: W must be 16-byte aligned");
+  if (dtype == PALU_DTYPE_BF16)
+    return gemv_dispatch<bf16>((const bf16*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
+  PALU_REQUIRE(dtype == PALU_DTYPE_F32, "palu_gemv: unknown dtype %d", dtype);
+  return gemv_dispatch<float>((const float*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
+}
+
+int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat, int G,
+                       const int* ranks, const int* lat_off, void* rows, float* scales, float* zps,
+                       double* scales64, int64_t* zps64, int R_pad, int T_cap, const int* t_dev,
+                       void* stream) {
+  PALU_REQUIRE(B > 0 && G > 0 && R_pad > 0 && T_cap > 0, "palu_latent_append: bad sizes");
+  dim3 grid(G, B);
+  if (bits == 16) {
+    if (dtype == PALU_DTYPE_BF16)
+      append_raw_kernel<bf16><<<grid, 128, 0, S(stream)>>>(lat, ld_lat, G, ranks, lat_off,
+                                                            (bf16*)rows, R_pad, T_cap, t_dev);
+    else
+      append_raw_kernel<float><<<grid, 128, 0, S(stream)>>>(lat, ld_lat, G, ranks, lat_off,
+                                                             (float*)rows, R_pad, T_cap, t_dev);
+    PALU_LAUNCHED();
+    return PALU_OK;
+  }
+  PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+               "bits must be one of (2, 3, 4, 8), got %d", bits);
+  PALU_REQUIRE(R_pad % 32 == 0, "quantised rows need R_pad %% 32 == 0 (got %d)", R_pad);
+  const size_t smem = (size_t)(R_pad + 64) * sizeof(double) + R_pad;
+  append_quant_kernel<<<grid, 128, smem, S(stream)>>>(lat, ld_lat, G, bits, ranks, lat_off,
+                                                      (uint8_t*)rows, scales, zps, scales64, zps64,
+                                                      R_pad, T_cap, t_dev);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_quantize_rows(const double* x, int rows, int cols, int bits, uint8_t* codes,
+                       double* scales, int64_t* zps, void* stream) {
+  PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+               "bits must be one of (2, 3, 4, 8), got %d", bits);
+  PALU_REQUIRE(rows >= 0 && cols > 0, "palu_quantize_rows: bad sizes");
+  if (rows == 0) return PALU_OK;
+  const size_t smem = (size_t)(cols + 64) * sizeof(double);
+  PALU_CK(cudaFuncSetAttribute(quantize_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  quantize_rows_kernel<<<rows, 128, smem, S(stream)>>>(x, cols, bits, codes, scales, zps);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* packed,
+                   void* stream) {
+  PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+               "bits must be one of (2, 3, 4, 8), got %d", bits);
+  PALU_REQUIRE((cols * bits) % 8 == 0, "palu_pack_rows: cols*bits must be byte aligned");
+  if (rows == 0) return PALU_OK;
+  pack_rows_kernel<<<rows, 128, 0, S(stream)>>>(codes, cols, bits, packed);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, int head_dim,
+                      int s_k, const void* bk, int R_pad, const double* theta, float scale,
+                      const int* t_dev, void* uw, int layout, void* stream) {
+  PALU_REQUIRE(head_dim % 2 == 0, "rotary embedding requires an even head_dim");
+  PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k,
+               n_heads);
+  PALU_REQUIRE(layout == 0 || layout == 1, "palu_query_absorb: layout must be 0 or 1");
+  dim3 grid(n_heads, B);
+  const size_t smem = head_dim * sizeof(float);
+  if (dtype == PALU_DTYPE_BF16)
+    query_absorb_kernel<bf16><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
+                                                              (const bf16*)bk, R_pad, theta, scale,
+                                                              t_dev, uw, layout);
+  else
+    query_absorb_kernel<float><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
+                                                               (const float*)bk, R_pad, theta,
+                                                               scale, t_dev, uw, layout);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_rope_score(int dtype, int bits, const void* hk, const float* scales, const float* zps,
+                    int B, int n_heads, int head_dim, int s_k, int G, int R_pad, int T_cap,
+                    const void* uw, const double* theta, const int* t_dev, float* logits,
+                    int ld_logits, void* stream) {
+  PALU_REQUIRE(G * s_k == n_heads, "palu_rope_score: G*s_k != n_heads");
+  PALU_REQUIRE(ld_logits >= T_cap, "palu_rope_score: ld_logits < T_cap");
+  cudaStream_t st = S(stream);
+  const float* u = (const float*)uw;
+#define SCORE(T_, B_) launch_score<T_, B_>(hk, scales, zps, B, n_heads, head_dim, s_k, G, R_pad, \
+                                           T_cap, u, theta, t_dev, logits, ld_logits, st)
+  if (bits == 16) {
+    if (dtype == PALU_DTYPE_BF16) SCORE(bf16, 16);
+    else SCORE(float, 16);
+  } else if (bits == 8) SCORE(float, 8);
+  else if (bits == 4) SCORE(float, 4);
+  else if (bits == 3) SCORE(float, 3);
+  else if (bits == 2) SCORE(float, 2);
+  else PALU_REQUIRE(false, "bits must be one of (2, 3, 4, 8, 16), got %d", bits);
+#undef SCORE
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks) {
+  return sizeof(float) * (size_t)B * n_heads * n_chunks * (2 + (size_t)R_pad);
+}
+
+int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales, const float* zps,
+                       int B, int n_heads, int s_v, int G, int R_pad, const int* ranks_v,
+                       const int* o_off, int T_cap, const float* logits, int ld_logits,
+                       const int* t_dev, int n_chunks, void* workspace, float* ctx, int ld_ctx,
+                       void* stream) {
+  PALU_REQUIRE(G * s_v == n_heads, "palu_softmax_value: G*s_v != n_heads");
+  PALU_REQUIRE(n_chunks >= 1, "palu_softmax_value: n_chunks must be >= 1");
+  SvPartial part = sv_carve(workspace, B, n_heads, R_pad, n_chunks);
+  cudaStream_t st = S(stream);
+#define SV(T_, B_) return launch_sv<T_, B_>(hv, scales, zps, B, n_heads, s_v, G, R_pad, ranks_v, \
+                                            o_off, T_cap, logits, ld_logits, t_dev, n_chunks,    \
+                                            part, ctx, ld_ctx, st)
+  if (bits == 16) {
+    if (dtype == PALU_DTYPE_BF16) SV(bf16, 16);
+    SV(float, 16);
+  }
+  if (bits == 8) SV(float, 8);
+  if (bits == 4) SV(float, 4);
+  if (bits == 3) SV(float, 3);
+  if (bits == 2) SV(float, 2);
+#undef SV
+  PALU_REQUIRE(false, "bits must be one of (2, 3, 4, 8, 16), got %d", bits);
+}
+
+int palu_advance(int* t_dev, void* stream) {
+  advance_kernel<<<1, 1, 0, S(stream)>>>(t_dev);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+size_t palu_dense_workspace(int B, int n_heads, int head_dim, int n_chunks) {
+  return sizeof(float) * ((size_t)B * n_heads * n_chunks * (2 + (size_t)head_dim) +
+                          (size_t)B * n_heads * head_dim);
+}
+
+int palu_dense_decode(int dtype, const float* qkv, int B, int n_heads, int head_dim, void* kc,
+                      void* vc, int T_cap, const double* theta, const int* t_dev, int n_chunks,
+                      void* workspace, float* attn, void* stream) {
+  PALU_REQUIRE(head_dim % 2 == 0 && head_dim <= 128, "palu_dense_decode: head_dim %d", head_dim);
+  cudaStream_t st = S(stream);
+  SvPartial part = sv_carve(workspace, B, n_heads, head_dim, n_chunks);
+  float* qrot = part.ctx + (size_t)B * n_heads * n_chunks * head_dim;
+  int clen = (T_cap + n_chunks - 1) / n_chunks;
+  clen = (clen + 7) & ~7;
+  const size_t smem = sizeof(float) * (head_dim + clen + 8 * head_dim + 16);
+  PALU_REQUIRE(smem <= 200 * 1024, "palu_dense_decode: raise n_chunks");
+  dim3 g1(n_heads, B), g2(n_chunks, n_heads, B);
+  if (dtype == PALU_DTYPE_BF16) {
+    dense_append_kernel<bf16><<<g1, 64, 0, st>>>(qkv, n_heads, head_dim, (bf16*)kc, (bf16*)vc,
+                                                 T_cap, theta, t_dev, qrot);
+    PALU_CK(cudaFuncSetAttribute(dense_partial_kernel<bf16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dense_partial_kernel<bf16><<<g2, 256, smem, st>>>(n_heads, head_dim, (const bf16*)kc,
+                                                      (const bf16*)vc, T_cap, t_dev, qrot,
+                                                      n_chunks, part);
+  } else {
+    dense_append_kernel<float><<<g1, 64, 0, st>>>(qkv, n_heads, head_dim, (float*)kc, (float*)vc,
+                                                  T_cap, theta, t_dev, qrot);
+    PALU_CK(cudaFuncSetAttribute(dense_partial_kernel<float>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    dense_partial_kernel<float><<<g2, 256, smem, st>>>(n_heads, head_dim, (const float*)kc,
+                                                       (const float*)vc, T_cap, t_dev, qrot,
+                                                       n_chunks, part);
+  }
+  PALU_LAUNCHED();
+  dense_combine_kernel<<<g1, 128, 0, st>>>(n_heads, head_dim, n_chunks, part, attn);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+}  // extern "C"
