@@ -54,7 +54,7 @@ def fill_cache_direct(cache: LatentKVCache, li: int, x_rows, b: int | None = Non
     kv = cache.decomposed[li]
     K, V = cache._stores[li]
     dev = cache.device
-    x = x_rows if hasattr(x_rows, "device") else torch.from_numpy(np.asarray(x_rows, np.float64))
+    x = torch.from_numpy(np.asarray(x_rows, np.float64)) if isinstance(x_rows, np.ndarray) else x_rows
     x = x.to(dev, torch.float64)
     T = x.shape[0]
     cache.reserve(cache.t + T)
