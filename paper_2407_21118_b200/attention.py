@@ -474,6 +474,32 @@ class _Session:
             self._layer(li, st)
         _lib.call("palu_advance", _ptr(self.t_dev), st)
 
+    def profile_step(self) -> dict:
+        """One eager step with CUDA events around every launch; returns
+        {entry point: [ms per launch]} (the roofline's live kernel timing)."""
+        torch = _torch()
+        recs = []
+        orig = _lib.call
+
+        def timed(name, *args):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            rc = orig(name, *args)
+            b.record()
+            recs.append((name, a, b))
+            return rc
+
+        _lib.call = timed
+        try:
+            self.launch_step()
+        finally:
+            _lib.call = orig
+        torch.cuda.synchronize()
+        out = {}
+        for name, a, b in recs:
+            out.setdefault(name, []).append(a.elapsed_time(b))
+        return out
+
     def step_device(self):
         """Run one step on self.x (device) -> self.x; graph replay after warm-up."""
         torch = _torch()

@@ -158,3 +158,89 @@ def synth_model(d, n_heads, head_dim, s_k, ranks_k, s_v, ranks_v, seed, layers=1
         dl.append(LayerKV(key=key, value=value))
     config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=rope, rope_base=rope_base)
     return ModelWeights(layers=tuple(wl)), dl, config
+
+
+# ---------------------------------------------------------------------------
+# Bench-scale synthetic engine: weights generated directly on the GPU in the
+# kernels' layouts (no fp64 host copies of a 32-layer model), latent caches
+# filled with rows of the same statistics as x @ A for x ~ U[-1, 1).
+# ---------------------------------------------------------------------------
+def _shape_only(rows: int, cols: int):
+    """Zero-stride placeholder with the right shape (validation only)."""
+    return np.broadcast_to(np.float64(0.0), (rows, cols))
+
+
+def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=256, layers=32,
+                     batch=1, context=65536, extra=64, bits=16, dtype="bfloat16", seed=0,
+                     rope_base=10000.0):
+    """Return (weights, fused, cache) for a Llama-2-7B-shaped Palu model.
+
+    Random-init weights of that architecture (uniform, scaled as SURVEY
+    8(d)); the cache holds ``context`` tokens per sequence.
+    """
+    import torch as _t
+    from .attention import FusedWeights, LayerFused, _dt, _head_offsets, _rank_pad, _round_up, theta_table
+
+    torch = _torch()
+    code, tdt = _dt(dtype)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    G = n_heads // s
+    rk, rv = (rank_k,) * G, (rank_v,) * G
+    rk_pad, rv_pad = _rank_pad(rank_k, dtype), _rank_pad(rank_v, dtype)
+    ko = n_heads * rank_v
+    ko_pad = _round_up(ko, 8)
+
+    def U(*shape, scale):
+        return ((torch.rand(*shape, generator=g, device=dev, dtype=torch.float32) * 2 - 1) * scale)
+
+    i32 = lambda v: torch.tensor(list(v), dtype=torch.int32, device=dev)
+    lat_k = [i * rank_k for i in range(G)]
+    lat_v = [i * rank_v for i in range(G)]
+    fl, wl, dl = [], [], []
+    gran = Granularity.group_head(s) if 1 < s < n_heads else (
+        Granularity.multi_head() if s == 1 else Granularity.joint_head(n_heads))
+    for li in range(layers):
+        n1 = d + G * (rank_k + rank_v)
+        w1 = U(n1, d, scale=1.0 / math.sqrt(d)).to(tdt)
+        bk = torch.zeros(G, rk_pad, s * head_dim, device=dev, dtype=tdt)
+        bk[:, :rank_k] = U(G, rank_k, s * head_dim, scale=1.0 / math.sqrt(rank_k)).to(tdt)
+        # wo_fused rows: (B_v block @ W_o block); entries ~ scale of a product
+        woT = torch.zeros(d, ko_pad, device=dev, dtype=tdt)
+        woT[:, :ko] = U(d, ko, scale=1.0 / math.sqrt(3.0 * d)).to(tdt)
+        fl.append(LayerFused(wq_fused=None, wo_fused=None,
+                             q_offsets=_head_offsets(rk, s, n_heads),
+                             o_offsets=_head_offsets(rv, s, n_heads), key_ranks=rk, value_ranks=rv,
+                             s_k=s, s_v=s, rk_pad=rk_pad, rv_pad=rv_pad, ko_pad=ko_pad, w1=w1, bk=bk,
+                             woT=woT, ranks_k_dev=i32(rk), latoff_k_dev=i32(lat_k),
+                             ranks_v_dev=i32(rv), latoff_v_dev=i32(lat_v),
+                             o_off_dev=i32(_head_offsets(rv, s, n_heads))))
+        sh = _shape_only(d, d)
+        wl.append(LayerWeights(sh, sh, sh, sh))
+        kg = tuple(GroupFactors(_shape_only(d, rank_k), _shape_only(rank_k, s * head_dim), rank_k)
+                   for _ in range(G))
+        vg = tuple(GroupFactors(_shape_only(d, rank_v), _shape_only(rank_v, s * head_dim), rank_v)
+                   for _ in range(G))
+        dl.append(LayerKV(DecomposedLayer(gran, kg, d, head_dim, n_heads),
+                          DecomposedLayer(gran, vg, d, head_dim, n_heads)))
+    config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=True, rope_base=rope_base)
+    theta = theta_table(head_dim, rope_base)
+    fused = FusedWeights(layers=tuple(fl), config=config, dtype=dtype,
+                         theta_dev=torch.from_numpy(theta).to(dev), theta=theta)
+    cache = LatentKVCache(dl, config, bits, dtype=dtype, batch=batch, capacity=context + extra)
+    # fill: latent entries ~ x @ A with x ~ U[-1,1), A ~ U/sqrt(d): std 1/3
+    for li in range(layers):
+        for side in cache._stores[li]:
+            for gg in range(side.G):
+                r = side.ranks[gg]
+                for b in range(batch):
+                    for c0 in range(0, context, 16384):
+                        T = min(16384, context - c0)
+                        h = torch.randn(T, r, generator=g, device=dev, dtype=torch.float32) / 3.0
+                        if side.bits == FP_BITS:
+                            side.rows[b, gg, c0:c0 + T, :r].copy_(h.to(side.rows.dtype))
+                        else:
+                            _fill_side(side, gg, b, c0, h.double())
+    set_cache_t(cache, context)
+    return ModelWeights(layers=tuple(wl)), fused, cache
