@@ -334,7 +334,8 @@ class LatentKVCache:
     """
 
     def __init__(self, decomposed, config, bits=FP_BITS, *, dtype: str = "float32",
-                 batch: int = 1, capacity: int | None = None, device=None):
+                 batch: int = 1, capacity: int | None = None, device=None,
+                 score_kernel: str = "auto"):
         torch = _torch()
         k_bits, v_bits = _norm_bits(bits)
         if len(decomposed) != config.layers:
@@ -358,6 +359,9 @@ class LatentKVCache:
             self._stores.append((
                 _SideStore(rk, k_bits, _rank_pad(max(rk), dtype), batch, cap, dtype, self.device),
                 _SideStore(rv, v_bits, _rank_pad(max(rv), dtype), batch, cap, dtype, self.device)))
+        if score_kernel not in ("auto", "simt", "tcgen05"):
+            raise ValidationError(f"score_kernel must be auto|simt|tcgen05, got {score_kernel!r}")
+        self.score_kernel = score_kernel
         self._session = None
 
     # reference-compatible accessors -------------------------------------
@@ -431,6 +435,23 @@ class _Session:
         self.t_dev = torch.tensor([cache.t], dtype=torch.int32, device=dev)
         self.x_host = torch.zeros(self.B, self.d, dtype=torch.float32).pin_memory()
         self.out_host = torch.zeros(self.B, self.d, dtype=torch.float32).pin_memory()
+        # tcgen05 score path: bf16 raw keys, d_h 128, head pairs, R_pad in 64..256
+        self.tc_layers = []
+        for li, L in enumerate(fused.layers):
+            K = cache._stores[li][0]
+            ok = (fused.dtype == "bfloat16" and K.bits == FP_BITS and self.dh == 128
+                  and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
+            if score_kernel == "tcgen05" and not ok:
+                raise ValidationError(f"layer {li}: shape not supported by the tcgen05 score kernel")
+            self.tc_layers.append(ok and score_kernel != "simt")
+        self.uw_bf = None
+        self.rope_tab = None
+        if any(self.tc_layers):
+            self.uw_bf = torch.zeros(self.B * self.n * 128 * rk, dtype=torch.bfloat16, device=dev)
+            nf = _lib.call("palu_rope_table_floats", self.dh // 2, self.cap)
+            self.rope_tab = torch.zeros(nf, dtype=torch.float32, device=dev)
+            _lib.call("palu_rope_table", _ptr(fused.theta_dev), self.dh // 2, self.cap,
+                      _ptr(self.rope_tab), _stream())
         self.use_graph = use_graph
         self.graph = None
         self.eager_steps = 0
@@ -455,11 +476,18 @@ class _Session:
         _lib.call("palu_latent_append", code, V.bits, yp + 4 * (d + sk_sum), B, self.n1, V.G,
                   _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev), _ptr(V.rows), _ptr(V.scales),
                   _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64), V.r_pad, V.cap, _ptr(self.t_dev), st)
-        _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
-                  _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw), 0, st)
-        _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B, n,
-                  dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),
-                  _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+        if self.tc_layers[li]:
+            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
+                      _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw_bf), 1, st)
+            _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
+                      n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
+                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+        else:
+            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
+                      _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw), 0, st)
+            _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps),
+                      B, n, dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),
+                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
         _lib.call("palu_softmax_value", code, V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B,
                   n, L.s_v, V.G, V.r_pad, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), V.cap,
                   _ptr(self.logits), self.ld_logits, _ptr(self.t_dev), self.n_chunks,
@@ -520,9 +548,11 @@ class _Session:
         self.graph.replay()
 
 
-def _session(fused, cache, score_kernel="auto") -> _Session:
+def _session(fused, cache, score_kernel=None) -> _Session:
     s = cache._session
-    if s is None or s.fused is not fused or s.cap != cache.capacity:
+    score_kernel = score_kernel or getattr(cache, "score_kernel", "auto")
+    if (s is None or s.fused is not fused or s.cap != cache.capacity
+            or s.score_kernel != score_kernel):
         s = _Session(fused, cache, score_kernel=score_kernel)
         cache._session = s
     return s

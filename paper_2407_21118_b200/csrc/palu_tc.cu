@@ -1,13 +1,334 @@
-// tcgen05 (sm_100a) RoPE score kernel -- placeholder until the tensor-core
-// path lands; the RoPE tables are final.
+// tcgen05 (sm_100a) RoPE score kernel: online key reconstruction on the
+// 5th-gen tensor cores with TMA-staged latents and a TMEM accumulator.
+//
+// Restates attention.py:433-444 (palu_decode_step_rope, per group and token
+// tile: K_tile = H_tile @ B_g, RoPE at absolute positions, q . k / sqrt(d_h))
+// in the query-absorbed form of palu_query_absorb:
+//
+//   logit[t, head] = sum_j cos(t th_j) (H_t . u_j) + sin(t th_j) (H_t . w_j)
+//
+// so the dense contraction is one GEMM per (sequence, group, head pair):
+//   ACC[128 tokens x 256] = H[128 x R] (smem, TMA, 128B swizzle)
+//                          x UW[256 x R]^T (smem, resident for the CTA)
+// accumulated in TMEM (2 x 256 columns, double buffered across tiles), and
+// the RoPE + q-dot collapses to a cos/sin-weighted row reduction in the
+// epilogue (tcgen05.ld 32x32b: one thread = one token).
+//
+// Warp roles (320 threads): warp 0 TMA producer, warp 1 MMA issuer + TMEM
+// owner, warps 2..9 epilogue (warp w reads TMEM lane quarter w % 4 and the
+// pair half (w - 2) / 4 of the 64 RoPE frequencies).
+#include <cuda.h>
 #include <math.h>
 
 #include "palu_common.cuh"
 
 namespace palu {
+namespace tc {
 
-// tile bases: cos/sin(t0 * th_j) for t0 = 128 * tile, fp64 angle reduction;
-// offsets: cos/sin(delta * th_j) for delta in [0, 128).
+constexpr int TILE_M = 128;    // tokens per tile = TMEM lanes
+constexpr int N_CTA = 256;     // accumulator columns: 2 heads x (64 u + 64 w)
+constexpr int KB = 64;         // bf16 per 128-byte swizzled row
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+constexpr int H_STAGE_BYTES = TILE_M * 128;  // 16 KB per (tile, k-block)
+constexpr int UW_KB_BYTES = N_CTA * 128;     // 32 KB per k-block
+constexpr int SMEM_LIMIT = 232448;           // 227 KB opt-in
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// ---- mbarrier -------------------------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_try_wait(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait(a, parity)) {
+  }
+}
+
+// ---- TMA --------------------------------------------------------------------
+__device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                            int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
+}
+
+// ---- tcgen05 ---------------------------------------------------------------
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+// smem matrix descriptor: K-major, 128B swizzle, 8-row core groups 1024 B apart
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;            // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;  // SBO
+  d |= (uint64_t)1 << 46;            // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;            // SWIZZLE_128B
+  return d;
+}
+// instruction descriptor: D f32, A/B bf16, K-major both, M=128, N=256
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N_CTA >> 3) << 17) |
+                           ((uint32_t)(TILE_M >> 4) << 24);
+
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_wait_ld() {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Params {
+  int n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
+  const float2* rope_tab;  // [n_tab + 128][64]
+  const int* t_dev;
+  float* logits;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
+                     const __grid_constant__ CUtensorMap map_uw, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int kblocks = p.R_pad / KB;
+  uint8_t* s_uw = smem;                                  // kblocks x 32 KB
+  uint8_t* s_h = smem + kblocks * UW_KB_BYTES;           // stages x 16 KB
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + p.stages * H_STAGE_BYTES);
+  uint64_t* full = bars;                                 // [stages]
+  uint64_t* empty = bars + p.stages;                     // [stages]
+  uint64_t* tfull = bars + 2 * p.stages;                 // [2]
+  uint64_t* tempty = tfull + 2;                          // [2]
+  uint64_t* uw_full = tempty + 2;                        // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_full + 1);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 acc][2 heads][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = blockIdx.y;  // head pair over all groups
+  const int b = blockIdx.z;
+  const int pairs_per_group = p.s_k / 2;
+  const int g = pair / pairs_per_group;
+  const int pair_in_g = pair - g * pairs_per_group;
+  const int T_rows = *p.t_dev + 1;
+  const int n_tiles = (T_rows + TILE_M - 1) / TILE_M;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&map_h);
+    prefetch_map(&map_uw);
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPI_WARPS);
+    }
+    mbar_init(uw_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer ----------------
+      const int uw_row = ((b * p.G + g) * p.s_k) * 128 + pair_in_g * N_CTA;
+      mbar_expect_tx(uw_full, kblocks * UW_KB_BYTES);
+      for (int kb = 0; kb < kblocks; ++kb)
+        tma_load_2d(&map_uw, uw_full, s_uw + kb * UW_KB_BYTES, kb * KB, uw_row);
+      const int h_row0 = (b * p.G + g) * p.T_cap;
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], H_STAGE_BYTES);
+          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB,
+                      h_row0 + tile * TILE_M);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer ----------------
+      mbar_wait(uw_full, 0);
+      fence_after();
+      const uint32_t uw_addr = smem_u32(s_uw);
+      const uint32_t h_addr = smem_u32(s_h);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+        const int acc = it & 1;
+        const uint32_t acc_phase = (it >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        const uint32_t d_tmem = tmem_base + acc * N_CTA;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t a0 = h_addr + stage * H_STAGE_BYTES;
+          const uint32_t b0 = uw_addr + kb * UW_KB_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < KB / 16; ++kk)
+            umma_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
+          umma_commit(&empty[stage]);
+          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+        }
+        umma_commit(&tfull[acc]);
+      }
+    }
+  } else {
+    // ---------------- epilogue: cos/sin-weighted row reduction ----------------
+    const int q = warp & 3;          // TMEM lane quarter
+    const int jh = (warp - 2) >> 2;  // which 32 of the 64 frequencies
+    const int delta = q * 32 + lane; // token row inside the tile
+    float cd[32], sd[32];
+    {
+      const float2* off = p.rope_tab + (size_t)(p.n_tab + delta) * 64 + jh * 32;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float2 v = off[j];
+        cd[j] = v.x;
+        sd[j] = v.y;
+      }
+    }
+    const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    int it = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const uint32_t acc_phase = (it >> 1) & 1;
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      const float2* base = p.rope_tab + (size_t)tile * 64 + jh * 32;
+      float v0 = 0.f, v1 = 0.f;
+#pragma unroll
+      for (int jc = 0; jc < 2; ++jc) {
+        float c[16], s[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float2 bs = base[jc * 16 + j];
+          const float cdj = cd[jc * 16 + j], sdj = sd[jc * 16 + j];
+          c[j] = bs.x * cdj - bs.y * sdj;  // cos(t0 + delta)
+          s[j] = bs.y * cdj + bs.x * sdj;  // sin(t0 + delta)
+        }
+#pragma unroll
+        for (int hp = 0; hp < 2; ++hp) {
+          float u[16], w[16];
+          const uint32_t col = acc * N_CTA + hp * 128 + jh * 32 + jc * 16;
+          tmem_ld16(lane_base + col, u);
+          tmem_ld16(lane_base + col + 64, w);
+          tmem_wait_ld();
+          float acc_v = 0.f;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc_v = fmaf(c[j], u[j], fmaf(s[j], w[j], acc_v));
+          if (hp == 0) v0 += acc_v; else v1 += acc_v;
+        }
+      }
+      float* r = red + acc * 2 * TILE_M;
+      if (jh == 1) {
+        r[delta] = v0;
+        r[TILE_M + delta] = v1;
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        named_bar_arrive(1 + acc, EPI_WARPS * 32);
+      } else {
+        named_bar_sync(1 + acc, EPI_WARPS * 32);
+        v0 += r[delta];
+        v1 += r[TILE_M + delta];
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        const int t = tile * TILE_M + delta;
+        if (t < T_rows) {
+          const int head0 = g * p.s_k + pair_in_g * 2;
+          float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
+          lg[0] = v0;
+          lg[p.ld_logits] = v1;
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// tile bases: cos/sin(t0 * th_j), t0 = 128 * row (fp64 angle reduction);
+// offsets: cos/sin(delta * th_j), delta in [0, 128).
 __global__ void rope_table_kernel(const double* __restrict__ theta, int half, int n_tiles,
                                   float2* __restrict__ tab) {
   const int total = (n_tiles + 128) * half;
@@ -20,6 +341,44 @@ __global__ void rope_table_kernel(const double* __restrict__ theta, int half, in
   }
 }
 
+// ---- host: tensor maps through the driver entry point (no -lcuda needed) ----
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  return fn;
+}
+
+static int make_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
+                       uint32_t box_cols, uint32_t box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {cols, rows};
+  const cuuint64_t strides[1] = {cols * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return PALU_ECUDA;
+  }
+  return PALU_OK;
+}
+
+}  // namespace tc
 }  // namespace palu
 
 using namespace palu;
@@ -34,8 +393,8 @@ size_t palu_rope_table_floats(int half, int T_cap) {
 int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, void* stream) {
   PALU_REQUIRE(half > 0 && T_cap > 0, "palu_rope_table: bad sizes");
   const int n_tiles = (T_cap + 127) / 128 + 1;
-  rope_table_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(theta, half, n_tiles,
-                                                           reinterpret_cast<float2*>(rope_tab));
+  tc::rope_table_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(theta, half, n_tiles,
+                                                               reinterpret_cast<float2*>(rope_tab));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -44,8 +403,59 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
                        void* stream) {
-  set_error("palu_rope_score_tc: tensor-core path not built yet");
-  return PALU_EUNSUPPORTED;
+  using namespace palu::tc;
+  (void)scales;
+  (void)zps;
+  if (bits != 16) {
+    set_error("palu_rope_score_tc: bits %d not on the tensor-core path yet", bits);
+    return PALU_EUNSUPPORTED;
+  }
+  if (R_pad % KB != 0 || R_pad > 256 || (s_k * 128) % N_CTA != 0 || G * s_k != n_heads) {
+    set_error("palu_rope_score_tc: unsupported shape (R_pad %d, s_k %d)", R_pad, s_k);
+    return PALU_EUNSUPPORTED;
+  }
+  PALU_REQUIRE(((uintptr_t)hk & 15) == 0 && ((uintptr_t)uw & 15) == 0, "tc: unaligned operands");
+  CUtensorMap map_h, map_uw;
+  int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  if (rc) return rc;
+  rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, N_CTA);
+  if (rc) return rc;
+  const int kblocks = R_pad / KB;
+  const int fixed = 1024 + kblocks * UW_KB_BYTES + 1024 + 2 * 2 * TILE_M * 4;
+  int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
+  if (stages > 8) stages = 8;
+  PALU_REQUIRE(stages >= 2, "tc: not enough shared memory");
+  const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_LIMIT));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int pairs = G * s_k / 2;
+  const int max_tiles = (T_cap + TILE_M - 1) / TILE_M;
+  int px = (sms + pairs * B - 1) / (pairs * B);
+  if (px < 1) px = 1;
+  if (px > max_tiles) px = max_tiles;
+  Params prm;
+  prm.n_heads = n_heads;
+  prm.s_k = s_k;
+  prm.G = G;
+  prm.R_pad = R_pad;
+  prm.T_cap = T_cap;
+  prm.ld_logits = ld_logits;
+  prm.n_tab = (T_cap + 127) / 128 + 1;
+  prm.stages = stages;
+  prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
+  prm.t_dev = t_dev;
+  prm.logits = logits;
+  dim3 grid(px, pairs, B);
+  rope_score_tc_kernel<<<grid, THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
+  PALU_LAUNCHED();
+  return PALU_OK;
 }
 
 }  // extern "C"

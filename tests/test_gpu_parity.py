@@ -220,3 +220,31 @@ def test_validation_errors(P, golden):
     cache2 = P.LatentKVCache(dec2, cfg2)
     with pytest.raises(P.ValidationError, match="rank mismatch"):
         P.palu_decode_step_rope(w, fused, cache2, np.zeros(16))
+
+
+@pytest.mark.parametrize("which", ["c1", "med_g4_r256", "med_g2_nonuniform"])
+def test_tcgen05_score_matches_simt_and_oracle(P, golden, which):
+    """The tcgen05 score kernel against the CUDA-core one (same bf16 cache)
+    and the whole step against the fp64 oracle."""
+    import torch
+    from paper_2407_21118_b200.harness import fill_cache_direct, set_cache_t
+    if which == "c1":
+        case = c1_case(golden("c1_step.npz"), "b16")
+    else:
+        g = golden("medium_step.npz")
+        case = medium_case(g, list(g["names"]).index(which))
+    w, dec, cfg = _to_types(P, [case["layer"]], case["n"], case["dh"], True, case["base"])
+    fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
+    out, logits = {}, {}
+    for sk in ("simt", "tcgen05"):
+        cache = P.LatentKVCache(dec, cfg, 16, dtype="bfloat16", capacity=case["T"] + 8,
+                                score_kernel=sk)
+        fill_cache_direct(cache, 0, case["x_rows"])
+        set_cache_t(cache, case["T"])
+        out[sk] = P.palu_decode_step_rope(w, fused, cache, case["x_t"])
+        sess = cache._session
+        assert any(sess.tc_layers) == (sk == "tcgen05")
+        logits[sk] = sess.logits[0, :, :case["T"] + 1].double().cpu().numpy()
+    e_log = rel_err(logits["tcgen05"], logits["simt"])
+    assert e_log < 5e-3, (e_log, logits["tcgen05"][0, :6], logits["simt"][0, :6])
+    assert rel_err(out["tcgen05"], case["out1"]) < TOL["bfloat16"]
