@@ -409,8 +409,6 @@ def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
 class _Session:
     """Device buffers + the per-step launch sequence for one (fused, cache) pair."""
 
-    N_CHUNKS_MIN = 32
-
     def __init__(self, fused: FusedWeights, cache: LatentKVCache, score_kernel: str = "auto",
                  use_graph: bool = True):
         torch = _torch()
@@ -429,7 +427,10 @@ class _Session:
         self.ld_logits = _round_up(self.cap, 4)
         self.logits = torch.zeros(self.B, self.n, self.ld_logits, dtype=torch.float32, device=dev)
         self.ctx = torch.zeros(self.B, self.ko, dtype=torch.float32, device=dev)
-        self.n_chunks = max(self.N_CHUNKS_MIN, -(-self.cap // 2048))
+        gv = max(len(L.value_ranks) for L in fused.layers)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        # split-T chunks: ~4 CTAs per SM for the value stream, <= 2048 tokens each
+        self.n_chunks = max(-(-4 * sms // (gv * self.B)), -(-self.cap // 2048), 1)
         ws = _lib.call("palu_softmax_value_workspace", self.B, self.n, rv, self.n_chunks)
         self.ws = torch.zeros(ws // 4 + 1, dtype=torch.float32, device=dev)
         self.t_dev = torch.tensor([cache.t], dtype=torch.int32, device=dev)

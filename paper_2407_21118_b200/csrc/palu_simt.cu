@@ -26,8 +26,8 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // one warp per 2 output rows, 16-byte non-allocating loads, 4 in flight per
 // lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
 // ---------------------------------------------------------------------------
-constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_ROWS_PER_WARP = 2;
+constexpr int GEMV_WARPS = 4;
+constexpr int GEMV_RPW = 4;  // rows per warp: 4 rows x 2 k-steps = 8 x 16 B loads in flight
 
 template <typename T, int MAXB>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
@@ -36,13 +36,17 @@ gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, 
   extern __shared__ float xs[];  // [MAXB][KC]
   using V = Vec16<T>;
   constexpr int VEC = V::N;
+  constexpr int STEP = 32 * VEC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = (blockIdx.x * GEMV_WARPS + warp) * GEMV_ROWS_PER_WARP;
-  float acc[GEMV_ROWS_PER_WARP][MAXB];
+  const int row0 = (blockIdx.x * GEMV_WARPS + warp) * GEMV_RPW;
+  float acc[GEMV_RPW][MAXB];
 #pragma unroll
-  for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r)
+  for (int r = 0; r < GEMV_RPW; ++r)
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) acc[r][b] = 0.f;
+  const T* wr[GEMV_RPW];
+#pragma unroll
+  for (int r = 0; r < GEMV_RPW; ++r) wr[r] = W + (size_t)min(row0 + r, N - 1) * K;
 
   for (int k0 = 0; k0 < K; k0 += KC) {
     const int kc = min(KC, K - k0);
@@ -52,46 +56,49 @@ gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, 
       xs[b * KC + k] = x[(size_t)b * ldx + k0 + k];
     }
     __syncthreads();
+    if (row0 >= N) continue;
+    for (int k = lane * VEC; k < kc; k += 2 * STEP) {
+      const bool two = k + STEP < kc;
+      uint4 v[2][GEMV_RPW];
 #pragma unroll
-    for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r) {
-      const int row = row0 + r;
-      if (row >= N) break;
-      const T* wr = W + (size_t)row * K + k0;
-      int k = lane * VEC;
-      for (; k + 3 * 32 * VEC < kc; k += 4 * 32 * VEC) {
-        uint4 v[4];
+      for (int r = 0; r < GEMV_RPW; ++r) {
+        v[0][r] = ldg_stream(wr[r] + k0 + k);
+        if (two) v[1][r] = ldg_stream(wr[r] + k0 + k + STEP);
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = ldg_stream(wr + k + u * 32 * VEC);
+      for (int u = 0; u < 2; ++u) {
+        if (u == 1 && !two) break;
+        const int kk = k + u * STEP;
+        float xv[MAXB][VEC];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int b = 0; b < MAXB; ++b) {
+          if (b < B) {
+            const float4* xp = reinterpret_cast<const float4*>(xs + b * KC + kk);
+#pragma unroll
+            for (int e4 = 0; e4 < VEC / 4; ++e4) {
+              const float4 t4 = xp[e4];
+              xv[b][4 * e4] = t4.x; xv[b][4 * e4 + 1] = t4.y;
+              xv[b][4 * e4 + 2] = t4.z; xv[b][4 * e4 + 3] = t4.w;
+            }
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < GEMV_RPW; ++r) {
           float wf[VEC];
-          V::unpack(v[u], wf);
-          const int kk = k + u * 32 * VEC;
+          V::unpack(v[u][r], wf);
 #pragma unroll
           for (int b = 0; b < MAXB; ++b) {
             if (b < B) {
 #pragma unroll
-              for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xs[b * KC + kk + e], acc[r][b]);
+              for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xv[b][e], acc[r][b]);
             }
-          }
-        }
-      }
-      for (; k < kc; k += 32 * VEC) {
-        uint4 v = ldg_stream(wr + k);
-        float wf[VEC];
-        V::unpack(v, wf);
-#pragma unroll
-        for (int b = 0; b < MAXB; ++b) {
-          if (b < B) {
-#pragma unroll
-            for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xs[b * KC + k + e], acc[r][b]);
           }
         }
       }
     }
   }
 #pragma unroll
-  for (int r = 0; r < GEMV_ROWS_PER_WARP; ++r) {
+  for (int r = 0; r < GEMV_RPW; ++r) {
     const int row = row0 + r;
 #pragma unroll
     for (int b = 0; b < MAXB; ++b) {
@@ -108,10 +115,10 @@ template <typename T, int MAXB>
 static int launch_gemv(const T* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
                        int acc, cudaStream_t st) {
   int KC = K;
-  const int cap = (48 * 1024) / (4 * MAXB);
+  const int cap = (32 * 1024) / (4 * MAXB);
   if (KC > cap) KC = (cap / 256) * 256;
   const size_t smem = (size_t)MAXB * KC * sizeof(float);
-  const int rows_per_cta = GEMV_WARPS * GEMV_ROWS_PER_WARP;
+  const int rows_per_cta = GEMV_WARPS * GEMV_RPW;
   dim3 grid((N + rows_per_cta - 1) / rows_per_cta);
   gemv_kernel<T, MAXB><<<grid, GEMV_WARPS * 32, smem, st>>>(W, N, K, x, B, ldx, y, ldy, acc, KC);
   PALU_LAUNCHED();
@@ -273,10 +280,14 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
                                     const double* __restrict__ theta, float scale,
                                     const int* __restrict__ t_dev, void* __restrict__ uw,
                                     int layout) {
-  extern __shared__ float qr[];  // [dh] rotated query
-  const int i = blockIdx.x, b = blockIdx.y;
+  // grid (n_heads, ceil(R_pad / 32), B): one head, 32 rank rows per CTA
+  extern __shared__ float qa_sm[];  // qr[dh] then bs[32][dh]
+  float* qr = qa_sm;
+  float* bs = qa_sm + dh;
+  const int i = blockIdx.x, k0 = blockIdx.y * 32, b = blockIdx.z;
   const int half = dh / 2;
   const int g = i / s_k, p = i - g * s_k;
+  const int nk = min(32, R_pad - k0);
   const double pos = (double)(*t_dev);
   const float* qh = q + (size_t)b * ld_q + (size_t)i * dh;
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
@@ -286,33 +297,30 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
     qr[j] = (float)(lo * cs - hi * sn);
     qr[j + half] = (float)(lo * sn + hi * cs);
   }
-  __syncthreads();
   const int width = s_k * dh;
-  const T* bg = bk + (size_t)g * R_pad * width + (size_t)p * dh;
+  const T* bg = bk + ((size_t)g * R_pad + k0) * width + (size_t)p * dh;
+  for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
+    const int kk = idx / dh, c = idx - kk * dh;
+    bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
+  }
+  __syncthreads();
   if (layout == 0) {
-    float* out = reinterpret_cast<float*>(uw) + ((size_t)b * n_heads + i) * R_pad * dh;
-    const int lanes_j = half < (int)blockDim.x ? half : (int)blockDim.x;
-    const int kstep = blockDim.x / lanes_j;
-    const int j0 = threadIdx.x % lanes_j, kk = threadIdx.x / lanes_j;
-    if (kk >= kstep) return;
-    for (int k = kk; k < R_pad; k += kstep) {
-      for (int j = j0; j < half; j += lanes_j) {
-        const float b1 = to_f(bg[(size_t)k * width + j]);
-        const float b2 = to_f(bg[(size_t)k * width + j + half]);
-        out[(size_t)k * dh + j] = scale * (qr[j] * b1 + qr[j + half] * b2);
-        out[(size_t)k * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
-      }
+    float* out = reinterpret_cast<float*>(uw) + (((size_t)b * n_heads + i) * R_pad + k0) * dh;
+    for (int idx = threadIdx.x; idx < nk * half; idx += blockDim.x) {
+      const int kk = idx / half, j = idx - kk * half;
+      const float b1 = bs[kk * dh + j], b2 = bs[kk * dh + j + half];
+      out[(size_t)kk * dh + j] = scale * (qr[j] * b1 + qr[j + half] * b2);
+      out[(size_t)kk * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
     }
   } else {
     // bf16 [B][G][s_k*dh][R_pad]: row n = p*dh + c, c < half -> u_c, else w_{c-half}
-    bf16* out = reinterpret_cast<bf16*>(uw) + (((size_t)b * (n_heads / s_k) + g) * width +
-                                              (size_t)p * dh) * R_pad;
-    for (int idx = threadIdx.x; idx < half * R_pad; idx += blockDim.x) {
-      const int j = idx / R_pad, k = idx - j * R_pad;
-      const float b1 = to_f(bg[(size_t)k * width + j]);
-      const float b2 = to_f(bg[(size_t)k * width + j + half]);
-      out[(size_t)j * R_pad + k] = __float2bfloat16_rn(scale * (qr[j] * b1 + qr[j + half] * b2));
-      out[(size_t)(j + half) * R_pad + k] =
+    bf16* out = reinterpret_cast<bf16*>(uw) +
+                (((size_t)b * (n_heads / s_k) + g) * width + (size_t)p * dh) * R_pad + k0;
+    for (int idx = threadIdx.x; idx < half * nk; idx += blockDim.x) {
+      const int j = idx / nk, kk = idx - j * nk;
+      const float b1 = bs[kk * dh + j], b2 = bs[kk * dh + j + half];
+      out[(size_t)j * R_pad + kk] = __float2bfloat16_rn(scale * (qr[j] * b1 + qr[j + half] * b2));
+      out[(size_t)(j + half) * R_pad + kk] =
           __float2bfloat16_rn(scale * (qr[j + half] * b1 - qr[j] * b2));
     }
   }
@@ -460,7 +468,7 @@ __global__ void rope_score_generic_kernel(const void* __restrict__ hk, const flo
 // ---------------------------------------------------------------------------
 constexpr int SV_THREADS = 256;
 constexpr int SV_HP = 4;           // heads per pass
-constexpr int SV_MAX_CHUNK = 4096;  // tokens per chunk cap (smem)
+constexpr int SV_MAX_CHUNK = 8192;  // tokens per chunk cap (smem)
 
 struct SvPartial {
   float* m;    // [B][n][NC]
@@ -477,114 +485,162 @@ __host__ __device__ inline SvPartial sv_carve(void* ws, int B, int n, int R_pad,
   return p;
 }
 
+// Streaming value pass.  A "segment" is what one lane loads per row: 16 B of
+// raw storage (8 bf16 / 4 fp32) or one 4-byte word of packed codes.  Lr
+// lanes cover a row (NSEG segments each), a warp covers 32/Lr rows, 8 warps
+// stream the chunk with 4 rows in flight per lane.  Quantised rows use
+// ctx = sum_t (p_t s_t) code_t - sum_t p_t s_t z_t (the z term per head is
+// accumulated once in the softmax pass).
 template <typename T, int BITS>
+struct SvSeg {
+  static constexpr bool RAW = BITS == 16;
+  static constexpr int BYTES = RAW ? 16 : 4;
+  static constexpr int COLV = RAW ? 16 / (int)sizeof(T) : 32 / BITS;
+  static __device__ __forceinline__ void unpack(const uint4& v, float* f) {
+    if constexpr (RAW) {
+      Vec16<T>::unpack(v, f);
+    } else {
+      const uint32_t w = v.x;
+#pragma unroll
+      for (int e = 0; e < COLV; ++e) f[e] = (float)((w >> (e * BITS)) & ((1u << BITS) - 1u));
+    }
+  }
+  static __device__ __forceinline__ uint4 load(const uint8_t* p) {
+    if constexpr (RAW) {
+      return ldg_stream(p);
+    } else {
+      uint4 r;
+      r.x = __ldg(reinterpret_cast<const uint32_t*>(p));
+      r.y = r.z = r.w = 0;
+      return r;
+    }
+  }
+};
+
+template <typename T, int BITS, int NSEG>
 __global__ void __launch_bounds__(SV_THREADS)
 softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restrict__ scales,
                              const float* __restrict__ zps, int n_heads, int s_v, int G, int R_pad,
                              int T_cap, const float* __restrict__ logits, int ld_logits,
                              const int* __restrict__ t_dev, int NC, SvPartial part) {
-  extern __shared__ float sv_sm[];  // ps[SV_HP][chunk] then red[...]
+  using Seg = SvSeg<T, BITS>;
+  constexpr int COLV = Seg::COLV;
+  constexpr int UNR = 4;
+  extern __shared__ float sv_sm[];  // ps[SV_HP][clen] | later red[8][SV_HP][R_pad]
+  __shared__ float zsum[SV_HP];
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int T_rows = *t_dev + 1;
   int clen = (T_rows + NC - 1) / NC;
   clen = (clen + 7) & ~7;
   const int c0 = c * clen;
   const int c1 = min(T_rows, c0 + clen);
-  const int tid = threadIdx.x;
-  float* ps = sv_sm;                       // [SV_HP][clen]
-  float* red = sv_sm + SV_HP * clen;       // [SV_THREADS/32 * 2]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  float* ps = sv_sm;
   const size_t tok_base = ((size_t)b * G + g) * T_cap;
-
-  // thread -> (row lane group, column segment): COLV columns per thread
-  constexpr int COLV = (BITS == 16) ? Vec16<T>::N : 8;
-  const int tpr = R_pad / COLV;               // threads per token row
-  const int rows_par = SV_THREADS / tpr;      // token rows in parallel (>= 1)
-  const int my_row = tid / tpr, my_seg = tid - my_row * tpr;
-  float* accred = red + 2 * (SV_THREADS / 32);  // [rows_par][SV_HP][R_pad]
+  const int row_bytes = Seg::RAW ? R_pad * (int)sizeof(T) : R_pad * BITS / 8;
+  const int segs = row_bytes / Seg::BYTES;
+  const int Lr = segs / NSEG;            // lanes per row (power of two <= 32)
+  const int RW = 32 / Lr;                // rows per warp
+  const int rs = lane / Lr, sb = lane - rs * Lr;
+  const uint8_t* hvb = reinterpret_cast<const uint8_t*>(hv);
 
   for (int p0 = 0; p0 < s_v; p0 += SV_HP) {
     const int hp = min(SV_HP, s_v - p0);
     __syncthreads();
-    // (1) per-head chunk max and exp, sums
-    for (int hh = 0; hh < hp; ++hh) {
-      const int head = g * s_v + p0 + hh;
+    // (1) one warp per head: chunk max, exp (x scale when quantised), sums
+    if (warp < hp) {
+      const int head = g * s_v + p0 + warp;
       const float* lg = logits + ((size_t)b * n_heads + head) * ld_logits;
       float m = -INFINITY;
-      for (int t = c0 + tid; t < c1; t += SV_THREADS) m = fmaxf(m, lg[t]);
+      for (int t = c0 + lane; t < c1; t += 32) m = fmaxf(m, lg[t]);
       m = warp_reduce(m, [](float a, float d) { return fmaxf(a, d); });
-      if ((tid & 31) == 0) red[tid >> 5] = m;
-      __syncthreads();
-      if (tid == 0) {
-        float mm = red[0];
-        for (int w = 1; w < SV_THREADS / 32; ++w) mm = fmaxf(mm, red[w]);
-        red[SV_THREADS / 32] = mm;
-      }
-      __syncthreads();
-      m = red[SV_THREADS / 32];
-      float l = 0.f;
-      for (int t = c0 + tid; t < c1; t += SV_THREADS) {
-        const float e = expf(lg[t] - m);
-        ps[hh * clen + (t - c0)] = e;
+      float l = 0.f, zs = 0.f;
+      for (int t = c0 + lane; t < c1; t += 32) {
+        float e = expf(lg[t] - m);
         l += e;
+        if constexpr (!Seg::RAW) {
+          const float sc = scales[tok_base + t];
+          zs = fmaf(e * sc, zps[tok_base + t], zs);
+          e *= sc;
+        }
+        ps[warp * clen + (t - c0)] = e;
       }
       l = warp_reduce(l, [](float a, float d) { return a + d; });
-      __syncthreads();
-      if ((tid & 31) == 0) red[tid >> 5] = l;
-      __syncthreads();
-      if (tid == 0) {
-        float ll = 0.f;
-        for (int w = 0; w < SV_THREADS / 32; ++w) ll += red[w];
+      zs = warp_reduce(zs, [](float a, float d) { return a + d; });
+      if (lane == 0) {
         const size_t pi = ((size_t)b * n_heads + head) * NC + c;
         part.m[pi] = (c0 < c1) ? m : -INFINITY;
-        part.l[pi] = (c0 < c1) ? ll : 0.f;
+        part.l[pi] = (c0 < c1) ? l : 0.f;
+        zsum[warp] = zs;
       }
-      __syncthreads();
     }
-    // (2) ctx partial: acc[h][e] = sum_t p_h[t] * H_v[t][seg*COLV + e]
-    float acc[SV_HP][COLV];
+    __syncthreads();
+    // (2) stream the chunk's rows
+    float acc[SV_HP][NSEG][COLV];
 #pragma unroll
     for (int h = 0; h < SV_HP; ++h)
 #pragma unroll
-      for (int e = 0; e < COLV; ++e) acc[h][e] = 0.f;
-    if (my_row < rows_par) {
-      for (int t = c0 + my_row; t < c1; t += rows_par) {
-        float hvv[COLV];
-        const size_t tok = tok_base + t;
-        if constexpr (BITS == 16) {
-          const T* row = reinterpret_cast<const T*>(hv) + tok * R_pad + my_seg * COLV;
-          Vec16<T>::unpack(ldg_stream(row), hvv);
-        } else {
-          const int rb = R_pad * BITS / 8;
-          const uint8_t* row = reinterpret_cast<const uint8_t*>(hv) + tok * rb + my_seg * BITS;
-          uint64_t bitsv = 0;
+      for (int q = 0; q < NSEG; ++q)
 #pragma unroll
-          for (int q = 0; q < BITS; ++q) bitsv |= uint64_t(row[q]) << (8 * q);
-          const float s = scales[tok], z = zps[tok];
+        for (int e = 0; e < COLV; ++e) acc[h][q][e] = 0.f;
+    const int row_step = 8 * RW;
+    for (int t = c0 + warp * RW + rs; t < c1; t += UNR * row_step) {
+      uint4 v[UNR][NSEG];
 #pragma unroll
-          for (int e = 0; e < COLV; ++e)
-            hvv[e] = ((float)((bitsv >> (e * BITS)) & ((1u << BITS) - 1u)) - z) * s;
+      for (int u = 0; u < UNR; ++u) {
+        const int tt = t + u * row_step;
+        if (tt < c1) {
+          const uint8_t* row = hvb + (tok_base + tt) * (size_t)row_bytes;
+#pragma unroll
+          for (int q = 0; q < NSEG; ++q) v[u][q] = Seg::load(row + (sb + q * Lr) * Seg::BYTES);
         }
+      }
 #pragma unroll
-        for (int h = 0; h < SV_HP; ++h) {
-          if (h < hp) {
-            const float pv = ps[h * clen + (t - c0)];
+      for (int u = 0; u < UNR; ++u) {
+        const int tt = t + u * row_step;
+        if (tt < c1) {
+          float pv[SV_HP];
 #pragma unroll
-            for (int e = 0; e < COLV; ++e) acc[h][e] = fmaf(pv, hvv[e], acc[h][e]);
+          for (int h = 0; h < SV_HP; ++h) pv[h] = (h < hp) ? ps[h * clen + (tt - c0)] : 0.f;
+#pragma unroll
+          for (int q = 0; q < NSEG; ++q) {
+            float f[COLV];
+            Seg::unpack(v[u][q], f);
+#pragma unroll
+            for (int h = 0; h < SV_HP; ++h)
+#pragma unroll
+              for (int e = 0; e < COLV; ++e) acc[h][q][e] = fmaf(pv[h], f[e], acc[h][q][e]);
           }
         }
       }
     }
-    // reduce the rows_par partial sums
-    if (my_row < rows_par) {
-      for (int h = 0; h < hp; ++h)
+    // (3) reduce: across row slots inside the warp, then across warps
+#pragma unroll
+    for (int h = 0; h < SV_HP; ++h)
+#pragma unroll
+      for (int q = 0; q < NSEG; ++q)
+#pragma unroll
         for (int e = 0; e < COLV; ++e)
-          accred[((size_t)my_row * SV_HP + h) * R_pad + my_seg * COLV + e] = acc[h][e];
+          for (int o = Lr; o < 32; o <<= 1)
+            acc[h][q][e] += __shfl_xor_sync(0xffffffffu, acc[h][q][e], o);
+    __syncthreads();  // ps no longer needed: reuse as red
+    float* red = sv_sm;
+    if (rs == 0) {
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h)
+#pragma unroll
+        for (int q = 0; q < NSEG; ++q)
+#pragma unroll
+          for (int e = 0; e < COLV; ++e)
+            red[((size_t)warp * SV_HP + h) * R_pad + (sb + q * Lr) * COLV + e] = acc[h][q][e];
     }
     __syncthreads();
     for (int idx = tid; idx < hp * R_pad; idx += SV_THREADS) {
       const int h = idx / R_pad, col = idx - h * R_pad;
       float v = 0.f;
-      for (int r = 0; r < rows_par; ++r) v += accred[((size_t)r * SV_HP + h) * R_pad + col];
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v += red[((size_t)w * SV_HP + h) * R_pad + col];
+      if constexpr (!Seg::RAW) v -= zsum[h];
       const int head = g * s_v + p0 + h;
       part.ctx[(((size_t)b * n_heads + head) * NC + c) * R_pad + col] = v;
     }
@@ -776,31 +832,53 @@ static void launch_score(const void* hk, const float* scales, const float* zps, 
   }
 }
 
-template <typename T, int BITS>
-static int launch_sv(const void* hv, const float* scales, const float* zps, int B, int n_heads,
-                     int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
-                     const float* logits, int ld_logits, const int* t_dev, int NC, SvPartial part,
-                     float* ctx, int ld_ctx, cudaStream_t st) {
-  constexpr int COLV = (BITS == 16) ? Vec16<T>::N : 8;
-  PALU_REQUIRE(R_pad % COLV == 0 && R_pad / COLV <= SV_THREADS,
-               "palu_softmax_value: R_pad=%d unsupported", R_pad);
+template <typename T, int BITS, int NSEG>
+static int launch_sv_n(const void* hv, const float* scales, const float* zps, int B, int n_heads,
+                       int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
+                       const float* logits, int ld_logits, const int* t_dev, int NC,
+                       SvPartial part, float* ctx, int ld_ctx, cudaStream_t st) {
   int clen = (T_cap + NC - 1) / NC;
   clen = (clen + 7) & ~7;
   PALU_REQUIRE(clen <= SV_MAX_CHUNK, "palu_softmax_value: raise n_chunks (chunk %d > %d)", clen,
                SV_MAX_CHUNK);
-  const int rows_par = SV_THREADS / (R_pad / COLV);
-  const size_t smem = sizeof(float) * ((size_t)SV_HP * clen + 2 * (SV_THREADS / 32) +
-                                       (size_t)rows_par * SV_HP * R_pad);
-  PALU_CK(cudaFuncSetAttribute(softmax_value_partial_kernel<T, BITS>,
-                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t ps = (size_t)SV_HP * clen, red = (size_t)8 * SV_HP * R_pad;
+  const size_t smem = sizeof(float) * (ps > red ? ps : red);
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(softmax_value_partial_kernel<T, BITS, NSEG>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
   dim3 grid(NC, G, B);
-  softmax_value_partial_kernel<T, BITS><<<grid, SV_THREADS, smem, st>>>(
+  softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_THREADS, smem, st>>>(
       hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, t_dev, NC, part);
   PALU_LAUNCHED();
   softmax_value_combine_kernel<<<dim3(n_heads, B), 128, NC * sizeof(float), st>>>(
       n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
   PALU_LAUNCHED();
   return PALU_OK;
+}
+
+template <typename T, int BITS>
+static int launch_sv(const void* hv, const float* scales, const float* zps, int B, int n_heads,
+                     int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
+                     const float* logits, int ld_logits, const int* t_dev, int NC, SvPartial part,
+                     float* ctx, int ld_ctx, cudaStream_t st) {
+  using Seg = SvSeg<T, BITS>;
+  const int row_bytes = Seg::RAW ? R_pad * (int)sizeof(T) : R_pad * BITS / 8;
+  PALU_REQUIRE(row_bytes % Seg::BYTES == 0, "palu_softmax_value: R_pad=%d unsupported", R_pad);
+  const int segs = row_bytes / Seg::BYTES;
+  const int nseg = segs <= 32 ? 1 : segs / 32;
+  const int lr = segs / nseg;
+  PALU_REQUIRE(segs % nseg == 0 && (lr & (lr - 1)) == 0 && lr <= 32 && nseg <= 4,
+               "palu_softmax_value: R_pad=%d unsupported (segments %d)", R_pad, segs);
+#define SVN(N_) return launch_sv_n<T, BITS, N_>(hv, scales, zps, B, n_heads, s_v, G, R_pad, ranks_v, \
+                                                 o_off, T_cap, logits, ld_logits, t_dev, NC, part,  \
+                                                 ctx, ld_ctx, st)
+  if (nseg == 1) SVN(1);
+  if (nseg == 2) SVN(2);
+  SVN(4);
+#undef SVN
 }
 
 }  // namespace palu
@@ -895,8 +973,8 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
   PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k,
                n_heads);
   PALU_REQUIRE(layout == 0 || layout == 1, "palu_query_absorb: layout must be 0 or 1");
-  dim3 grid(n_heads, B);
-  const size_t smem = head_dim * sizeof(float);
+  dim3 grid(n_heads, (R_pad + 31) / 32, B);
+  const size_t smem = (size_t)33 * head_dim * sizeof(float);
   if (dtype == PALU_DTYPE_BF16)
     query_absorb_kernel<bf16><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
                                                               (const bf16*)bk, R_pad, theta, scale,

@@ -137,7 +137,7 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
 }
 
 struct Params {
-  int n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
+  int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
@@ -158,17 +158,22 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   uint64_t* tfull = bars + 2 * p.stages;                 // [2]
   uint64_t* tempty = tfull + 2;                          // [2]
   uint64_t* uw_full = tempty + 2;                        // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_full + 1);
+  uint64_t* uw_empty = uw_full + 1;                      // [1]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_empty + 1);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 acc][2 heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int pair = blockIdx.y;  // head pair over all groups
-  const int b = blockIdx.z;
+  // Balanced persistent schedule: work item = (sequence b, head pair, tile),
+  // flattened; CTA c owns the contiguous range [i0, i1).  A range spans few
+  // (b, pair) blocks, so the resident UW operand is reloaded rarely.
   const int pairs_per_group = p.s_k / 2;
-  const int g = pair / pairs_per_group;
-  const int pair_in_g = pair - g * pairs_per_group;
+  const int pairs = p.G * pairs_per_group;
   const int T_rows = *p.t_dev + 1;
   const int n_tiles = (T_rows + TILE_M - 1) / TILE_M;
+  const int total = p.B * pairs * n_tiles;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int i0 = min(total, (int)blockIdx.x * per);
+  const int i1 = min(total, i0 + per);
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_h);
@@ -182,6 +187,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
       mbar_init(&tempty[a], EPI_WARPS);
     }
     mbar_init(uw_full, 1);
+    mbar_init(uw_empty, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -199,19 +205,26 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      const int uw_row = ((b * p.G + g) * p.s_k) * 128 + pair_in_g * N_CTA;
-      mbar_expect_tx(uw_full, kblocks * UW_KB_BYTES);
-      for (int kb = 0; kb < kblocks; ++kb)
-        tma_load_2d(&map_uw, uw_full, s_uw + kb * UW_KB_BYTES, kb * KB, uw_row);
-      const int h_row0 = (b * p.G + g) * p.T_cap;
-      int stage = 0;
+      int cur = -1, nloads = 0, stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+      for (int i = i0; i < i1; ++i) {
+        const int bp = i / n_tiles, tile = i - bp * n_tiles;
+        const int b = bp / pairs, pair = bp - b * pairs;
+        const int g = pair / pairs_per_group, pig = pair - g * pairs_per_group;
+        if (bp != cur) {
+          if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
+          const int uw_row = ((b * p.G + g) * p.s_k) * 128 + pig * N_CTA;
+          mbar_expect_tx(uw_full, kblocks * UW_KB_BYTES);
+          for (int kb = 0; kb < kblocks; ++kb)
+            tma_load_2d(&map_uw, uw_full, s_uw + kb * UW_KB_BYTES, kb * KB, uw_row);
+          ++nloads;
+          cur = bp;
+        }
+        const int h_row = (b * p.G + g) * p.T_cap + tile * TILE_M;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           mbar_expect_tx(&full[stage], H_STAGE_BYTES);
-          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB,
-                      h_row0 + tile * TILE_M);
+          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB, h_row);
           if (++stage == p.stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -219,14 +232,20 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer ----------------
-      mbar_wait(uw_full, 0);
-      fence_after();
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
-      int stage = 0;
+      int stage = 0, cur = -1, nloads = 0;
       uint32_t phase = 0;
       int it = 0;
-      for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+      for (int i = i0; i < i1; ++i, ++it) {
+        const int bp = i / n_tiles;
+        if (bp != cur) {
+          if (nloads > 0) umma_commit(uw_empty);  // frees UW once issued MMAs retire
+          mbar_wait(uw_full, nloads & 1);
+          fence_after();
+          ++nloads;
+          cur = bp;
+        }
         const int acc = it & 1;
         const uint32_t acc_phase = (it >> 1) & 1;
         mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -263,7 +282,10 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     int it = 0;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++it) {
+    for (int i = i0; i < i1; ++i, ++it) {
+      const int bp = i / n_tiles, tile = i - bp * n_tiles;
+      const int b = bp / pairs, pair = bp - b * pairs;
+      const int g = pair / pairs_per_group, pair_in_g = pair - g * pairs_per_group;
       const int acc = it & 1;
       const uint32_t acc_phase = (it >> 1) & 1;
       mbar_wait(&tfull[acc], acc_phase);
@@ -435,12 +457,8 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int pairs = G * s_k / 2;
-  const int max_tiles = (T_cap + TILE_M - 1) / TILE_M;
-  int px = (sms + pairs * B - 1) / (pairs * B);
-  if (px < 1) px = 1;
-  if (px > max_tiles) px = max_tiles;
   Params prm;
+  prm.B = B;
   prm.n_heads = n_heads;
   prm.s_k = s_k;
   prm.G = G;
@@ -452,7 +470,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
-  dim3 grid(px, pairs, B);
+  dim3 grid(sms);
   rope_score_tc_kernel<<<grid, THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
   PALU_LAUNCHED();
   return PALU_OK;
