@@ -117,15 +117,19 @@ int palu_rope_score(int dtype, int bits, const void* hk, const float* scales, co
                     int ld_logits, void* stream);
 
 /*
- * tcgen05 (sm_100a) RoPE score kernel, bf16 raw latents or 4/2-bit codes.
- * Same contract as palu_rope_score with uw in layout 1.  Requires d_h 128,
- * s_k*d_h a multiple of 256 and R_pad a multiple of 64 (<= 256);
+ * tcgen05 (sm_100a) RoPE score kernel, bf16 raw latents.  Same math as
+ * palu_rope_score with uw in layout 1.  The rank is split into
+ * palu_rope_score_tc_splits(s_k, R_pad) = KS slices (so the resident UW
+ * operand fits in shared memory); slice ks writes partial logits to plane
+ * ks (logits + ks * plane_stride) and palu_softmax_value adds the planes.
+ * Requires d_h 128, s_k in {2, 4}, R_pad a multiple of 64 (KS != 0);
  * returns PALU_EUNSUPPORTED otherwise.
  */
+int palu_rope_score_tc_splits(int s_k, int R_pad);
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
-                       void* stream);
+                       size_t plane_stride, void* stream);
 
 /* cos/sin tables for palu_rope_score_tc: [T_cap/128 + 1][64 pairs] tile bases
  * (fp64-reduced) followed by [128][64] in-tile offsets, float2 each. */
@@ -135,7 +139,8 @@ size_t palu_rope_table_floats(int half, int T_cap);
 /*
  * Softmax + fused value path (attention.py:445-446, _value_output :350-362
  * up to the wo_fused product):  ctx[b][o_off[i] + c] = sum_t' p_i[t'] H_v[g(i)][t'][c]
- * with p_i = softmax(logits[b][i][0..*t_dev]), split over n_chunks token
+ * with p_i = softmax(sum of the n_planes logit planes [b][i][0..*t_dev]),
+ * split over n_chunks token
  * chunks per (b, group) and merged in a fixed order (deterministic).
  * workspace: palu_softmax_value_workspace() bytes.
  */
@@ -143,8 +148,8 @@ size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks)
 int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales,
                        const float* zps, int B, int n_heads, int s_v, int G, int R_pad,
                        const int* ranks_v, const int* o_off, int T_cap, const float* logits,
-                       int ld_logits, const int* t_dev, int n_chunks, void* workspace,
-                       float* ctx, int ld_ctx, void* stream);
+                       int ld_logits, int n_planes, size_t plane_stride, const int* t_dev,
+                       int n_chunks, void* workspace, float* ctx, int ld_ctx, void* stream);
 
 /* *t_dev += 1 (cache.t += 1, attention.py:447) -- the last node of a step. */
 int palu_advance(int* t_dev, void* stream);

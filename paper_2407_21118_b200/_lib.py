@@ -36,12 +36,14 @@ SIGNATURES = {
     "palu_query_absorb": (i32, [i32, p, i32, i32, i32, i32, i32, p, i32, p, f32, p, p, i32, p]),
     "palu_rope_score": (i32, [i32, i32, p, p, p, i32, i32, i32, i32, i32, i32, i32, p, p, p, p,
                               i32, p]),
-    "palu_rope_score_tc": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, p]),
+    "palu_rope_score_tc_splits": (i32, [i32, i32]),
+    "palu_rope_score_tc": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, sz,
+                                 p]),
     "palu_rope_table": (i32, [p, i32, i32, p, p]),
     "palu_rope_table_floats": (sz, [i32, i32]),
     "palu_softmax_value_workspace": (sz, [i32, i32, i32, i32]),
-    "palu_softmax_value": (i32, [i32, i32, p, p, p, i32, i32, i32, i32, i32, p, p, i32, p, i32, p,
-                                 i32, p, p, i32, p]),
+    "palu_softmax_value": (i32, [i32, i32, p, p, p, i32, i32, i32, i32, i32, p, p, i32, p, i32, i32,
+                                 sz, p, i32, p, p, i32, p]),
     "palu_advance": (i32, [p, p]),
     "palu_dense_decode": (i32, [i32, p, i32, i32, i32, p, p, i32, p, p, i32, p, p, p]),
     "palu_dense_workspace": (sz, [i32, i32, i32, i32]),

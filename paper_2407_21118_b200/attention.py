@@ -425,7 +425,10 @@ class _Session:
         self.y = torch.zeros(self.B, self.n1, dtype=torch.float32, device=dev)
         self.uw = torch.zeros(self.B * self.n * rk * self.dh, dtype=torch.float32, device=dev)
         self.ld_logits = _round_up(self.cap, 4)
-        self.logits = torch.zeros(self.B, self.n, self.ld_logits, dtype=torch.float32, device=dev)
+        self.max_planes = 2  # rank splits of the tcgen05 score kernel
+        self.plane = self.B * self.n * self.ld_logits
+        self.logits = torch.zeros(self.max_planes, self.B, self.n, self.ld_logits,
+                                  dtype=torch.float32, device=dev)
         self.ctx = torch.zeros(self.B, self.ko, dtype=torch.float32, device=dev)
         gv = max(len(L.value_ranks) for L in fused.layers)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
@@ -438,13 +441,20 @@ class _Session:
         self.out_host = torch.zeros(self.B, self.d, dtype=torch.float32).pin_memory()
         # tcgen05 score path: bf16 raw keys, d_h 128, head pairs, R_pad in 64..256
         self.tc_layers = []
+        c = cache
         for li, L in enumerate(fused.layers):
             K = cache._stores[li][0]
             ok = (fused.dtype == "bfloat16" and K.bits == FP_BITS and self.dh == 128
                   and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
             if score_kernel == "tcgen05" and not ok:
                 raise ValidationError(f"layer {li}: shape not supported by the tcgen05 score kernel")
+            ks = _lib.call("palu_rope_score_tc_splits", L.s_k, K.r_pad) if ok else 0
+            ok = ok and 1 <= ks <= 2
+            if score_kernel == "tcgen05" and not ok:
+                raise ValidationError(f"layer {li}: rank {K.r_pad} not supported by the tcgen05 kernel")
             self.tc_layers.append(ok and score_kernel != "simt")
+        self.planes = [(_lib.call("palu_rope_score_tc_splits", L.s_k, c._stores[li][0].r_pad)
+                        if self.tc_layers[li] else 1) for li, L in enumerate(fused.layers)]
         self.uw_bf = None
         self.rope_tab = None
         if any(self.tc_layers):
@@ -482,7 +492,7 @@ class _Session:
                       _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw_bf), 1, st)
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
-                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, self.plane, st)
         else:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
                       _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw), 0, st)
@@ -491,7 +501,8 @@ class _Session:
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
         _lib.call("palu_softmax_value", code, V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B,
                   n, L.s_v, V.G, V.r_pad, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), V.cap,
-                  _ptr(self.logits), self.ld_logits, _ptr(self.t_dev), self.n_chunks,
+                  _ptr(self.logits), self.ld_logits, self.planes[li], self.plane, _ptr(self.t_dev),
+                  self.n_chunks,
                   _ptr(self.ws), _ptr(self.ctx), self.ko, st)
         _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko, _ptr(x),
                   d, 0, st)

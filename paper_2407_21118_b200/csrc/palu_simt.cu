@@ -26,71 +26,45 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // one warp per 2 output rows, 16-byte non-allocating loads, 4 in flight per
 // lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
 // ---------------------------------------------------------------------------
-constexpr int GEMV_WARPS = 4;
-constexpr int GEMV_RPW = 4;  // rows per warp: 4 rows x 2 k-steps = 8 x 16 B loads in flight
+constexpr int GEMV_WARPS = 8;
+constexpr int GEMV_UNROLL = 8;  // 16-byte weight loads in flight per lane
 
 template <typename T, int MAXB>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
 gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, int B, int ldx,
-            float* __restrict__ y, int ldy, int accumulate, int KC) {
-  extern __shared__ float xs[];  // [MAXB][KC]
+            float* __restrict__ y, int ldy, int accumulate) {
   using V = Vec16<T>;
   constexpr int VEC = V::N;
   constexpr int STEP = 32 * VEC;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int row0 = (blockIdx.x * GEMV_WARPS + warp) * GEMV_RPW;
-  float acc[GEMV_RPW][MAXB];
+  const int row = blockIdx.x * GEMV_WARPS + warp;
+  if (row >= N) return;
+  const T* wr = W + (size_t)row * K;
+  float acc[MAXB];
 #pragma unroll
-  for (int r = 0; r < GEMV_RPW; ++r)
+  for (int b = 0; b < MAXB; ++b) acc[b] = 0.f;
+  for (int k = lane * VEC; k < K; k += GEMV_UNROLL * STEP) {
+    uint4 v[GEMV_UNROLL];
 #pragma unroll
-    for (int b = 0; b < MAXB; ++b) acc[r][b] = 0.f;
-  const T* wr[GEMV_RPW];
+    for (int u = 0; u < GEMV_UNROLL; ++u)
+      if (k + u * STEP < K) v[u] = ldg_stream(wr + k + u * STEP);
 #pragma unroll
-  for (int r = 0; r < GEMV_RPW; ++r) wr[r] = W + (size_t)min(row0 + r, N - 1) * K;
-
-  for (int k0 = 0; k0 < K; k0 += KC) {
-    const int kc = min(KC, K - k0);
-    __syncthreads();
-    for (int i = threadIdx.x; i < B * kc; i += blockDim.x) {
-      const int b = i / kc, k = i - b * kc;
-      xs[b * KC + k] = x[(size_t)b * ldx + k0 + k];
-    }
-    __syncthreads();
-    if (row0 >= N) continue;
-    for (int k = lane * VEC; k < kc; k += 2 * STEP) {
-      const bool two = k + STEP < kc;
-      uint4 v[2][GEMV_RPW];
-#pragma unroll
-      for (int r = 0; r < GEMV_RPW; ++r) {
-        v[0][r] = ldg_stream(wr[r] + k0 + k);
-        if (two) v[1][r] = ldg_stream(wr[r] + k0 + k + STEP);
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (u == 1 && !two) break;
-        const int kk = k + u * STEP;
-        float xv[MAXB][VEC];
+    for (int u = 0; u < GEMV_UNROLL; ++u) {
+      const int kk = k + u * STEP;
+      if (kk < K) {
+        float wf[VEC];
+        V::unpack(v[u], wf);
 #pragma unroll
         for (int b = 0; b < MAXB; ++b) {
           if (b < B) {
-            const float4* xp = reinterpret_cast<const float4*>(xs + b * KC + kk);
+            const float4* xp = reinterpret_cast<const float4*>(x + (size_t)b * ldx + kk);
 #pragma unroll
             for (int e4 = 0; e4 < VEC / 4; ++e4) {
-              const float4 t4 = xp[e4];
-              xv[b][4 * e4] = t4.x; xv[b][4 * e4 + 1] = t4.y;
-              xv[b][4 * e4 + 2] = t4.z; xv[b][4 * e4 + 3] = t4.w;
-            }
-          }
-        }
-#pragma unroll
-        for (int r = 0; r < GEMV_RPW; ++r) {
-          float wf[VEC];
-          V::unpack(v[u][r], wf);
-#pragma unroll
-          for (int b = 0; b < MAXB; ++b) {
-            if (b < B) {
-#pragma unroll
-              for (int e = 0; e < VEC; ++e) acc[r][b] = fmaf(wf[e], xv[b][e], acc[r][b]);
+              const float4 t4 = __ldg(xp + e4);
+              acc[b] = fmaf(wf[4 * e4], t4.x, acc[b]);
+              acc[b] = fmaf(wf[4 * e4 + 1], t4.y, acc[b]);
+              acc[b] = fmaf(wf[4 * e4 + 2], t4.z, acc[b]);
+              acc[b] = fmaf(wf[4 * e4 + 3], t4.w, acc[b]);
             }
           }
         }
@@ -98,15 +72,11 @@ gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, 
     }
   }
 #pragma unroll
-  for (int r = 0; r < GEMV_RPW; ++r) {
-    const int row = row0 + r;
-#pragma unroll
-    for (int b = 0; b < MAXB; ++b) {
-      float v = warp_reduce(acc[r][b], [](float a, float c) { return a + c; });
-      if (lane == 0 && row < N && b < B) {
-        float* dst = y + (size_t)b * ldy + row;
-        *dst = accumulate ? *dst + v : v;
-      }
+  for (int b = 0; b < MAXB; ++b) {
+    const float v = warp_reduce(acc[b], [](float a, float c) { return a + c; });
+    if (lane == 0 && b < B) {
+      float* dst = y + (size_t)b * ldy + row;
+      *dst = accumulate ? *dst + v : v;
     }
   }
 }
@@ -114,13 +84,8 @@ gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, 
 template <typename T, int MAXB>
 static int launch_gemv(const T* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
                        int acc, cudaStream_t st) {
-  int KC = K;
-  const int cap = (32 * 1024) / (4 * MAXB);
-  if (KC > cap) KC = (cap / 256) * 256;
-  const size_t smem = (size_t)MAXB * KC * sizeof(float);
-  const int rows_per_cta = GEMV_WARPS * GEMV_RPW;
-  dim3 grid((N + rows_per_cta - 1) / rows_per_cta);
-  gemv_kernel<T, MAXB><<<grid, GEMV_WARPS * 32, smem, st>>>(W, N, K, x, B, ldx, y, ldy, acc, KC);
+  dim3 grid((N + GEMV_WARPS - 1) / GEMV_WARPS);
+  gemv_kernel<T, MAXB><<<grid, GEMV_WARPS * 32, 0, st>>>(W, N, K, x, B, ldx, y, ldy, acc);
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -494,11 +459,21 @@ __host__ __device__ inline SvPartial sv_carve(void* ws, int B, int n, int R_pad,
 template <typename T, int BITS>
 struct SvSeg {
   static constexpr bool RAW = BITS == 16;
-  static constexpr int BYTES = RAW ? 16 : 4;
-  static constexpr int COLV = RAW ? 16 / (int)sizeof(T) : 32 / BITS;
+  // raw: 16 B; packed: one 32-bit word, or 12 B (= 32 codes) for 3-bit rows
+  static constexpr int BYTES = RAW ? 16 : (BITS == 3 ? 12 : 4);
+  static constexpr int COLV = RAW ? 16 / (int)sizeof(T) : (BITS == 3 ? 32 : 32 / BITS);
   static __device__ __forceinline__ void unpack(const uint4& v, float* f) {
     if constexpr (RAW) {
       Vec16<T>::unpack(v, f);
+    } else if constexpr (BITS == 3) {
+      const uint32_t w[3] = {v.x, v.y, v.z};
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int bit = 3 * e, wi = bit >> 5, off = bit & 31;
+        uint32_t c = w[wi] >> off;
+        if (off > 29) c |= w[wi + 1] << (32 - off);
+        f[e] = (float)(c & 7u);
+      }
     } else {
       const uint32_t w = v.x;
 #pragma unroll
@@ -509,9 +484,12 @@ struct SvSeg {
     if constexpr (RAW) {
       return ldg_stream(p);
     } else {
+      const uint32_t* q = reinterpret_cast<const uint32_t*>(p);
       uint4 r;
-      r.x = __ldg(reinterpret_cast<const uint32_t*>(p));
-      r.y = r.z = r.w = 0;
+      r.x = __ldg(q);
+      r.y = BITS == 3 ? __ldg(q + 1) : 0u;
+      r.z = BITS == 3 ? __ldg(q + 2) : 0u;
+      r.w = 0u;
       return r;
     }
   }
@@ -522,7 +500,8 @@ __global__ void __launch_bounds__(SV_THREADS)
 softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restrict__ scales,
                              const float* __restrict__ zps, int n_heads, int s_v, int G, int R_pad,
                              int T_cap, const float* __restrict__ logits, int ld_logits,
-                             const int* __restrict__ t_dev, int NC, SvPartial part) {
+                             int n_planes, long long plane, const int* __restrict__ t_dev, int NC,
+                             SvPartial part) {
   using Seg = SvSeg<T, BITS>;
   constexpr int COLV = Seg::COLV;
   constexpr int UNR = 4;
@@ -551,12 +530,18 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
     if (warp < hp) {
       const int head = g * s_v + p0 + warp;
       const float* lg = logits + ((size_t)b * n_heads + head) * ld_logits;
+      // logits of every rank-split plane add up (palu_rope_score_tc)
       float m = -INFINITY;
-      for (int t = c0 + lane; t < c1; t += 32) m = fmaxf(m, lg[t]);
+      for (int t = c0 + lane; t < c1; t += 32) {
+        float v = lg[t];
+        for (int pl = 1; pl < n_planes; ++pl) v += lg[pl * plane + t];
+        ps[warp * clen + (t - c0)] = v;
+        m = fmaxf(m, v);
+      }
       m = warp_reduce(m, [](float a, float d) { return fmaxf(a, d); });
       float l = 0.f, zs = 0.f;
       for (int t = c0 + lane; t < c1; t += 32) {
-        float e = expf(lg[t] - m);
+        float e = expf(ps[warp * clen + (t - c0)] - m);
         l += e;
         if constexpr (!Seg::RAW) {
           const float sc = scales[tok_base + t];
@@ -651,34 +636,34 @@ __global__ void softmax_value_combine_kernel(int n_heads, int s_v, int R_pad,
                                              const int* __restrict__ ranks_v,
                                              const int* __restrict__ o_off, int NC, SvPartial part,
                                              float* __restrict__ ctx, int ld_ctx) {
-  extern __shared__ float wsm[];  // [NC] weights
+  // grid (n_heads, B, column blocks of 128): fixed-order merge of the chunks
+  extern __shared__ float wsm[];  // [NC] chunk weights
+  __shared__ float inv_l;
   const int head = blockIdx.x, b = blockIdx.y;
   const size_t base = ((size_t)b * n_heads + head) * NC;
-  __shared__ float Msh, Lsh;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
     float M = -INFINITY;
-    for (int c = 0; c < NC; ++c) M = fmaxf(M, part.m[base + c]);
+    for (int c = threadIdx.x; c < NC; c += 32) M = fmaxf(M, part.m[base + c]);
+    M = warp_reduce(M, [](float a, float d) { return fmaxf(a, d); });
     float L = 0.f;
-    for (int c = 0; c < NC; ++c) {
-      const float w = (part.l[base + c] > 0.f) ? expf(part.m[base + c] - M) : 0.f;
+    for (int c = threadIdx.x; c < NC; c += 32) {
+      const float l = part.l[base + c];
+      const float w = (l > 0.f) ? expf(part.m[base + c] - M) : 0.f;
       wsm[c] = w;
-      L += w * part.l[base + c];
+      L += w * l;
     }
-    Msh = M;
-    Lsh = L;
+    L = warp_reduce(L, [](float a, float d) { return a + d; });
+    if (threadIdx.x == 0) inv_l = 1.f / L;
   }
   __syncthreads();
-  const float invL = 1.f / Lsh;
   const int r = ranks_v[head / s_v];
-  float* dst = ctx + (size_t)b * ld_ctx + o_off[head];
-  for (int col = threadIdx.x; col < r; col += blockDim.x) {
-    float v = 0.f;
-    for (int c = 0; c < NC; ++c) {
-      const float w = wsm[c];
-      if (w != 0.f) v = fmaf(w, part.ctx[(base + c) * R_pad + col], v);
-    }
-    dst[col] = v * invL;
-  }
+  const int col = blockIdx.z * blockDim.x + threadIdx.x;
+  if (col >= r) return;
+  const float* src = part.ctx + base * R_pad + col;
+  float v = 0.f;
+#pragma unroll 4
+  for (int c = 0; c < NC; ++c) v = fmaf(wsm[c], src[(size_t)c * R_pad], v);
+  ctx[(size_t)b * ld_ctx + o_off[head] + col] = v * inv_l;
 }
 
 __global__ void advance_kernel(int* t_dev) { *t_dev += 1; }
@@ -835,8 +820,9 @@ static void launch_score(const void* hk, const float* scales, const float* zps, 
 template <typename T, int BITS, int NSEG>
 static int launch_sv_n(const void* hv, const float* scales, const float* zps, int B, int n_heads,
                        int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
-                       const float* logits, int ld_logits, const int* t_dev, int NC,
-                       SvPartial part, float* ctx, int ld_ctx, cudaStream_t st) {
+                       const float* logits, int ld_logits, int n_planes, long long plane,
+                       const int* t_dev, int NC, SvPartial part, float* ctx, int ld_ctx,
+                       cudaStream_t st) {
   int clen = (T_cap + NC - 1) / NC;
   clen = (clen + 7) & ~7;
   PALU_REQUIRE(clen <= SV_MAX_CHUNK, "palu_softmax_value: raise n_chunks (chunk %d > %d)", clen,
@@ -851,9 +837,11 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
   }
   dim3 grid(NC, G, B);
   softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_THREADS, smem, st>>>(
-      hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, t_dev, NC, part);
+      hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, n_planes, plane, t_dev, NC,
+      part);
   PALU_LAUNCHED();
-  softmax_value_combine_kernel<<<dim3(n_heads, B), 128, NC * sizeof(float), st>>>(
+  softmax_value_combine_kernel<<<dim3(n_heads, B, (R_pad + 127) / 128), 128, NC * sizeof(float),
+                                 st>>>(
       n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
   PALU_LAUNCHED();
   return PALU_OK;
@@ -862,8 +850,9 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
 template <typename T, int BITS>
 static int launch_sv(const void* hv, const float* scales, const float* zps, int B, int n_heads,
                      int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
-                     const float* logits, int ld_logits, const int* t_dev, int NC, SvPartial part,
-                     float* ctx, int ld_ctx, cudaStream_t st) {
+                     const float* logits, int ld_logits, int n_planes, long long plane,
+                     const int* t_dev, int NC, SvPartial part, float* ctx, int ld_ctx,
+                     cudaStream_t st) {
   using Seg = SvSeg<T, BITS>;
   const int row_bytes = Seg::RAW ? R_pad * (int)sizeof(T) : R_pad * BITS / 8;
   PALU_REQUIRE(row_bytes % Seg::BYTES == 0, "palu_softmax_value: R_pad=%d unsupported", R_pad);
@@ -873,8 +862,8 @@ static int launch_sv(const void* hv, const float* scales, const float* zps, int 
   PALU_REQUIRE(segs % nseg == 0 && (lr & (lr - 1)) == 0 && lr <= 32 && nseg <= 4,
                "palu_softmax_value: R_pad=%d unsupported (segments %d)", R_pad, segs);
 #define SVN(N_) return launch_sv_n<T, BITS, N_>(hv, scales, zps, B, n_heads, s_v, G, R_pad, ranks_v, \
-                                                 o_off, T_cap, logits, ld_logits, t_dev, NC, part,  \
-                                                 ctx, ld_ctx, st)
+                                                 o_off, T_cap, logits, ld_logits, n_planes, plane, \
+                                                 t_dev, NC, part, ctx, ld_ctx, st)
   if (nseg == 1) SVN(1);
   if (nseg == 2) SVN(2);
   SVN(4);
@@ -907,7 +896,8 @@ int palu_gemv(int dtype, const void* W, int N, int K, const float* x, int B, int
   PALU_REQUIRE(N > 0 && K > 0 && B > 0, "palu_gemv: bad sizes N=%d K=%d B=%d", N, K, B);
   const int vec = dtype == PALU_DTYPE_BF16 ? 8 : 4;
   PALU_REQUIRE(K % vec == 0, "palu_gemv: K=%d must be a multiple of %d", K, vec);
-  PALU_REQUIRE(((uintptr_t)W & 15) == 0, "palu_gemv: W must be 16-byte aligned");
+  PALU_REQUIRE(((uintptr_t)W & 15) == 0 && ((uintptr_t)x & 15) == 0 && ldx % 4 == 0,
+               "palu_gemv: W/x must be 16-byte aligned");
   if (dtype == PALU_DTYPE_BF16)
     return gemv_dispatch<bf16>((const bf16*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
   PALU_REQUIRE(dtype == PALU_DTYPE_F32, "palu_gemv: unknown dtype %d", dtype);
@@ -1017,15 +1007,17 @@ size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks)
 int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales, const float* zps,
                        int B, int n_heads, int s_v, int G, int R_pad, const int* ranks_v,
                        const int* o_off, int T_cap, const float* logits, int ld_logits,
-                       const int* t_dev, int n_chunks, void* workspace, float* ctx, int ld_ctx,
-                       void* stream) {
+                       int n_planes, size_t plane_stride, const int* t_dev, int n_chunks,
+                       void* workspace, float* ctx, int ld_ctx, void* stream) {
+  const long long plane = (long long)plane_stride;
+  PALU_REQUIRE(n_planes >= 1, "palu_softmax_value: n_planes must be >= 1");
   PALU_REQUIRE(G * s_v == n_heads, "palu_softmax_value: G*s_v != n_heads");
   PALU_REQUIRE(n_chunks >= 1, "palu_softmax_value: n_chunks must be >= 1");
   SvPartial part = sv_carve(workspace, B, n_heads, R_pad, n_chunks);
   cudaStream_t st = S(stream);
 #define SV(T_, B_) return launch_sv<T_, B_>(hv, scales, zps, B, n_heads, s_v, G, R_pad, ranks_v, \
-                                            o_off, T_cap, logits, ld_logits, t_dev, n_chunks,    \
-                                            part, ctx, ld_ctx, st)
+                                            o_off, T_cap, logits, ld_logits, n_planes, plane,    \
+                                            t_dev, n_chunks, part, ctx, ld_ctx, st)
   if (bits == 16) {
     if (dtype == PALU_DTYPE_BF16) SV(bf16, 16);
     SV(float, 16);

@@ -136,41 +136,62 @@ __device__ __forceinline__ void named_bar_arrive(int id, int n) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int BASE_RING = 4;       // tile-base cos/sin rows in flight
+constexpr int BASE_BYTES = 64 * 8; // 64 float2
+
 struct Params {
-  int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
+  int B, n_heads, s_k, G, R_pad, KS, T_cap, ld_logits, n_tab, stages;
+  long long plane;         // logits plane stride (one plane per rank split)
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
 };
 
+// Work item = (sequence b, key group g, rank split ks, 128-token tile),
+// flattened; CTA c owns [i0, i1).  Per item the CTA computes
+//   ACC_h[128 x 256] = H[tile, ks-th R/KS columns] x UW_h[256 x R/KS]^T
+// for each head pair h of the group (N_CTA = s_k * 128 = 256 or 512) and
+// writes the partial logits of its rank split; the softmax pass adds the
+// KS planes (the cos/sin epilogue is linear in ACC).  Splitting the rank
+// instead of the heads means every latent byte crosses L2 -> SM once.
 __global__ void __launch_bounds__(THREADS, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int kblocks = p.R_pad / KB;
-  uint8_t* s_uw = smem;                                  // kblocks x 32 KB
-  uint8_t* s_h = smem + kblocks * UW_KB_BYTES;           // stages x 16 KB
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + p.stages * H_STAGE_BYTES);
+  const int r_loc = p.R_pad / p.KS;
+  const int kblocks = r_loc / KB;
+  const int n_cta = p.s_k * 128;
+  const int halves = n_cta / N_CTA;
+  const int uw_kb_bytes = n_cta * 128;
+  uint8_t* s_uw = smem;                                  // kblocks x n_cta rows x 128 B
+  uint8_t* s_h = smem + kblocks * uw_kb_bytes;           // stages x 16 KB
+  float2* s_base = reinterpret_cast<float2*>(s_h + p.stages * H_STAGE_BYTES);  // ring
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_base + BASE_RING * 64);
   uint64_t* full = bars;                                 // [stages]
   uint64_t* empty = bars + p.stages;                     // [stages]
   uint64_t* tfull = bars + 2 * p.stages;                 // [2]
   uint64_t* tempty = tfull + 2;                          // [2]
   uint64_t* uw_full = tempty + 2;                        // [1]
   uint64_t* uw_empty = uw_full + 1;                      // [1]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_empty + 1);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 acc][2 heads][128]
+  uint64_t* bfull = uw_empty + 1;                        // [BASE_RING]
+  uint64_t* bempty = bfull + BASE_RING;                  // [BASE_RING]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + BASE_RING);
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // Balanced persistent schedule: work item = (sequence b, head pair, tile),
-  // flattened; CTA c owns the contiguous range [i0, i1).  A range spans few
-  // (b, pair) blocks, so the resident UW operand is reloaded rarely.
-  const int pairs_per_group = p.s_k / 2;
-  const int pairs = p.G * pairs_per_group;
   const int T_rows = *p.t_dev + 1;
   const int n_tiles = (T_rows + TILE_M - 1) / TILE_M;
-  const int total = p.B * pairs * n_tiles;
+  const int total = p.B * p.G * p.KS * n_tiles;
   const int per = (total + gridDim.x - 1) / gridDim.x;
   const int i0 = min(total, (int)blockIdx.x * per);
   const int i1 = min(total, i0 + per);
@@ -185,6 +206,10 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS);
+    }
+    for (int a = 0; a < BASE_RING; ++a) {
+      mbar_init(&bfull[a], 1);
+      mbar_init(&bempty[a], EPI_WARPS);
     }
     mbar_init(uw_full, 1);
     mbar_init(uw_empty, 1);
@@ -205,27 +230,31 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer ----------------
-      int cur = -1, nloads = 0, stage = 0;
-      uint32_t phase = 0;
-      for (int i = i0; i < i1; ++i) {
-        const int bp = i / n_tiles, tile = i - bp * n_tiles;
-        const int b = bp / pairs, pair = bp - b * pairs;
-        const int g = pair / pairs_per_group, pig = pair - g * pairs_per_group;
-        if (bp != cur) {
+      int cur = -1, nloads = 0, kc = 0, it = 0;
+      for (int i = i0; i < i1; ++i, ++it) {
+        const int bgk = i / n_tiles, tile = i - bgk * n_tiles;
+        const int bg = bgk / p.KS, ks = bgk - bg * p.KS;
+        if (bgk != cur) {
           if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
-          const int uw_row = ((b * p.G + g) * p.s_k) * 128 + pig * N_CTA;
-          mbar_expect_tx(uw_full, kblocks * UW_KB_BYTES);
+          mbar_expect_tx(uw_full, kblocks * uw_kb_bytes);
           for (int kb = 0; kb < kblocks; ++kb)
-            tma_load_2d(&map_uw, uw_full, s_uw + kb * UW_KB_BYTES, kb * KB, uw_row);
+            for (int h = 0; h < halves; ++h)
+              tma_load_2d(&map_uw, uw_full, s_uw + kb * uw_kb_bytes + h * UW_KB_BYTES,
+                          ks * r_loc + kb * KB, bg * n_cta + h * N_CTA);
           ++nloads;
-          cur = bp;
+          cur = bgk;
         }
-        const int h_row = (b * p.G + g) * p.T_cap + tile * TILE_M;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
+        const int bs = it % BASE_RING;
+        mbar_wait(&bempty[bs], ((it / BASE_RING) & 1) ^ 1);
+        mbar_expect_tx(&bfull[bs], BASE_BYTES);
+        bulk_load(s_base + bs * 64, p.rope_tab + (size_t)tile * 64, BASE_BYTES, &bfull[bs]);
+        const int h_row = bg * p.T_cap + tile * TILE_M;
+        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+          const int stage = kc % p.stages;
+          mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
           mbar_expect_tx(&full[stage], H_STAGE_BYTES);
-          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB, h_row);
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, ks * r_loc + kb * KB,
+                      h_row);
         }
       }
     }
@@ -234,35 +263,38 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
       // ---------------- MMA issuer ----------------
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
-      int stage = 0, cur = -1, nloads = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int i = i0; i < i1; ++i, ++it) {
-        const int bp = i / n_tiles;
-        if (bp != cur) {
+      int cur = -1, nloads = 0, kc = 0, unit = 0;
+      for (int i = i0; i < i1; ++i) {
+        const int bgk = i / n_tiles;
+        if (bgk != cur) {
           if (nloads > 0) umma_commit(uw_empty);  // frees UW once issued MMAs retire
           mbar_wait(uw_full, nloads & 1);
           fence_after();
           ++nloads;
-          cur = bp;
+          cur = bgk;
         }
-        const int acc = it & 1;
-        const uint32_t acc_phase = (it >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        fence_after();
-        const uint32_t d_tmem = tmem_base + acc * N_CTA;
-        for (int kb = 0; kb < kblocks; ++kb) {
-          mbar_wait(&full[stage], phase);
+        for (int h = 0; h < halves; ++h, ++unit) {
+          const int slot = unit & 1;
+          mbar_wait(&tempty[slot], ((unit >> 1) & 1) ^ 1);
           fence_after();
-          const uint32_t a0 = h_addr + stage * H_STAGE_BYTES;
-          const uint32_t b0 = uw_addr + kb * UW_KB_BYTES;
+          const uint32_t d_tmem = tmem_base + slot * N_CTA;
+          for (int kb = 0; kb < kblocks; ++kb) {
+            const int cnt = kc + kb;
+            const int stage = cnt % p.stages;
+            if (h == 0) {
+              mbar_wait(&full[stage], (cnt / p.stages) & 1);
+              fence_after();
+            }
+            const uint32_t a0 = h_addr + stage * H_STAGE_BYTES;
+            const uint32_t b0 = uw_addr + kb * uw_kb_bytes + h * UW_KB_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < KB / 16; ++kk)
-            umma_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
-          umma_commit(&empty[stage]);
-          if (++stage == p.stages) { stage = 0; phase ^= 1; }
+            for (int kk = 0; kk < KB / 16; ++kk)
+              umma_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
+            if (h == halves - 1) umma_commit(&empty[stage]);
+          }
+          umma_commit(&tfull[slot]);
         }
-        umma_commit(&tfull[acc]);
+        kc += kblocks;
       }
     }
   } else {
@@ -281,63 +313,69 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
       }
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
-    int it = 0;
+    int unit = 0, it = 0;
     for (int i = i0; i < i1; ++i, ++it) {
-      const int bp = i / n_tiles, tile = i - bp * n_tiles;
-      const int b = bp / pairs, pair = bp - b * pairs;
-      const int g = pair / pairs_per_group, pair_in_g = pair - g * pairs_per_group;
-      const int acc = it & 1;
-      const uint32_t acc_phase = (it >> 1) & 1;
-      mbar_wait(&tfull[acc], acc_phase);
-      fence_after();
-      const float2* base = p.rope_tab + (size_t)tile * 64 + jh * 32;
-      float v0 = 0.f, v1 = 0.f;
+      const int bgk = i / n_tiles, tile = i - bgk * n_tiles;
+      const int bg = bgk / p.KS, ks = bgk - bg * p.KS;
+      const int b = bg / p.G, g = bg - b * p.G;
+      const int bs = it % BASE_RING;
+      mbar_wait(&bfull[bs], (it / BASE_RING) & 1);
+      const float2* base = s_base + bs * 64 + jh * 32;
+      for (int h = 0; h < halves; ++h, ++unit) {
+        const int slot = unit & 1;
+        mbar_wait(&tfull[slot], (unit >> 1) & 1);
+        fence_after();
+        float v0 = 0.f, v1 = 0.f;
 #pragma unroll
-      for (int jc = 0; jc < 2; ++jc) {
-        float c[16], s[16];
+        for (int jc = 0; jc < 2; ++jc) {
+          float c[16], s[16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float2 bs = base[jc * 16 + j];
-          const float cdj = cd[jc * 16 + j], sdj = sd[jc * 16 + j];
-          c[j] = bs.x * cdj - bs.y * sdj;  // cos(t0 + delta)
-          s[j] = bs.y * cdj + bs.x * sdj;  // sin(t0 + delta)
+          for (int j = 0; j < 16; ++j) {
+            const float2 bsv = base[jc * 16 + j];
+            const float cdj = cd[jc * 16 + j], sdj = sd[jc * 16 + j];
+            c[j] = bsv.x * cdj - bsv.y * sdj;  // cos((t0 + delta) th_j)
+            s[j] = bsv.y * cdj + bsv.x * sdj;  // sin((t0 + delta) th_j)
+          }
+#pragma unroll
+          for (int hp = 0; hp < 2; ++hp) {
+            float u[16], w[16];
+            const uint32_t col = slot * N_CTA + hp * 128 + jh * 32 + jc * 16;
+            tmem_ld16(lane_base + col, u);
+            tmem_ld16(lane_base + col + 64, w);
+            tmem_wait_ld();
+            float acc_v = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc_v = fmaf(c[j], u[j], fmaf(s[j], w[j], acc_v));
+            if (hp == 0) v0 += acc_v; else v1 += acc_v;
+          }
         }
-#pragma unroll
-        for (int hp = 0; hp < 2; ++hp) {
-          float u[16], w[16];
-          const uint32_t col = acc * N_CTA + hp * 128 + jh * 32 + jc * 16;
-          tmem_ld16(lane_base + col, u);
-          tmem_ld16(lane_base + col + 64, w);
-          tmem_wait_ld();
-          float acc_v = 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc_v = fmaf(c[j], u[j], fmaf(s[j], w[j], acc_v));
-          if (hp == 0) v0 += acc_v; else v1 += acc_v;
+        float* r = red + slot * 2 * TILE_M;
+        if (jh == 1) {
+          r[delta] = v0;
+          r[TILE_M + delta] = v1;
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[slot]);
+          named_bar_arrive(1 + slot, EPI_WARPS * 32);
+        } else {
+          named_bar_sync(1 + slot, EPI_WARPS * 32);
+          v0 += r[delta];
+          v1 += r[TILE_M + delta];
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[slot]);
+          const int t = tile * TILE_M + delta;
+          if (t < T_rows) {
+            const int head0 = g * p.s_k + h * 2;
+            float* lg = p.logits + (size_t)ks * p.plane +
+                        ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
+            lg[0] = v0;
+            lg[p.ld_logits] = v1;
+          }
         }
       }
-      float* r = red + acc * 2 * TILE_M;
-      if (jh == 1) {
-        r[delta] = v0;
-        r[TILE_M + delta] = v1;
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        named_bar_arrive(1 + acc, EPI_WARPS * 32);
-      } else {
-        named_bar_sync(1 + acc, EPI_WARPS * 32);
-        v0 += r[delta];
-        v1 += r[TILE_M + delta];
-        fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[acc]);
-        const int t = tile * TILE_M + delta;
-        if (t < T_rows) {
-          const int head0 = g * p.s_k + pair_in_g * 2;
-          float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
-          lg[0] = v0;
-          lg[p.ld_logits] = v1;
-        }
-      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bempty[bs]);
     }
   }
   fence_before();
@@ -421,10 +459,20 @@ int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, v
   return PALU_OK;
 }
 
+int palu_rope_score_tc_splits(int s_k, int R_pad) {
+  using namespace palu::tc;
+  const int n = s_k * 128;
+  for (int ks = 1; ks <= 4; ks *= 2) {
+    if (R_pad % (ks * KB) != 0) break;
+    if ((size_t)n * (R_pad / ks) * 2 <= 128 * 1024) return ks;
+  }
+  return 0;
+}
+
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
-                       void* stream) {
+                       size_t plane_stride, void* stream) {
   using namespace palu::tc;
   (void)scales;
   (void)zps;
@@ -432,7 +480,8 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
     set_error("palu_rope_score_tc: bits %d not on the tensor-core path yet", bits);
     return PALU_EUNSUPPORTED;
   }
-  if (R_pad % KB != 0 || R_pad > 256 || (s_k * 128) % N_CTA != 0 || G * s_k != n_heads) {
+  const int KS = palu_rope_score_tc_splits(s_k, R_pad);
+  if (R_pad % KB != 0 || (s_k != 2 && s_k != 4) || G * s_k != n_heads || KS == 0) {
     set_error("palu_rope_score_tc: unsupported shape (R_pad %d, s_k %d)", R_pad, s_k);
     return PALU_EUNSUPPORTED;
   }
@@ -442,11 +491,12 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   if (rc) return rc;
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, N_CTA);
   if (rc) return rc;
-  const int kblocks = R_pad / KB;
-  const int fixed = 1024 + kblocks * UW_KB_BYTES + 1024 + 2 * 2 * TILE_M * 4;
+  const int kblocks = R_pad / KS / KB;
+  const int fixed = 1024 + kblocks * s_k * 128 * 128 + BASE_RING * BASE_BYTES + 1024 +
+                    2 * 2 * TILE_M * 4;
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
-  if (stages > 8) stages = 8;
-  PALU_REQUIRE(stages >= 2, "tc: not enough shared memory");
+  if (stages > 12) stages = 12;
+  PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
   const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
   static bool attr = false;
   if (!attr) {
@@ -463,15 +513,16 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.s_k = s_k;
   prm.G = G;
   prm.R_pad = R_pad;
+  prm.KS = KS;
   prm.T_cap = T_cap;
   prm.ld_logits = ld_logits;
   prm.n_tab = (T_cap + 127) / 128 + 1;
   prm.stages = stages;
+  prm.plane = (long long)plane_stride;
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
-  dim3 grid(sms);
-  rope_score_tc_kernel<<<grid, THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
+  rope_score_tc_kernel<<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
   PALU_LAUNCHED();
   return PALU_OK;
 }
