@@ -76,7 +76,7 @@ def exported_symbols(path: str = LIB_PATH) -> list[str]:
 
 
 def check(status: int, what: str) -> None:
-    if status == PALU_OK:
+    if status >= PALU_OK:
         return
     msg = (_lib.palu_last_error() or b"").decode(errors="replace")
     if status == PALU_EVALIDATION:
