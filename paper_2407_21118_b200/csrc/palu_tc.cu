@@ -144,56 +144,121 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+// ---- CTA-pair (cta_group::2) primitives ---------------------------------------
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address -> CTA rank 0
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
+// TMA into this CTA's smem, completing bytes on the LEADER's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(const CUtensorMap* map, uint64_t* bar, void* dst,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar) & PEER_MASK), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK)
+               : "memory");
+}
+// M=256 (128 tokens per SM) x N=256 (128 UW rows per SM), fp32 accumulate in TMEM
+constexpr uint32_t IDESC2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                            ((uint32_t)(256 >> 4) << 24);
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC2), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_commit_both(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+// ---- packed fp32x2 FMA (FFMA2) ------------------------------------------------
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 constexpr int BASE_RING = 4;       // tile-base cos/sin rows in flight
 constexpr int BASE_BYTES = 64 * 8; // 64 float2
+constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
+constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16
 
 struct Params {
-  int B, n_heads, s_k, G, R_pad, KS, T_cap, ld_logits, n_tab, stages;
-  long long plane;         // logits plane stride (one plane per rank split)
+  int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
 };
 
-// Work item = (sequence b, key group g, rank split ks, 128-token tile),
-// flattened; CTA c owns [i0, i1).  Per item the CTA computes
-//   ACC_h[128 x 256] = H[tile, ks-th R/KS columns] x UW_h[256 x R/KS]^T
-// for each head pair h of the group (N_CTA = s_k * 128 = 256 or 512) and
-// writes the partial logits of its rank split; the softmax pass adds the
-// KS planes (the cos/sin epilogue is linear in ACC).  Splitting the rank
-// instead of the heads means every latent byte crosses L2 -> SM once.
-__global__ void __launch_bounds__(THREADS, 1)
+// Work item = (sequence b, key group g, 256-token super-tile) for a CTA pair
+// (cluster of 2, cta_group::2).  SM r of the pair loads tokens
+// [256 st + 128 r, +128) of H once and the UW rows of head 2h + r for each head
+// pair h of the group; the leader SM issues
+//   ACC_h[256 tokens x 256] += H[256 x 64] x UW_h[256 x 64]^T   (per k-block)
+// whose rows 128 r .. land in SM r's TMEM.  Each SM's epilogue reduces its
+// own 128 tokens x 2 heads per head pair.  Every latent byte crosses L2 -> SM
+// once and both SMs' tensor pipes run at the 2-SM rate.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  const int r_loc = p.R_pad / p.KS;
-  const int kblocks = r_loc / KB;
-  const int n_cta = p.s_k * 128;
-  const int halves = n_cta / N_CTA;
-  const int uw_kb_bytes = n_cta * 128;
-  uint8_t* s_uw = smem;                                  // kblocks x n_cta rows x 128 B
-  uint8_t* s_h = smem + kblocks * uw_kb_bytes;           // stages x 16 KB
+  const int kblocks = p.R_pad / KB;
+  const int halves = p.s_k / 2;
+  uint8_t* s_uw = smem;                                  // [kblocks][halves] x 16 KB
+  uint8_t* s_h = smem + kblocks * halves * HEAD_BYTES;   // stages x 16 KB
   float2* s_base = reinterpret_cast<float2*>(s_h + p.stages * H_STAGE_BYTES);  // ring
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_base + BASE_RING * 64);
-  uint64_t* full = bars;                                 // [stages]
-  uint64_t* empty = bars + p.stages;                     // [stages]
-  uint64_t* tfull = bars + 2 * p.stages;                 // [2]
-  uint64_t* tempty = tfull + 2;                          // [2]
-  uint64_t* uw_full = tempty + 2;                        // [1]
-  uint64_t* uw_empty = uw_full + 1;                      // [1]
-  uint64_t* bfull = uw_empty + 1;                        // [BASE_RING]
-  uint64_t* bempty = bfull + BASE_RING;                  // [BASE_RING]
+  uint64_t* full = bars;                                 // [stages]   (leader's used)
+  uint64_t* empty = bars + p.stages;                     // [stages]   (each SM's own)
+  uint64_t* tfull = bars + 2 * p.stages;                 // [2]        (each SM's own)
+  uint64_t* tempty = tfull + 2;                          // [2]        (leader's used)
+  uint64_t* uw_full = tempty + 2;                        // [1]        (leader's used)
+  uint64_t* uw_empty = uw_full + 1;                      // [1]        (each SM's own)
+  uint64_t* bfull = uw_empty + 1;                        // [BASE_RING] local
+  uint64_t* bempty = bfull + BASE_RING;                  // [BASE_RING] local
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + BASE_RING);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
   const int T_rows = *p.t_dev + 1;
-  const int n_tiles = (T_rows + TILE_M - 1) / TILE_M;
-  const int total = p.B * p.G * p.KS * n_tiles;
-  const int per = (total + gridDim.x - 1) / gridDim.x;
-  const int i0 = min(total, (int)blockIdx.x * per);
+  const int n_super = (T_rows + SUPER - 1) / SUPER;
+  const int total = p.B * p.G * n_super;
+  const int per = (total + n_pairs - 1) / n_pairs;
+  const int i0 = min(total, pair_id * per);
   const int i1 = min(total, i0 + per);
 
   if (warp == 0 && lane == 0) {
@@ -205,7 +270,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], EPI_WARPS);
+      mbar_init(&tempty[a], 2 * EPI_WARPS);
     }
     for (int a = 0; a < BASE_RING; ++a) {
       mbar_init(&bfull[a], 1);
@@ -217,33 +282,34 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   fence_before();
   __syncthreads();
+  cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer ----------------
+      // ---------------- TMA producer (both SMs) ----------------
       int cur = -1, nloads = 0, kc = 0, it = 0;
       for (int i = i0; i < i1; ++i, ++it) {
-        const int bgk = i / n_tiles, tile = i - bgk * n_tiles;
-        const int bg = bgk / p.KS, ks = bgk - bg * p.KS;
-        if (bgk != cur) {
+        const int bg = i / n_super, st = i - bg * n_super;
+        if (bg != cur) {
           if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
-          mbar_expect_tx(uw_full, kblocks * uw_kb_bytes);
+          if (leader) mbar_expect_tx(uw_full, 2 * kblocks * halves * HEAD_BYTES);
           for (int kb = 0; kb < kblocks; ++kb)
             for (int h = 0; h < halves; ++h)
-              tma_load_2d(&map_uw, uw_full, s_uw + kb * uw_kb_bytes + h * UW_KB_BYTES,
-                          ks * r_loc + kb * KB, bg * n_cta + h * N_CTA);
+              tma_load_2d_pair(&map_uw, uw_full, s_uw + (kb * halves + h) * HEAD_BYTES, kb * KB,
+                               (bg * p.s_k + 2 * h + (int)rank) * 128);
           ++nloads;
-          cur = bgk;
+          cur = bg;
         }
+        const int tile = 2 * st + (int)rank;  // this SM's 128-token tile
         const int bs = it % BASE_RING;
         mbar_wait(&bempty[bs], ((it / BASE_RING) & 1) ^ 1);
         mbar_expect_tx(&bfull[bs], BASE_BYTES);
@@ -252,26 +318,25 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         for (int kb = 0; kb < kblocks; ++kb, ++kc) {
           const int stage = kc % p.stages;
           mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
-          mbar_expect_tx(&full[stage], H_STAGE_BYTES);
-          tma_load_2d(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, ks * r_loc + kb * KB,
-                      h_row);
+          if (leader) mbar_expect_tx(&full[stage], 2 * H_STAGE_BYTES);
+          tma_load_2d_pair(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB, h_row);
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer ----------------
+    if (leader && lane == 0) {
+      // ---------------- MMA issuer (leader SM issues for the pair) ----------------
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
       int cur = -1, nloads = 0, kc = 0, unit = 0;
       for (int i = i0; i < i1; ++i) {
-        const int bgk = i / n_tiles;
-        if (bgk != cur) {
-          if (nloads > 0) umma_commit(uw_empty);  // frees UW once issued MMAs retire
+        const int bg = i / n_super;
+        if (bg != cur) {
+          if (nloads > 0) umma2_commit_both(uw_empty);  // frees UW in both SMs
           mbar_wait(uw_full, nloads & 1);
           fence_after();
           ++nloads;
-          cur = bgk;
+          cur = bg;
         }
         for (int h = 0; h < halves; ++h, ++unit) {
           const int slot = unit & 1;
@@ -286,103 +351,111 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
               fence_after();
             }
             const uint32_t a0 = h_addr + stage * H_STAGE_BYTES;
-            const uint32_t b0 = uw_addr + kb * uw_kb_bytes + h * UW_KB_BYTES;
+            const uint32_t b0 = uw_addr + (kb * halves + h) * HEAD_BYTES;
 #pragma unroll
             for (int kk = 0; kk < KB / 16; ++kk)
-              umma_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
-            if (h == halves - 1) umma_commit(&empty[stage]);
+              umma2_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
+            if (h == halves - 1) umma2_commit_both(&empty[stage]);
           }
-          umma_commit(&tfull[slot]);
+          umma2_commit_both(&tfull[slot]);
         }
         kc += kblocks;
       }
     }
   } else {
-    // ---------------- epilogue: cos/sin-weighted row reduction ----------------
+    // ---------------- epilogue (both SMs): cos/sin-weighted row reduction ----------------
     const int q = warp & 3;          // TMEM lane quarter
     const int jh = (warp - 2) >> 2;  // which 32 of the 64 frequencies
-    const int delta = q * 32 + lane; // token row inside the tile
-    float cd[32], sd[32];
+    const int delta = q * 32 + lane; // token row inside this SM's tile
+    float2 cd2[16], sd2[16];         // cos/sin(delta th_j) for j pairs (2i, 2i + 1)
     {
-      const float2* off = p.rope_tab + (size_t)(p.n_tab + delta) * 64 + jh * 32;
+      const float4* off =
+          reinterpret_cast<const float4*>(p.rope_tab + (size_t)(p.n_tab + delta) * 64 + jh * 32);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float2 v = off[j];
-        cd[j] = v.x;
-        sd[j] = v.y;
+      for (int i = 0; i < 16; ++i) {
+        const float4 v = off[i];
+        cd2[i] = make_float2(v.x, v.z);
+        sd2[i] = make_float2(v.y, v.w);
       }
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     int unit = 0, it = 0;
     for (int i = i0; i < i1; ++i, ++it) {
-      const int bgk = i / n_tiles, tile = i - bgk * n_tiles;
-      const int bg = bgk / p.KS, ks = bgk - bg * p.KS;
+      const int bg = i / n_super, st = i - bg * n_super;
       const int b = bg / p.G, g = bg - b * p.G;
+      const int tile = 2 * st + (int)rank;
       const int bs = it % BASE_RING;
       mbar_wait(&bfull[bs], (it / BASE_RING) & 1);
-      const float2* base = s_base + bs * 64 + jh * 32;
+      // cos/sin((t0 + delta) th_j) = base (x) offset, for this thread's 32 frequencies
+      float2 c2[16], s2[16];
+      {
+        const float4* base = reinterpret_cast<const float4*>(s_base + bs * 64 + jh * 32);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float4 bv = base[k];
+          const float2 bc = make_float2(bv.x, bv.z), bsn = make_float2(bv.y, bv.w);
+          const float2 t = fmul2(bsn, sd2[k]);
+          c2[k] = ffma2(bc, cd2[k], make_float2(-t.x, -t.y));
+          s2[k] = ffma2(bsn, cd2[k], fmul2(bc, sd2[k]));
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bempty[bs]);
       for (int h = 0; h < halves; ++h, ++unit) {
         const int slot = unit & 1;
         mbar_wait(&tfull[slot], (unit >> 1) & 1);
         fence_after();
-        float v0 = 0.f, v1 = 0.f;
+        float v[2];
 #pragma unroll
-        for (int jc = 0; jc < 2; ++jc) {
-          float c[16], s[16];
+        for (int hp = 0; hp < 2; ++hp) {
+          float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const float2 bsv = base[jc * 16 + j];
-            const float cdj = cd[jc * 16 + j], sdj = sd[jc * 16 + j];
-            c[j] = bsv.x * cdj - bsv.y * sdj;  // cos((t0 + delta) th_j)
-            s[j] = bsv.y * cdj + bsv.x * sdj;  // sin((t0 + delta) th_j)
-          }
-#pragma unroll
-          for (int hp = 0; hp < 2; ++hp) {
+          for (int jc = 0; jc < 2; ++jc) {
             float u[16], w[16];
             const uint32_t col = slot * N_CTA + hp * 128 + jh * 32 + jc * 16;
             tmem_ld16(lane_base + col, u);
             tmem_ld16(lane_base + col + 64, w);
             tmem_wait_ld();
-            float acc_v = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc_v = fmaf(c[j], u[j], fmaf(s[j], w[j], acc_v));
-            if (hp == 0) v0 += acc_v; else v1 += acc_v;
+            for (int k = 0; k < 8; ++k) {
+              acc2 = ffma2(c2[jc * 8 + k], make_float2(u[2 * k], u[2 * k + 1]), acc2);
+              acc2 = ffma2(s2[jc * 8 + k], make_float2(w[2 * k], w[2 * k + 1]), acc2);
+            }
           }
+          v[hp] = acc2.x + acc2.y;
         }
         float* r = red + slot * 2 * TILE_M;
         if (jh == 1) {
-          r[delta] = v0;
-          r[TILE_M + delta] = v1;
+          r[delta] = v[0];
+          r[TILE_M + delta] = v[1];
           fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[slot]);
+          if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           named_bar_arrive(1 + slot, EPI_WARPS * 32);
         } else {
           named_bar_sync(1 + slot, EPI_WARPS * 32);
-          v0 += r[delta];
-          v1 += r[TILE_M + delta];
+          const float v0 = v[0] + r[delta], v1 = v[1] + r[TILE_M + delta];
           fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tempty[slot]);
+          if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           const int t = tile * TILE_M + delta;
           if (t < T_rows) {
-            const int head0 = g * p.s_k + h * 2;
-            float* lg = p.logits + (size_t)ks * p.plane +
-                        ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
+            // D columns 0..127 = head 2h (leader's UW rows), 128..255 = head 2h + 1
+            const int head0 = g * p.s_k + 2 * h;
+            float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
             lg[0] = v0;
             lg[p.ld_logits] = v1;
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bempty[bs]);
     }
   }
   fence_before();
   __syncthreads();
+  cluster_sync();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
 }
 
@@ -461,12 +534,8 @@ int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, v
 
 int palu_rope_score_tc_splits(int s_k, int R_pad) {
   using namespace palu::tc;
-  const int n = s_k * 128;
-  for (int ks = 1; ks <= 4; ks *= 2) {
-    if (R_pad % (ks * KB) != 0) break;
-    if ((size_t)n * (R_pad / ks) * 2 <= 128 * 1024) return ks;
-  }
-  return 0;
+  // one rank slice: the 2-SM pair keeps the whole UW operand resident
+  return ((s_k == 2 || s_k == 4) && R_pad % KB == 0 && R_pad <= 256) ? 1 : 0;
 }
 
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
@@ -476,12 +545,12 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   using namespace palu::tc;
   (void)scales;
   (void)zps;
+  (void)plane_stride;
   if (bits != 16) {
     set_error("palu_rope_score_tc: bits %d not on the tensor-core path yet", bits);
     return PALU_EUNSUPPORTED;
   }
-  const int KS = palu_rope_score_tc_splits(s_k, R_pad);
-  if (R_pad % KB != 0 || (s_k != 2 && s_k != 4) || G * s_k != n_heads || KS == 0) {
+  if (!palu_rope_score_tc_splits(s_k, R_pad) || G * s_k != n_heads) {
     set_error("palu_rope_score_tc: unsupported shape (R_pad %d, s_k %d)", R_pad, s_k);
     return PALU_EUNSUPPORTED;
   }
@@ -489,10 +558,10 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   CUtensorMap map_h, map_uw;
   int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
   if (rc) return rc;
-  rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, N_CTA);
+  rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, TILE_M);
   if (rc) return rc;
-  const int kblocks = R_pad / KS / KB;
-  const int fixed = 1024 + kblocks * s_k * 128 * 128 + BASE_RING * BASE_BYTES + 1024 +
+  const int kblocks = R_pad / KB;
+  const int fixed = 1024 + kblocks * (s_k / 2) * HEAD_BYTES + BASE_RING * BASE_BYTES + 1024 +
                     2 * 2 * TILE_M * 4;
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
@@ -513,16 +582,14 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.s_k = s_k;
   prm.G = G;
   prm.R_pad = R_pad;
-  prm.KS = KS;
   prm.T_cap = T_cap;
   prm.ld_logits = ld_logits;
   prm.n_tab = (T_cap + 127) / 128 + 1;
   prm.stages = stages;
-  prm.plane = (long long)plane_stride;
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
-  rope_score_tc_kernel<<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
+  rope_score_tc_kernel<<<dim3(sms & ~1), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
   PALU_LAUNCHED();
   return PALU_OK;
 }
