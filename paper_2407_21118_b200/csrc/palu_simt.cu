@@ -495,42 +495,110 @@ struct SvSeg {
   }
 };
 
+__device__ __forceinline__ uint32_t sv_smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void sv_mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = sv_smem_u32(bar);
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  }
+}
+
+constexpr int SV_CONSUMERS = 8;              // consumer warps
+constexpr int SV_BLOCK = (SV_CONSUMERS + 1) * 32;
+constexpr int SV_STAGE_BYTES = 16384;
+constexpr int SV_NSTAGE = 4;
+
+// Split-T softmax + value pass.  The chunk's H_v rows are contiguous in HBM,
+// so one elected producer lane streams them with 1-D TMA bulk copies
+// (cp.async.bulk, 16 KB stages, 4 in flight) while 8 consumer warps first
+// compute the per-head softmax statistics and then reduce the staged rows
+// out of shared memory.  Lr lanes cover a row (NSEG segments each); rows are
+// spread over warps.  Quantised rows use ctx = sum_t (p_t s_t) code_t -
+// sum_t p_t s_t z_t with the z term folded into the statistics pass.
 template <typename T, int BITS, int NSEG>
-__global__ void __launch_bounds__(SV_THREADS)
+__global__ void __launch_bounds__(SV_BLOCK)
 softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restrict__ scales,
                              const float* __restrict__ zps, int n_heads, int s_v, int G, int R_pad,
                              int T_cap, const float* __restrict__ logits, int ld_logits,
                              int n_planes, long long plane, const int* __restrict__ t_dev, int NC,
-                             SvPartial part) {
+                             int Lr, SvPartial part) {
   using Seg = SvSeg<T, BITS>;
   constexpr int COLV = Seg::COLV;
-  constexpr int UNR = 4;
-  extern __shared__ float sv_sm[];  // ps[SV_HP][clen] | later red[8][SV_HP][R_pad]
+  extern __shared__ __align__(128) uint8_t sv_raw[];
+  uint8_t* ring = sv_raw;                                            // SV_NSTAGE x 16 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + SV_NSTAGE * SV_STAGE_BYTES);
+  uint64_t* empty = full + SV_NSTAGE;
+  float* ps = reinterpret_cast<float*>(empty + SV_NSTAGE);           // [SV_HP][clen]
   __shared__ float zsum[SV_HP];
   const int c = blockIdx.x, g = blockIdx.y, b = blockIdx.z;
   const int T_rows = *t_dev + 1;
   int clen = (T_rows + NC - 1) / NC;
   clen = (clen + 7) & ~7;
-  const int c0 = c * clen;
+  const int c0 = min(T_rows, c * clen);
   const int c1 = min(T_rows, c0 + clen);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  float* ps = sv_sm;
   const size_t tok_base = ((size_t)b * G + g) * T_cap;
   const int row_bytes = Seg::RAW ? R_pad * (int)sizeof(T) : R_pad * BITS / 8;
   const int segs = row_bytes / Seg::BYTES;
-  const int Lr = segs / NSEG;            // lanes per row (power of two <= 32)
-  const int RW = 32 / Lr;                // rows per warp
+  const int RW = 32 / Lr;  // rows per warp step
   const int rs = lane / Lr, sb = lane - rs * Lr;
-  const uint8_t* hvb = reinterpret_cast<const uint8_t*>(hv);
+  const int stage_rows = SV_STAGE_BYTES / row_bytes;
+  const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
+  const uint8_t* src0 = reinterpret_cast<const uint8_t*>(hv) + (tok_base + c0) * (size_t)row_bytes;
 
+  if (tid == 0) {
+    for (int st = 0; st < SV_NSTAGE; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sv_smem_u32(&full[st])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sv_smem_u32(&empty[st])),
+                   "r"(SV_CONSUMERS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  int load_ctr = 0;  // producer and consumers walk the same stage sequence
   for (int p0 = 0; p0 < s_v; p0 += SV_HP) {
     const int hp = min(SV_HP, s_v - p0);
-    __syncthreads();
+    if (warp == SV_CONSUMERS) {
+      // ---------------- producer: stream the chunk rows ----------------
+      // the ring doubles as the consumers' reduction buffer: wait until the
+      // previous head pass has finished with it
+      if (p0 > 0) asm volatile("bar.sync 2, %0;" ::"r"(SV_BLOCK) : "memory");
+      if (lane == 0) {
+        for (int l = 0; l < n_loads; ++l) {
+          const int ctr = load_ctr + l;
+          const int st = ctr % SV_NSTAGE;
+          sv_mbar_wait(&empty[st], ((ctr / SV_NSTAGE) & 1) ^ 1);
+          const int r0 = l * stage_rows;
+          const int nr = min(stage_rows, (c1 - c0) - r0);
+          const uint32_t bytes = (uint32_t)(nr * row_bytes);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                           sv_smem_u32(&full[st])),
+                       "r"(bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  sv_smem_u32(ring + st * SV_STAGE_BYTES)),
+              "l"(src0 + (size_t)r0 * row_bytes), "r"(bytes), "r"(sv_smem_u32(&full[st]))
+              : "memory");
+        }
+      }
+      load_ctr += n_loads;
+      continue;
+    }
     // (1) one warp per head: chunk max, exp (x scale when quantised), sums
     if (warp < hp) {
       const int head = g * s_v + p0 + warp;
       const float* lg = logits + ((size_t)b * n_heads + head) * ld_logits;
-      // logits of every rank-split plane add up (palu_rope_score_tc)
       float m = -INFINITY;
       for (int t = c0 + lane; t < c1; t += 32) {
         float v = lg[t];
@@ -559,8 +627,8 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
         zsum[warp] = zs;
       }
     }
-    __syncthreads();
-    // (2) stream the chunk's rows
+    asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+    // (2) reduce the staged rows
     float acc[SV_HP][NSEG][COLV];
 #pragma unroll
     for (int h = 0; h < SV_HP; ++h)
@@ -568,29 +636,34 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
       for (int q = 0; q < NSEG; ++q)
 #pragma unroll
         for (int e = 0; e < COLV; ++e) acc[h][q][e] = 0.f;
-    const int row_step = 8 * RW;
-    for (int t = c0 + warp * RW + rs; t < c1; t += UNR * row_step) {
-      uint4 v[UNR][NSEG];
+    for (int l = 0; l < n_loads; ++l) {
+      const int ctr = load_ctr + l;
+      const int st = ctr % SV_NSTAGE;
+      sv_mbar_wait(&full[st], (ctr / SV_NSTAGE) & 1);
+      const int r0 = l * stage_rows;
+      const int nr = min(stage_rows, (c1 - c0) - r0);
+      const uint8_t* sbase = ring + st * SV_STAGE_BYTES;
+      for (int r = warp * RW + rs; r < nr; r += SV_CONSUMERS * RW) {
+        const uint8_t* row = sbase + (size_t)r * row_bytes;
+        float pv[SV_HP];
 #pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int tt = t + u * row_step;
-        if (tt < c1) {
-          const uint8_t* row = hvb + (tok_base + tt) * (size_t)row_bytes;
+        for (int h = 0; h < SV_HP; ++h) pv[h] = (h < hp) ? ps[h * clen + r0 + r] : 0.f;
 #pragma unroll
-          for (int q = 0; q < NSEG; ++q) v[u][q] = Seg::load(row + (sb + q * Lr) * Seg::BYTES);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < UNR; ++u) {
-        const int tt = t + u * row_step;
-        if (tt < c1) {
-          float pv[SV_HP];
-#pragma unroll
-          for (int h = 0; h < SV_HP; ++h) pv[h] = (h < hp) ? ps[h * clen + (tt - c0)] : 0.f;
-#pragma unroll
-          for (int q = 0; q < NSEG; ++q) {
+        for (int q = 0; q < NSEG; ++q) {
+          const int sg = sb + q * Lr;
+          if (sg < segs) {
+            uint4 v;
+            if constexpr (Seg::BYTES == 16) {
+              v = *reinterpret_cast<const uint4*>(row + sg * 16);
+            } else {
+              const uint32_t* w = reinterpret_cast<const uint32_t*>(row + sg * Seg::BYTES);
+              v.x = w[0];
+              v.y = Seg::BYTES > 4 ? w[1] : 0u;
+              v.z = Seg::BYTES > 8 ? w[2] : 0u;
+              v.w = 0u;
+            }
             float f[COLV];
-            Seg::unpack(v[u][q], f);
+            Seg::unpack(v, f);
 #pragma unroll
             for (int h = 0; h < SV_HP; ++h)
 #pragma unroll
@@ -598,7 +671,12 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
           }
         }
       }
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sv_smem_u32(&empty[st]))
+                     : "memory");
     }
+    load_ctr += n_loads;
     // (3) reduce: across row slots inside the warp, then across warps
 #pragma unroll
     for (int h = 0; h < SV_HP; ++h)
@@ -608,27 +686,32 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
         for (int e = 0; e < COLV; ++e)
           for (int o = Lr; o < 32; o <<= 1)
             acc[h][q][e] += __shfl_xor_sync(0xffffffffu, acc[h][q][e], o);
-    __syncthreads();  // ps no longer needed: reuse as red
-    float* red = sv_sm;
+    asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+    float* red = reinterpret_cast<float*>(ring);  // all stages consumed: reuse
     if (rs == 0) {
 #pragma unroll
       for (int h = 0; h < SV_HP; ++h)
 #pragma unroll
-        for (int q = 0; q < NSEG; ++q)
+        for (int q = 0; q < NSEG; ++q) {
+          const int sg = sb + q * Lr;
+          if (sg < segs)
 #pragma unroll
-          for (int e = 0; e < COLV; ++e)
-            red[((size_t)warp * SV_HP + h) * R_pad + (sb + q * Lr) * COLV + e] = acc[h][q][e];
+            for (int e = 0; e < COLV; ++e)
+              red[((size_t)warp * SV_HP + h) * R_pad + sg * COLV + e] = acc[h][q][e];
+        }
     }
-    __syncthreads();
-    for (int idx = tid; idx < hp * R_pad; idx += SV_THREADS) {
+    asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+    for (int idx = tid; idx < hp * R_pad; idx += SV_CONSUMERS * 32) {
       const int h = idx / R_pad, col = idx - h * R_pad;
       float v = 0.f;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) v += red[((size_t)w * SV_HP + h) * R_pad + col];
+      for (int w = 0; w < SV_CONSUMERS; ++w) v += red[((size_t)w * SV_HP + h) * R_pad + col];
       if constexpr (!Seg::RAW) v -= zsum[h];
       const int head = g * s_v + p0 + h;
       part.ctx[(((size_t)b * n_heads + head) * NC + c) * R_pad + col] = v;
     }
+    asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+    if (p0 + SV_HP < s_v) asm volatile("bar.arrive 2, %0;" ::"r"(SV_BLOCK) : "memory");
   }
 }
 
@@ -821,14 +904,16 @@ template <typename T, int BITS, int NSEG>
 static int launch_sv_n(const void* hv, const float* scales, const float* zps, int B, int n_heads,
                        int s_v, int G, int R_pad, const int* ranks_v, const int* o_off, int T_cap,
                        const float* logits, int ld_logits, int n_planes, long long plane,
-                       const int* t_dev, int NC, SvPartial part, float* ctx, int ld_ctx,
+                       const int* t_dev, int NC, int Lr, SvPartial part, float* ctx, int ld_ctx,
                        cudaStream_t st) {
   int clen = (T_cap + NC - 1) / NC;
   clen = (clen + 7) & ~7;
   PALU_REQUIRE(clen <= SV_MAX_CHUNK, "palu_softmax_value: raise n_chunks (chunk %d > %d)", clen,
                SV_MAX_CHUNK);
-  const size_t ps = (size_t)SV_HP * clen, red = (size_t)8 * SV_HP * R_pad;
-  const size_t smem = sizeof(float) * (ps > red ? ps : red);
+  const size_t ring = (size_t)SV_NSTAGE * SV_STAGE_BYTES;
+  const size_t red = (size_t)SV_CONSUMERS * SV_HP * R_pad * sizeof(float);
+  PALU_REQUIRE(red <= ring, "palu_softmax_value: R_pad %d too large", R_pad);
+  const size_t smem = ring + 2 * SV_NSTAGE * sizeof(uint64_t) + (size_t)SV_HP * clen * sizeof(float);
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(softmax_value_partial_kernel<T, BITS, NSEG>,
@@ -836,13 +921,12 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
     attr = true;
   }
   dim3 grid(NC, G, B);
-  softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_THREADS, smem, st>>>(
+  softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_BLOCK, smem, st>>>(
       hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, n_planes, plane, t_dev, NC,
-      part);
+      Lr, part);
   PALU_LAUNCHED();
   softmax_value_combine_kernel<<<dim3(n_heads, B, (R_pad + 127) / 128), 128, NC * sizeof(float),
-                                 st>>>(
-      n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
+                                 st>>>(n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -855,19 +939,22 @@ static int launch_sv(const void* hv, const float* scales, const float* zps, int 
                      cudaStream_t st) {
   using Seg = SvSeg<T, BITS>;
   const int row_bytes = Seg::RAW ? R_pad * (int)sizeof(T) : R_pad * BITS / 8;
-  PALU_REQUIRE(row_bytes % Seg::BYTES == 0, "palu_softmax_value: R_pad=%d unsupported", R_pad);
+  PALU_REQUIRE(row_bytes % Seg::BYTES == 0 && row_bytes % 16 == 0 && row_bytes <= SV_STAGE_BYTES,
+               "palu_softmax_value: R_pad=%d unsupported", R_pad);
   const int segs = row_bytes / Seg::BYTES;
-  const int nseg = segs <= 32 ? 1 : segs / 32;
-  const int lr = segs / nseg;
-  PALU_REQUIRE(segs % nseg == 0 && (lr & (lr - 1)) == 0 && lr <= 32 && nseg <= 4,
-               "palu_softmax_value: R_pad=%d unsupported (segments %d)", R_pad, segs);
+  const int nseg = (segs + 31) / 32;
+  int lr = 1;
+  while (lr < (segs + nseg - 1) / nseg) lr <<= 1;
+  PALU_REQUIRE(nseg <= 4 && lr <= 32, "palu_softmax_value: R_pad=%d unsupported (segments %d)",
+               R_pad, segs);
 #define SVN(N_) return launch_sv_n<T, BITS, N_>(hv, scales, zps, B, n_heads, s_v, G, R_pad, ranks_v, \
                                                  o_off, T_cap, logits, ld_logits, n_planes, plane, \
-                                                 t_dev, NC, part, ctx, ld_ctx, st)
+                                                 t_dev, NC, lr, part, ctx, ld_ctx, st)
   if (nseg == 1) SVN(1);
   if (nseg == 2) SVN(2);
-  SVN(4);
+  if (nseg <= 4) SVN(4);
 #undef SVN
+  PALU_REQUIRE(false, "palu_softmax_value: unsupported segment count");
 }
 
 }  // namespace palu

@@ -19,6 +19,7 @@
 // pair half (w - 2) / 4 of the 64 RoPE frequencies).
 #include <cuda.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "palu_common.cuh"
 
@@ -75,6 +76,11 @@ __device__ __forceinline__ void tma_load_2d(const CUtensorMap* map, uint64_t* ba
       " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_l2(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(map), "r"(c0),
+               "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -208,12 +214,14 @@ __device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
 }
 
 constexpr int BASE_RING = 4;       // tile-base cos/sin rows in flight
+constexpr int PF_DIST = 3;         // L2 prefetch distance (work items)
 constexpr int BASE_BYTES = 64 * 8; // 64 float2
 constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
 constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16
 
 struct Params {
   int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
+  int mode;  // 0 = full; 1 = profiling: epilogue skips the TMEM math (pipeline-only timing)
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
@@ -315,6 +323,14 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         mbar_expect_tx(&bfull[bs], BASE_BYTES);
         bulk_load(s_base + bs * 64, p.rope_tab + (size_t)tile * 64, BASE_BYTES, &bfull[bs]);
         const int h_row = bg * p.T_cap + tile * TILE_M;
+        // warm L2 with this SM's rows of the item PF_DIST ahead: smem holds only
+        // ~1.25 items next to the resident UW, so HBM latency must be hidden in L2
+        if (i + PF_DIST < i1) {
+          const int ip = i + PF_DIST;
+          const int bgp = ip / n_super, stp = ip - bgp * n_super;
+          const int rowp = bgp * p.T_cap + (2 * stp + (int)rank) * TILE_M;
+          for (int kb = 0; kb < kblocks; ++kb) tma_prefetch_l2(&map_h, kb * KB, rowp);
+        }
         for (int kb = 0; kb < kblocks; ++kb, ++kc) {
           const int stage = kc % p.stages;
           mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
@@ -405,7 +421,8 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         const int slot = unit & 1;
         mbar_wait(&tfull[slot], (unit >> 1) & 1);
         fence_after();
-        float v[2];
+        float v[2] = {0.f, 0.f};
+        if (p.mode == 0)
 #pragma unroll
         for (int hp = 0; hp < 2; ++hp) {
           float2 acc2 = make_float2(0.f, 0.f);
@@ -586,6 +603,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.ld_logits = ld_logits;
   prm.n_tab = (T_cap + 127) / 128 + 1;
   prm.stages = stages;
+  prm.mode = getenv("PALU_TC_PROFILE_MODE") ? atoi(getenv("PALU_TC_PROFILE_MODE")) : 0;
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
