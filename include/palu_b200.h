@@ -96,13 +96,13 @@ int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* 
  *     u_j = scale * (q_rot[j]   * B_g[:, p*d_h+j] + q_rot[j+h] * B_g[:, p*d_h+j+h])
  *     w_j = scale * (q_rot[j+h] * B_g[:, p*d_h+j] - q_rot[j]   * B_g[:, p*d_h+j+h])
  *   so that  q_rot . RoPE_t'(h B_g[:, head]) = sum_j cos(t' th_j) h.u_j + sin(t' th_j) h.w_j.
- * bk: [G][R_pad][s_k*d_h] in `dtype` (rows >= rank zero).
+ * bk: [G][bk_rows][s_k*d_h] in `dtype` (rows >= rank zero, bk_rows >= R_pad).
  * layout 0: uw fp32 [B][n][R_pad][d_h]  (cols j < h: u_j, j >= h: w_{j-h})
  * layout 1: uw bf16 [B][G][s_k*d_h][R_pad] (K-major rows, tcgen05 B operand)
  */
 int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, int head_dim,
-                      int s_k, const void* bk, int R_pad, const double* theta, float scale,
-                      const int* t_dev, void* uw, int layout, void* stream);
+                      int s_k, const void* bk, int bk_rows, int R_pad, const double* theta,
+                      float scale, const int* t_dev, void* uw, int layout, void* stream);
 
 /*
  * RoPE score over the latent key cache (attention.py:433-444):
@@ -141,8 +141,9 @@ size_t palu_rope_table_floats(int half, int T_cap);
  * up to the wo_fused product):  ctx[b][o_off[i] + c] = sum_t' p_i[t'] H_v[g(i)][t'][c]
  * with p_i = softmax(sum of the n_planes logit planes [b][i][0..*t_dev]),
  * split over n_chunks token
- * chunks per (b, group) and merged in a fixed order (deterministic).
- * workspace: palu_softmax_value_workspace() bytes.
+ * chunks per (b, group) and merged in a fixed order (deterministic) by the
+ * last CTA of each (b, group).  workspace: palu_softmax_value_workspace()
+ * bytes, zero-initialised once (the arrival tickets reset themselves).
  */
 size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks);
 int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales,

@@ -140,8 +140,13 @@ class FusedWeights:
         return _lib.DTYPE_F32 if self.dtype == "float32" else _lib.DTYPE_BF16
 
 
-def _rank_pad(r: int, dtype: str) -> int:
-    return _round_up(max(r, 1), 64 if dtype == "bfloat16" else 32)
+def _rank_pad(r: int, dtype: str, bits: int = 16) -> int:
+    """Row width of a latent store: bf16 rows are 128-byte swizzle blocks for
+    the tcgen05 path; packed rows must be whole 16-byte TMA granules."""
+    m = 64 if dtype == "bfloat16" else 32
+    if bits != 16:
+        m = max(m, {2: 64, 3: 128, 4: 32, 8: 32}[bits])
+    return _round_up(max(r, 1), m)
 
 
 def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=None) -> FusedWeights:
@@ -181,8 +186,8 @@ def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=N
         wo_fused = np.concatenate(o_blocks, axis=0)
         key_ranks = tuple(g.rank for g in kv.key.groups)
         value_ranks = tuple(g.rank for g in kv.value.groups)
-        rk_pad = _rank_pad(max(key_ranks), dtype)
-        rv_pad = _rank_pad(max(value_ranks), dtype)
+        rk_pad = _round_up(max(key_ranks), 128)  # covers every store width below
+        rv_pad = _round_up(max(value_ranks), 128)
         ko = wo_fused.shape[0]
         ko_pad = _round_up(ko, 8)
         w1 = np.concatenate([wq.T] + [a.T for a in ak] + [a.T for a in av], axis=0)
@@ -357,8 +362,10 @@ class LatentKVCache:
         for kv in self.decomposed:
             rk, rv = kv.key.ranks, kv.value.ranks
             self._stores.append((
-                _SideStore(rk, k_bits, _rank_pad(max(rk), dtype), batch, cap, dtype, self.device),
-                _SideStore(rv, v_bits, _rank_pad(max(rv), dtype), batch, cap, dtype, self.device)))
+                _SideStore(rk, k_bits, _rank_pad(max(rk), dtype, k_bits), batch, cap, dtype,
+                           self.device),
+                _SideStore(rv, v_bits, _rank_pad(max(rv), dtype, v_bits), batch, cap, dtype,
+                           self.device)))
         if score_kernel not in ("auto", "simt", "tcgen05"):
             raise ValidationError(f"score_kernel must be auto|simt|tcgen05, got {score_kernel!r}")
         self.score_kernel = score_kernel
@@ -488,14 +495,16 @@ class _Session:
                   _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev), _ptr(V.rows), _ptr(V.scales),
                   _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64), V.r_pad, V.cap, _ptr(self.t_dev), st)
         if self.tc_layers[li]:
-            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
-                      _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw_bf), 1, st)
+            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
+                      L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
+                      _ptr(self.uw_bf), 1, st)
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, self.plane, st)
         else:
-            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk), K.r_pad,
-                      _ptr(f.theta_dev), self.scale, _ptr(self.t_dev), _ptr(self.uw), 0, st)
+            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
+                      L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
+                      _ptr(self.uw), 0, st)
             _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps),
                       B, n, dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)

@@ -89,4 +89,13 @@ __device__ __forceinline__ double round_half_away(double x) {
   return x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5));
 }
 
+// sincos of a large fp64 angle: Cody-Waite reduction by 2*pi first, so the
+// library call stays on its fast path (t * theta reaches 1e5 rad at 128K).
+__device__ __forceinline__ void sincos_big(double x, double* sn, double* cs) {
+  const double k = rint(x * 0.15915494309189535);    // 1 / (2 pi)
+  double r = fma(-k, 6.283185307179586, x);           // 2 pi (hi)
+  r = fma(-k, 2.4492935982947064e-16, r);             // 2 pi (lo)
+  sincos(r, sn, cs);
+}
+
 }  // namespace palu

@@ -241,7 +241,7 @@ __global__ void pack_rows_kernel(const uint8_t* __restrict__ codes, int cols, in
 // ---------------------------------------------------------------------------
 template <typename T>
 __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n_heads, int dh,
-                                    int s_k, const T* __restrict__ bk, int R_pad,
+                                    int s_k, const T* __restrict__ bk, int bk_rows, int R_pad,
                                     const double* __restrict__ theta, float scale,
                                     const int* __restrict__ t_dev, void* __restrict__ uw,
                                     int layout) {
@@ -257,13 +257,13 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   const float* qh = q + (size_t)b * ld_q + (size_t)i * dh;
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
     double sn, cs;
-    sincos(pos * theta[j], &sn, &cs);  // attention.py:108-112 (fp64 angles)
+    sincos_big(pos * theta[j], &sn, &cs);  // attention.py:108-112 (fp64 angles)
     const double lo = qh[j], hi = qh[j + half];
     qr[j] = (float)(lo * cs - hi * sn);
     qr[j + half] = (float)(lo * sn + hi * cs);
   }
   const int width = s_k * dh;
-  const T* bg = bk + ((size_t)g * R_pad + k0) * width + (size_t)p * dh;
+  const T* bg = bk + ((size_t)g * bk_rows + k0) * width + (size_t)p * dh;
   for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
     const int kk = idx / dh, c = idx - kk * dh;
     bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
@@ -336,7 +336,7 @@ rope_score_tiled_kernel(const void* __restrict__ hk, const float* __restrict__ s
     for (int idx = tid; idx < SC_TT * HALF; idx += blockDim.x) {
       const int tt = idx / HALF, j = idx - tt * HALF;
       double sn, cs;
-      sincos((double)(t0 + tt) * theta[j], &sn, &cs);
+      sincos_big((double)(t0 + tt) * theta[j], &sn, &cs);
       CSs[tt][j] = make_float2((float)cs, (float)sn);
     }
     for (int p = 0; p < s_k; ++p) {
@@ -420,7 +420,7 @@ __global__ void rope_score_generic_kernel(const void* __restrict__ hk, const flo
         w = fmaf(h, uwh[(size_t)k * dh + j + half], w);
       }
       double sn, cs;
-      sincos((double)t * theta[j], &sn, &cs);
+      sincos_big((double)t * theta[j], &sn, &cs);
       v += (float)cs * a + (float)sn * w;
     }
     logits[((size_t)b * n_heads + head) * ld_logits + t] = v;
@@ -436,18 +436,52 @@ constexpr int SV_HP = 4;           // heads per pass
 constexpr int SV_MAX_CHUNK = 8192;  // tokens per chunk cap (smem)
 
 struct SvPartial {
-  float* m;    // [B][n][NC]
-  float* l;    // [B][n][NC]
-  float* ctx;  // [B][n][NC][R_pad]
+  float* m;       // [B][n][NC]
+  float* l;       // [B][n][NC]
+  float* ctx;     // [B][n][NC][R_pad]
+  unsigned* cnt;  // [B][G] arrival tickets (self-resetting)
 };
 
 __host__ __device__ inline SvPartial sv_carve(void* ws, int B, int n, int R_pad, int NC) {
+  // tickets first: their offset must not depend on R_pad (layers may differ)
   SvPartial p;
-  float* f = reinterpret_cast<float*>(ws);
+  p.cnt = reinterpret_cast<unsigned*>(ws);
+  float* f = reinterpret_cast<float*>(ws) + (((size_t)B * n + 31) & ~size_t(31));
   p.m = f;
   p.l = f + (size_t)B * n * NC;
   p.ctx = f + 2 * (size_t)B * n * NC;
   return p;
+}
+
+// Fixed-order merge of a head's NC chunk partials (flash-decoding combine):
+// ctx = sum_c e^(m_c - M) ctx_c / sum_c e^(m_c - M) l_c.  nthreads threads.
+__device__ void sv_merge_head(const SvPartial& part, size_t base, int NC, int R_pad, int r,
+                              float* dst, float* wsm, int tid, int nthreads, int bar_id) {
+  __shared__ float inv_l_sh;
+  if (tid < 32) {
+    float M = -INFINITY;
+    for (int c = tid; c < NC; c += 32) M = fmaxf(M, part.m[base + c]);
+    M = warp_reduce(M, [](float a, float d) { return fmaxf(a, d); });
+    float L = 0.f;
+    for (int c = tid; c < NC; c += 32) {
+      const float l = part.l[base + c];
+      const float w = (l > 0.f) ? expf(part.m[base + c] - M) : 0.f;
+      wsm[c] = w;
+      L += w * l;
+    }
+    L = warp_reduce(L, [](float a, float d) { return a + d; });
+    if (tid == 0) inv_l_sh = 1.f / L;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+  const float inv_l = inv_l_sh;
+  const float* src = part.ctx + base * R_pad;
+  for (int col = tid; col < r; col += nthreads) {
+    float v = 0.f;
+#pragma unroll 8
+    for (int c = 0; c < NC; ++c) v = fmaf(wsm[c], src[(size_t)c * R_pad + col], v);
+    dst[col] = v * inv_l;
+  }
+  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
 }
 
 // Streaming value pass.  A "segment" is what one lane loads per row: 16 B of
@@ -529,7 +563,9 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
                              const float* __restrict__ zps, int n_heads, int s_v, int G, int R_pad,
                              int T_cap, const float* __restrict__ logits, int ld_logits,
                              int n_planes, long long plane, const int* __restrict__ t_dev, int NC,
-                             int Lr, SvPartial part) {
+                             int Lr, SvPartial part, const int* __restrict__ ranks_v,
+                             const int* __restrict__ o_off, float* __restrict__ ctx_out,
+                             int ld_ctx) {
   using Seg = SvSeg<T, BITS>;
   constexpr int COLV = Seg::COLV;
   extern __shared__ __align__(128) uint8_t sv_raw[];
@@ -713,40 +749,23 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
     asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
     if (p0 + SV_HP < s_v) asm volatile("bar.arrive 2, %0;" ::"r"(SV_BLOCK) : "memory");
   }
-}
-
-__global__ void softmax_value_combine_kernel(int n_heads, int s_v, int R_pad,
-                                             const int* __restrict__ ranks_v,
-                                             const int* __restrict__ o_off, int NC, SvPartial part,
-                                             float* __restrict__ ctx, int ld_ctx) {
-  // grid (n_heads, B, column blocks of 128): fixed-order merge of the chunks
-  extern __shared__ float wsm[];  // [NC] chunk weights
-  __shared__ float inv_l;
-  const int head = blockIdx.x, b = blockIdx.y;
-  const size_t base = ((size_t)b * n_heads + head) * NC;
-  if (threadIdx.x < 32) {
-    float M = -INFINITY;
-    for (int c = threadIdx.x; c < NC; c += 32) M = fmaxf(M, part.m[base + c]);
-    M = warp_reduce(M, [](float a, float d) { return fmaxf(a, d); });
-    float L = 0.f;
-    for (int c = threadIdx.x; c < NC; c += 32) {
-      const float l = part.l[base + c];
-      const float w = (l > 0.f) ? expf(part.m[base + c] - M) : 0.f;
-      wsm[c] = w;
-      L += w * l;
-    }
-    L = warp_reduce(L, [](float a, float d) { return a + d; });
-    if (threadIdx.x == 0) inv_l = 1.f / L;
+  if (warp == SV_CONSUMERS) return;
+  // The last CTA of this (sequence, group) to finish merges the chunks.
+  __shared__ unsigned ticket_sh;
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+  if (tid == 0) ticket_sh = atomicAdd(&part.cnt[(size_t)b * G + g], 1u);
+  asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+  if (ticket_sh != (unsigned)(NC - 1)) return;
+  __threadfence();
+  float* wsm = reinterpret_cast<float*>(ring);  // NC weights
+  const int r = ranks_v[g];
+  for (int p = 0; p < s_v; ++p) {
+    const int head = g * s_v + p;
+    sv_merge_head(part, ((size_t)b * n_heads + head) * NC, NC, R_pad, r,
+                  ctx_out + (size_t)b * ld_ctx + o_off[head], wsm, tid, SV_CONSUMERS * 32, 1);
   }
-  __syncthreads();
-  const int r = ranks_v[head / s_v];
-  const int col = blockIdx.z * blockDim.x + threadIdx.x;
-  if (col >= r) return;
-  const float* src = part.ctx + base * R_pad + col;
-  float v = 0.f;
-#pragma unroll 4
-  for (int c = 0; c < NC; ++c) v = fmaf(wsm[c], src[(size_t)c * R_pad], v);
-  ctx[(size_t)b * ld_ctx + o_off[head] + col] = v * inv_l;
+  if (tid == 0) part.cnt[(size_t)b * G + g] = 0u;  // ready for the next launch
 }
 
 __global__ void advance_kernel(int* t_dev) { *t_dev += 1; }
@@ -768,7 +787,7 @@ __global__ void dense_append_kernel(const float* __restrict__ qkv, int n_heads, 
   const size_t row = (((size_t)b * n_heads + i) * T_cap + t) * dh;
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
     double sn, cs;
-    sincos((double)t * theta[j], &sn, &cs);
+    sincos_big((double)t * theta[j], &sn, &cs);
     const double klo = k[j], khi = k[j + half], qlo = q[j], qhi = q[j + half];
     kc[row + j] = from_f<T>((float)(klo * cs - khi * sn));
     kc[row + j + half] = from_f<T>((float)(klo * sn + khi * cs));
@@ -921,12 +940,10 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
     attr = true;
   }
   dim3 grid(NC, G, B);
+  PALU_REQUIRE((size_t)NC * sizeof(float) <= ring, "palu_softmax_value: too many chunks");
   softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_BLOCK, smem, st>>>(
       hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, n_planes, plane, t_dev, NC,
-      Lr, part);
-  PALU_LAUNCHED();
-  softmax_value_combine_kernel<<<dim3(n_heads, B, (R_pad + 127) / 128), 128, NC * sizeof(float),
-                                 st>>>(n_heads, s_v, R_pad, ranks_v, o_off, NC, part, ctx, ld_ctx);
+      Lr, part, ranks_v, o_off, ctx, ld_ctx);
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1044,8 +1061,9 @@ int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* 
 }
 
 int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, int head_dim,
-                      int s_k, const void* bk, int R_pad, const double* theta, float scale,
-                      const int* t_dev, void* uw, int layout, void* stream) {
+                      int s_k, const void* bk, int bk_rows, int R_pad, const double* theta,
+                      float scale, const int* t_dev, void* uw, int layout, void* stream) {
+  PALU_REQUIRE(bk_rows >= R_pad, "palu_query_absorb: bk has %d rows < R_pad %d", bk_rows, R_pad);
   PALU_REQUIRE(head_dim % 2 == 0, "rotary embedding requires an even head_dim");
   PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k,
                n_heads);
@@ -1054,12 +1072,13 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
   const size_t smem = (size_t)33 * head_dim * sizeof(float);
   if (dtype == PALU_DTYPE_BF16)
     query_absorb_kernel<bf16><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
-                                                              (const bf16*)bk, R_pad, theta, scale,
+                                                              (const bf16*)bk, bk_rows, R_pad, theta,
+                                                              scale,
                                                               t_dev, uw, layout);
   else
     query_absorb_kernel<float><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
-                                                               (const float*)bk, R_pad, theta,
-                                                               scale, t_dev, uw, layout);
+                                                               (const float*)bk, bk_rows, R_pad,
+                                                               theta, scale, t_dev, uw, layout);
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1088,7 +1107,9 @@ int palu_rope_score(int dtype, int bits, const void* hk, const float* scales, co
 }
 
 size_t palu_softmax_value_workspace(int B, int n_heads, int R_pad, int n_chunks) {
-  return sizeof(float) * (size_t)B * n_heads * n_chunks * (2 + (size_t)R_pad);
+  // partial (m, l, ctx) per chunk + one ticket per (sequence, group) (zero-initialised)
+  return sizeof(float) * (size_t)B * n_heads * n_chunks * (2 + (size_t)R_pad) +
+         sizeof(unsigned) * (((size_t)B * n_heads + 31) & ~size_t(31));
 }
 
 int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales, const float* zps,
@@ -1125,7 +1146,7 @@ int palu_advance(int* t_dev, void* stream) {
 
 size_t palu_dense_workspace(int B, int n_heads, int head_dim, int n_chunks) {
   return sizeof(float) * ((size_t)B * n_heads * n_chunks * (2 + (size_t)head_dim) +
-                          (size_t)B * n_heads * head_dim);
+                          (size_t)B * n_heads * head_dim + (((size_t)B * n_heads + 31) & ~size_t(31)));
 }
 
 int palu_dense_decode(int dtype, const float* qkv, int B, int n_heads, int head_dim, void* kc,

@@ -221,7 +221,8 @@ constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16
 
 struct Params {
   int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
-  int mode;  // 0 = full; 1 = profiling: epilogue skips the TMEM math (pipeline-only timing)
+  int mode;     // profiling only (bit flags): 1 epilogue skips math; 2 MMA skips TMA waits; 4 MMA skips TMEM-empty waits
+  int pf_dist;  // L2 prefetch distance in work items (0 = off)
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
@@ -325,8 +326,8 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         const int h_row = bg * p.T_cap + tile * TILE_M;
         // warm L2 with this SM's rows of the item PF_DIST ahead: smem holds only
         // ~1.25 items next to the resident UW, so HBM latency must be hidden in L2
-        if (i + PF_DIST < i1) {
-          const int ip = i + PF_DIST;
+        if (p.pf_dist > 0 && i + p.pf_dist < i1) {
+          const int ip = i + p.pf_dist;
           const int bgp = ip / n_super, stp = ip - bgp * n_super;
           const int rowp = bgp * p.T_cap + (2 * stp + (int)rank) * TILE_M;
           for (int kb = 0; kb < kblocks; ++kb) tma_prefetch_l2(&map_h, kb * KB, rowp);
@@ -356,13 +357,13 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         }
         for (int h = 0; h < halves; ++h, ++unit) {
           const int slot = unit & 1;
-          mbar_wait(&tempty[slot], ((unit >> 1) & 1) ^ 1);
+          if ((p.mode & 4) == 0) mbar_wait(&tempty[slot], ((unit >> 1) & 1) ^ 1);
           fence_after();
           const uint32_t d_tmem = tmem_base + slot * N_CTA;
           for (int kb = 0; kb < kblocks; ++kb) {
             const int cnt = kc + kb;
             const int stage = cnt % p.stages;
-            if (h == 0) {
+            if (h == 0 && (p.mode & 2) == 0) {
               mbar_wait(&full[stage], (cnt / p.stages) & 1);
               fence_after();
             }
@@ -422,7 +423,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
         mbar_wait(&tfull[slot], (unit >> 1) & 1);
         fence_after();
         float v[2] = {0.f, 0.f};
-        if (p.mode == 0)
+        if ((p.mode & 1) == 0)
 #pragma unroll
         for (int hp = 0; hp < 2; ++hp) {
           float2 acc2 = make_float2(0.f, 0.f);
@@ -486,7 +487,7 @@ __global__ void rope_table_kernel(const double* __restrict__ theta, int half, in
     const int row = i / half, j = i - row * half;
     const double pos = row < n_tiles ? 128.0 * row : (double)(row - n_tiles);
     double sn, cs;
-    sincos(pos * theta[j], &sn, &cs);
+    sincos_big(pos * theta[j], &sn, &cs);
     tab[i] = make_float2((float)cs, (float)sn);
   }
 }
@@ -604,6 +605,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.n_tab = (T_cap + 127) / 128 + 1;
   prm.stages = stages;
   prm.mode = getenv("PALU_TC_PROFILE_MODE") ? atoi(getenv("PALU_TC_PROFILE_MODE")) : 0;
+  prm.pf_dist = getenv("PALU_TC_PF") ? atoi(getenv("PALU_TC_PF")) : PF_DIST;
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;

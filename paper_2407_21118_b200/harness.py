@@ -188,7 +188,7 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
     g.manual_seed(seed)
     G = n_heads // s
     rk, rv = (rank_k,) * G, (rank_v,) * G
-    rk_pad, rv_pad = _rank_pad(rank_k, dtype), _rank_pad(rank_v, dtype)
+    rk_pad, rv_pad = _round_up(rank_k, 128), _round_up(rank_v, 128)
     ko = n_heads * rank_v
     ko_pad = _round_up(ko, 8)
 
