@@ -27,7 +27,7 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
 // ---------------------------------------------------------------------------
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_UNROLL = 8;  // 16-byte weight loads in flight per lane
+constexpr int GEMV_UNROLL = 16;  // 16-byte weight loads in flight per lane
 
 template <typename T, int MAXB>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
@@ -264,9 +264,37 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   }
   const int width = s_k * dh;
   const T* bg = bk + ((size_t)g * bk_rows + k0) * width + (size_t)p * dh;
-  for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
-    const int kk = idx / dh, c = idx - kk * dh;
-    bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
+  constexpr int V = 16 / (int)sizeof(T);
+  if (dh % V == 0 && (width % V) == 0) {
+    // 16-byte loads, all issued before the shared stores
+    const int per_row = dh / V;
+    for (int base = threadIdx.x; base < nk * per_row; base += 4 * blockDim.x) {
+      uint4 v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < nk * per_row) {
+          const int kk = idx / per_row, c = (idx - kk * per_row) * V;
+          v[u] = *reinterpret_cast<const uint4*>(bg + (size_t)kk * width + c);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < nk * per_row) {
+          const int kk = idx / per_row, c = (idx - kk * per_row) * V;
+          float f[V];
+          Vec16<T>::unpack(v[u], f);
+#pragma unroll
+          for (int e = 0; e < V; ++e) bs[kk * dh + c + e] = f[e];
+        }
+      }
+    }
+  } else {
+    for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
+      const int kk = idx / dh, c = idx - kk * dh;
+      bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
+    }
   }
   __syncthreads();
   if (layout == 0) {
@@ -453,43 +481,64 @@ __host__ __device__ inline SvPartial sv_carve(void* ws, int B, int n, int R_pad,
   return p;
 }
 
-// Fixed-order merge of a head's NC chunk partials (flash-decoding combine):
-// ctx = sum_c e^(m_c - M) ctx_c / sum_c e^(m_c - M) l_c.  nthreads threads.
-__device__ void sv_merge_head(const SvPartial& part, size_t base, int NC, int R_pad, int r,
-                              float* dst, float* wsm, int tid, int nthreads, int bar_id) {
-  __shared__ float inv_l_sh;
-  if (tid < 32) {
+// Fixed-order merge of a group's NC chunk partials (flash-decoding combine)
+// by one CTA of 8 warps: ctx = sum_c e^(m_c - M) ctx_c / sum_c e^(m_c - M) l_c.
+// Warp w takes chunks c = w (mod 8) for every head of the group, lanes take
+// columns; the 8 warp sums are added in a fixed order (deterministic).
+__device__ void sv_merge_group(const SvPartial& part, size_t head_base, int hp, int NC, int R_pad,
+                               int r, float* const* dst, float* sm, int tid) {
+  constexpr int NW = 8;
+  const int warp = tid >> 5, lane = tid & 31;
+  float* wsm = sm;                     // [hp][NC] chunk weights
+  float* inv_l = sm + SV_HP * NC;      // [hp]
+  float* red = inv_l + SV_HP;          // [NW][hp][R_pad]
+  if (warp < hp) {
+    const size_t base = (head_base + warp) * NC;
     float M = -INFINITY;
-    for (int c = tid; c < NC; c += 32) M = fmaxf(M, part.m[base + c]);
+    for (int c = lane; c < NC; c += 32) M = fmaxf(M, part.m[base + c]);
     M = warp_reduce(M, [](float a, float d) { return fmaxf(a, d); });
     float L = 0.f;
-    for (int c = tid; c < NC; c += 32) {
+    for (int c = lane; c < NC; c += 32) {
       const float l = part.l[base + c];
       const float w = (l > 0.f) ? expf(part.m[base + c] - M) : 0.f;
-      wsm[c] = w;
+      wsm[warp * NC + c] = w;
       L += w * l;
     }
     L = warp_reduce(L, [](float a, float d) { return a + d; });
-    if (tid == 0) inv_l_sh = 1.f / L;
+    if (lane == 0) inv_l[warp] = 1.f / L;
   }
-  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
-  const float inv_l = inv_l_sh;
-  const float* src = part.ctx + base * R_pad;
-  for (int col = tid; col < r; col += nthreads) {
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  for (int h = 0; h < hp; ++h) {
+    const float* src = part.ctx + (head_base + h) * NC * (size_t)R_pad;
+    for (int col0 = 0; col0 < r; col0 += 32 * 4) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int c = warp; c < NC; c += NW) {
+        const float w = wsm[h * NC + c];
+        const float* row = src + (size_t)c * R_pad + col0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int col = lane + 32 * k;
+          if (col0 + col < r) acc[k] = fmaf(w, row[col], acc[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int col = col0 + lane + 32 * k;
+        if (col < r) red[((size_t)warp * SV_HP + h) * R_pad + col] = acc[k];
+      }
+    }
+  }
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+  for (int idx = tid; idx < hp * r; idx += NW * 32) {
+    const int h = idx / r, col = idx - h * r;
     float v = 0.f;
-#pragma unroll 8
-    for (int c = 0; c < NC; ++c) v = fmaf(wsm[c], src[(size_t)c * R_pad + col], v);
-    dst[col] = v * inv_l;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) v += red[((size_t)w * SV_HP + h) * R_pad + col];
+    dst[h][col] = v * inv_l[h];
   }
-  asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(nthreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
 }
 
-// Streaming value pass.  A "segment" is what one lane loads per row: 16 B of
-// raw storage (8 bf16 / 4 fp32) or one 4-byte word of packed codes.  Lr
-// lanes cover a row (NSEG segments each), a warp covers 32/Lr rows, 8 warps
-// stream the chunk with 4 rows in flight per lane.  Quantised rows use
-// ctx = sum_t (p_t s_t) code_t - sum_t p_t s_t z_t (the z term per head is
-// accumulated once in the softmax pass).
 template <typename T, int BITS>
 struct SvSeg {
   static constexpr bool RAW = BITS == 16;
@@ -758,12 +807,15 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
   asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
   if (ticket_sh != (unsigned)(NC - 1)) return;
   __threadfence();
-  float* wsm = reinterpret_cast<float*>(ring);  // NC weights
   const int r = ranks_v[g];
-  for (int p = 0; p < s_v; ++p) {
-    const int head = g * s_v + p;
-    sv_merge_head(part, ((size_t)b * n_heads + head) * NC, NC, R_pad, r,
-                  ctx_out + (size_t)b * ld_ctx + o_off[head], wsm, tid, SV_CONSUMERS * 32, 1);
+  for (int p0 = 0; p0 < s_v; p0 += SV_HP) {
+    const int hp = min(SV_HP, s_v - p0);
+    float* dst[SV_HP];
+#pragma unroll
+    for (int h = 0; h < SV_HP; ++h)
+      dst[h] = ctx_out + (size_t)b * ld_ctx + o_off[g * s_v + p0 + min(h, hp - 1)];
+    sv_merge_group(part, (size_t)b * n_heads + g * s_v + p0, hp, NC, R_pad, r, dst,
+                   reinterpret_cast<float*>(ring), tid);
   }
   if (tid == 0) part.cnt[(size_t)b * G + g] = 0u;  // ready for the next launch
 }
@@ -940,7 +992,8 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
     attr = true;
   }
   dim3 grid(NC, G, B);
-  PALU_REQUIRE((size_t)NC * sizeof(float) <= ring, "palu_softmax_value: too many chunks");
+  PALU_REQUIRE(sizeof(float) * ((size_t)SV_HP * NC + SV_HP + (size_t)8 * SV_HP * R_pad) <= ring,
+               "palu_softmax_value: too many chunks for the merge buffer");
   softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_BLOCK, smem, st>>>(
       hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, n_planes, plane, t_dev, NC,
       Lr, part, ranks_v, o_off, ctx, ld_ctx);
