@@ -84,6 +84,17 @@ __device__ __forceinline__ uint32_t packed_code(const uint8_t* row, int row_byte
   return (v >> (bit & 7)) & ((1u << bits) - 1u);
 }
 
+// packed fp32x2 FMA (sm_100 FFMA2): d = a * b + c elementwise
+__device__ __forceinline__ float2 ffma2_f(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
 // Round half away from zero (quant.py:31-32), no contraction.
 __device__ __forceinline__ double round_half_away(double x) {
   return x >= 0.0 ? floor(__dadd_rn(x, 0.5)) : ceil(__dsub_rn(x, 0.5));

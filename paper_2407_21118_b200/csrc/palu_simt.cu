@@ -27,7 +27,7 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
 // ---------------------------------------------------------------------------
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_UNROLL = 16;  // 16-byte weight loads in flight per lane
+constexpr int GEMV_UNROLL = 8;  // 16-byte weight loads in flight per lane
 
 template <typename T, int MAXB>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
@@ -713,14 +713,19 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
-    // (2) reduce the staged rows
-    float acc[SV_HP][NSEG][COLV];
+    // (2) reduce the staged rows (packed FFMA2; probabilities of all SV_HP
+    // head slots are read unconditionally -- slots >= hp hold stale values
+    // whose accumulators are never stored)
+    static_assert(COLV % 2 == 0, "COLV must be even");
+    float2 acc[SV_HP][NSEG][COLV / 2];
 #pragma unroll
     for (int h = 0; h < SV_HP; ++h)
 #pragma unroll
       for (int q = 0; q < NSEG; ++q)
 #pragma unroll
-        for (int e = 0; e < COLV; ++e) acc[h][q][e] = 0.f;
+        for (int e = 0; e < COLV / 2; ++e) acc[h][q][e] = make_float2(0.f, 0.f);
+    const int my_first = warp * RW + rs;
+    const int row_step = SV_CONSUMERS * RW;
     for (int l = 0; l < n_loads; ++l) {
       const int ctr = load_ctr + l;
       const int st = ctr % SV_NSTAGE;
@@ -728,15 +733,16 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
       const int r0 = l * stage_rows;
       const int nr = min(stage_rows, (c1 - c0) - r0);
       const uint8_t* sbase = ring + st * SV_STAGE_BYTES;
-      for (int r = warp * RW + rs; r < nr; r += SV_CONSUMERS * RW) {
+      const float* pst = ps + r0;
+      for (int r = my_first; r < nr; r += row_step) {
         const uint8_t* row = sbase + (size_t)r * row_bytes;
         float pv[SV_HP];
 #pragma unroll
-        for (int h = 0; h < SV_HP; ++h) pv[h] = (h < hp) ? ps[h * clen + r0 + r] : 0.f;
+        for (int h = 0; h < SV_HP; ++h) pv[h] = pst[h * clen + r];
 #pragma unroll
         for (int q = 0; q < NSEG; ++q) {
           const int sg = sb + q * Lr;
-          if (sg < segs) {
+          if (NSEG == 1 || sg < segs) {
             uint4 v;
             if constexpr (Seg::BYTES == 16) {
               v = *reinterpret_cast<const uint4*>(row + sg * 16);
@@ -750,9 +756,12 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
             float f[COLV];
             Seg::unpack(v, f);
 #pragma unroll
-            for (int h = 0; h < SV_HP; ++h)
+            for (int h = 0; h < SV_HP; ++h) {
+              const float2 p2 = make_float2(pv[h], pv[h]);
 #pragma unroll
-              for (int e = 0; e < COLV; ++e) acc[h][q][e] = fmaf(pv[h], f[e], acc[h][q][e]);
+              for (int e = 0; e < COLV / 2; ++e)
+                acc[h][q][e] = ffma2_f(p2, make_float2(f[2 * e], f[2 * e + 1]), acc[h][q][e]);
+            }
           }
         }
       }
@@ -768,9 +777,11 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
 #pragma unroll
       for (int q = 0; q < NSEG; ++q)
 #pragma unroll
-        for (int e = 0; e < COLV; ++e)
-          for (int o = Lr; o < 32; o <<= 1)
-            acc[h][q][e] += __shfl_xor_sync(0xffffffffu, acc[h][q][e], o);
+        for (int e = 0; e < COLV / 2; ++e)
+          for (int o = Lr; o < 32; o <<= 1) {
+            acc[h][q][e].x += __shfl_xor_sync(0xffffffffu, acc[h][q][e].x, o);
+            acc[h][q][e].y += __shfl_xor_sync(0xffffffffu, acc[h][q][e].y, o);
+          }
     asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
     float* red = reinterpret_cast<float*>(ring);  // all stages consumed: reuse
     if (rs == 0) {
@@ -781,8 +792,10 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
           const int sg = sb + q * Lr;
           if (sg < segs)
 #pragma unroll
-            for (int e = 0; e < COLV; ++e)
-              red[((size_t)warp * SV_HP + h) * R_pad + sg * COLV + e] = acc[h][q][e];
+            for (int e = 0; e < COLV / 2; ++e) {
+              red[((size_t)warp * SV_HP + h) * R_pad + sg * COLV + 2 * e] = acc[h][q][e].x;
+              red[((size_t)warp * SV_HP + h) * R_pad + sg * COLV + 2 * e + 1] = acc[h][q][e].y;
+            }
         }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
