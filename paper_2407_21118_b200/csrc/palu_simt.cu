@@ -680,36 +680,86 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
       load_ctr += n_loads;
       continue;
     }
-    // (1) one warp per head: chunk max, exp (x scale when quantised), sums
-    if (warp < hp) {
-      const int head = g * s_v + p0 + warp;
-      const float* lg = logits + ((size_t)b * n_heads + head) * ld_logits;
-      float m = -INFINITY;
-      for (int t = c0 + lane; t < c1; t += 32) {
-        float v = lg[t];
-        for (int pl = 1; pl < n_planes; ++pl) v += lg[pl * plane + t];
-        ps[warp * clen + (t - c0)] = v;
-        m = fmaxf(m, v);
-      }
-      m = warp_reduce(m, [](float a, float d) { return fmaxf(a, d); });
-      float l = 0.f, zs = 0.f;
-      for (int t = c0 + lane; t < c1; t += 32) {
-        float e = expf(ps[warp * clen + (t - c0)] - m);
-        l += e;
-        if constexpr (!Seg::RAW) {
-          const float sc = scales[tok_base + t];
-          zs = fmaf(e * sc, zps[tok_base + t], zs);
-          e *= sc;
+    // (1) softmax statistics of the chunk for the hp heads, all 8 consumer
+    // warps over tokens (independent loads, block reductions)
+    __shared__ float red_m[SV_CONSUMERS][SV_HP], red_l[SV_CONSUMERS][SV_HP],
+        red_z[SV_CONSUMERS][SV_HP];
+    __shared__ float m_sh[SV_HP];
+    {
+      const float* lg[SV_HP];
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h)
+        lg[h] = logits + ((size_t)b * n_heads + g * s_v + p0 + min(h, hp - 1)) * ld_logits;
+      float m[SV_HP];
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h) m[h] = -INFINITY;
+      for (int t = c0 + tid; t < c1; t += SV_CONSUMERS * 32) {
+        float v[SV_HP];
+#pragma unroll
+        for (int h = 0; h < SV_HP; ++h) {
+          v[h] = lg[h][t];
+          for (int pl = 1; pl < n_planes; ++pl) v[h] += lg[h][pl * plane + t];
         }
-        ps[warp * clen + (t - c0)] = e;
+#pragma unroll
+        for (int h = 0; h < SV_HP; ++h) {
+          ps[h * clen + (t - c0)] = v[h];
+          m[h] = fmaxf(m[h], v[h]);
+        }
       }
-      l = warp_reduce(l, [](float a, float d) { return a + d; });
-      zs = warp_reduce(zs, [](float a, float d) { return a + d; });
-      if (lane == 0) {
-        const size_t pi = ((size_t)b * n_heads + head) * NC + c;
-        part.m[pi] = (c0 < c1) ? m : -INFINITY;
-        part.l[pi] = (c0 < c1) ? l : 0.f;
-        zsum[warp] = zs;
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h) {
+        m[h] = warp_reduce(m[h], [](float x, float y) { return fmaxf(x, y); });
+        if (lane == 0) red_m[warp][h] = m[h];
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+      if (tid < SV_HP) {
+        float mm = red_m[0][tid];
+        for (int w = 1; w < SV_CONSUMERS; ++w) mm = fmaxf(mm, red_m[w][tid]);
+        m_sh[tid] = mm;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h) m[h] = m_sh[h];
+      float l[SV_HP], zs[SV_HP];
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h) l[h] = zs[h] = 0.f;
+      for (int t = c0 + tid; t < c1; t += SV_CONSUMERS * 32) {
+        float sc = 1.f, zp = 0.f;
+        if constexpr (!Seg::RAW) {
+          sc = scales[tok_base + t];
+          zp = zps[tok_base + t];
+        }
+#pragma unroll
+        for (int h = 0; h < SV_HP; ++h) {
+          float e = expf(ps[h * clen + (t - c0)] - m[h]);
+          l[h] += e;
+          if constexpr (!Seg::RAW) {
+            zs[h] = fmaf(e * sc, zp, zs[h]);
+            e *= sc;
+          }
+          ps[h * clen + (t - c0)] = e;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < SV_HP; ++h) {
+        l[h] = warp_reduce(l[h], [](float x, float y) { return x + y; });
+        zs[h] = warp_reduce(zs[h], [](float x, float y) { return x + y; });
+        if (lane == 0) {
+          red_l[warp][h] = l[h];
+          red_z[warp][h] = zs[h];
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
+      if (tid < hp) {
+        float ll = 0.f, zz = 0.f;
+        for (int w = 0; w < SV_CONSUMERS; ++w) {
+          ll += red_l[w][tid];
+          zz += red_z[w][tid];
+        }
+        const size_t pi = ((size_t)b * n_heads + g * s_v + p0 + tid) * NC + c;
+        part.m[pi] = (c0 < c1) ? m_sh[tid] : -INFINITY;
+        part.l[pi] = (c0 < c1) ? ll : 0.f;
+        zsum[tid] = zz;
       }
     }
     asm volatile("bar.sync 1, %0;" ::"r"(SV_CONSUMERS * 32) : "memory");
