@@ -21,6 +21,7 @@ reference behaviour):
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -441,6 +442,8 @@ class _Session:
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
         # split-T chunks: ~4 CTAs per SM for the value stream, <= 2048 tokens each
         self.n_chunks = max(-(-4 * sms // (gv * self.B)), -(-self.cap // 2048), 1)
+        if os.environ.get("PALU_SV_CHUNKS"):  # tuning experiments only
+            self.n_chunks = max(int(os.environ["PALU_SV_CHUNKS"]), -(-self.cap // 8192))
         ws = _lib.call("palu_softmax_value_workspace", self.B, self.n, rv, self.n_chunks)
         self.ws = torch.zeros(ws // 4 + 1, dtype=torch.float32, device=dev)
         self.t_dev = torch.tensor([cache.t], dtype=torch.int32, device=dev)
