@@ -20,6 +20,7 @@ from .attention import (
     palu_prefill,
     rope_apply,
 )
+from .dense import DecodeResult, DenseModel, reference_decode
 from .errors import GoldenMismatchError, NumericalError, PaluError, ValidationError
 from .model import (
     AttentionConfig,

@@ -440,8 +440,9 @@ class _Session:
         self.ctx = torch.zeros(self.B, self.ko, dtype=torch.float32, device=dev)
         gv = max(len(L.value_ranks) for L in fused.layers)
         sms = torch.cuda.get_device_properties(dev).multi_processor_count
-        # split-T chunks: ~4 CTAs per SM for the value stream, <= 2048 tokens each
-        self.n_chunks = max(-(-4 * sms // (gv * self.B)), -(-self.cap // 2048), 1)
+        # split-T chunks: one wave of 2 CTAs per SM for the value stream (per-CTA
+        # statistics and merge costs favour few, long chunks), <= 4096 tokens each
+        self.n_chunks = max(-(-2 * sms // (gv * self.B)), -(-self.cap // 4096), 1)
         if os.environ.get("PALU_SV_CHUNKS"):  # tuning experiments only
             self.n_chunks = max(int(os.environ["PALU_SV_CHUNKS"]), -(-self.cap // 8192))
         ws = _lib.call("palu_softmax_value_workspace", self.B, self.n, rv, self.n_chunks)

@@ -249,3 +249,23 @@ def test_tcgen05_score_matches_simt_and_oracle(P, golden, which):
     e_log = rel_err(logits["tcgen05"], logits["simt"])
     assert e_log < 5e-3, (e_log, logits["tcgen05"][0, :6], logits["simt"][0, :6])
     assert rel_err(out["tcgen05"], case["out1"]) < TOL["bfloat16"]
+
+
+def test_reference_decode_uncompressed_baseline(P, golden):
+    """K0 (attention.py:133-168 on the GPU) against the reference's own
+    reference_decode outputs stored in the golden fixture."""
+    g = golden("small_decode.npz")
+    done = 0
+    for ci, name in enumerate(g["names"]):
+        p = f"c{ci}_"
+        if p + "reference_decode" not in g:
+            continue
+        case = small_case(g, ci)
+        if not case["rope"]:
+            continue
+        w, dec, cfg = _to_types(P, case["layers"], case["n"], case["dh"], True, case["base"])
+        res = P.reference_decode(w, cfg, case["tokens"])
+        worst = max(rel_err(res.outputs[t], g[p + "reference_decode"][t]) for t in range(case["T"]))
+        assert worst < 1e-5, (name, worst)
+        done += 1
+    assert done >= 2
