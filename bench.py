@@ -40,6 +40,8 @@ def parse():
     ap.add_argument("--batch", type=int, default=1, help="sequences per GPU")
     ap.add_argument("--layers", type=int, default=LAYERS)
     ap.add_argument("--bits", type=int, default=16)
+    ap.add_argument("--rank-k", type=int, default=RANK, help="kept key rank per group (256 = uniform 50%%)")
+    ap.add_argument("--rank-v", type=int, default=RANK, help="kept value rank per group (paper preset: 128/384)")
     ap.add_argument("--dtype", default="bfloat16")
     ap.add_argument("--score-kernel", default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
@@ -305,7 +307,8 @@ def main():
     extra = 2 * (K + W) + 16
     weights, fused, cache = synthetic_engine(layers=args.layers, batch=args.batch,
                                              context=args.context, extra=extra, bits=args.bits,
-                                             dtype=args.dtype, seed=1234 + rank)
+                                             dtype=args.dtype, seed=1234 + rank,
+                                             rank_k=args.rank_k, rank_v=args.rank_v)
     sess = _session(fused, cache, score_kernel=args.score_kernel)
     sess.x.copy_(torch.randn(args.batch, D, device="cuda") * 0.5)
     torch.cuda.synchronize()
@@ -367,12 +370,12 @@ def main():
     n_groups = NH // GS
     score_name = "palu_rope_score_tc" if "palu_rope_score_tc" in prof else "palu_rope_score"
     score_ms = statistics.mean(prof[score_name])
-    flops = 2.0 * T1 * NH * RANK * DH * args.batch  # reconstruction, one layer
-    lat_bytes = T1 * n_groups * RANK * 2 * args.batch  # H_k stream bf16
+    flops = 2.0 * T1 * NH * args.rank_k * DH * args.batch  # reconstruction, one layer
+    lat_bytes = T1 * n_groups * args.rank_k * 2 * args.batch  # H_k stream bf16
     achieved_tf = flops / (score_ms * 1e-3) / 1e12
     total_kernel_ms = sum(sum(v) for v in prof.values())
     sv_ms = statistics.mean(prof["palu_softmax_value"])
-    latent_total = T1 * n_groups * (RANK + RANK) * 2 * args.batch
+    latent_total = T1 * n_groups * (args.rank_k + args.rank_v) * 2 * args.batch
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
                 "frac": achieved_tf / tf_sus, "traffic": None, "peak_source": f"{src} sustained bf16",
                 "kernel": score_name, "kernel_ms": score_ms,
@@ -400,7 +403,8 @@ def main():
             "warmup": W, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16" if args.dtype == "bfloat16" else "f32",
             "data": "synthetic (random-init weights, N(0,1/9) latent cache rows)",
-            "config": {"workload": "llama2-7b-32L-palu50-gs4-r256-rope", "context": args.context,
+            "config": {"workload": f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-rope",
+                       "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
                        "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                        "layers": args.layers, "bits": args.bits, "parallelism": f"replicas{world}",
                        "l2": "inputs larger than L2 (latent cache 17 GB/step)"},

@@ -252,6 +252,9 @@ MEDIUM_CASES = [
     ("med_g2_b16_4", 512, 4, 128, 2, [64, 64], 2, [96, 64], 250, (16, 4), 1e6, 2.0, True),
     ("med_mixed_gran", 512, 4, 128, 1, [32, 16, 24, 8], 4, [128], 130, 16, 10000.0, 2.0, False),
     ("med_b8_b3", 256, 2, 128, 2, [48], 1, [40, 24], 140, (8, 3), 10000.0, 2.0, True),
+    # the paper's Palu-50% latency preset: kept K 25% / V 75%
+    ("med_preset_k128_v384", 512, 4, 128, 4, [128], 4, [384], 300, 16, 10000.0, 2.0, False),
+    ("med_preset_b4v", 512, 4, 128, 4, [128], 4, [384], 260, (16, 4), 10000.0, 2.0, True),
 ]
 
 
