@@ -368,19 +368,21 @@ def main():
     hbm, tf_burst, tf_sus, src = _peaks()
     T1 = args.context + W + K + 1  # rows scored in the profiled step (approx.)
     n_groups = NH // GS
-    score_name = "palu_rope_score_tc" if "palu_rope_score_tc" in prof else "palu_rope_score"
+    for score_name in ("palu_rope_attend_tc", "palu_rope_score_tc", "palu_rope_score"):
+        if score_name in prof:
+            break
     score_ms = statistics.mean(prof[score_name])
     flops = 2.0 * T1 * NH * args.rank_k * DH * args.batch  # reconstruction, one layer
     lat_bytes = T1 * n_groups * args.rank_k * 2 * args.batch  # H_k stream bf16
     achieved_tf = flops / (score_ms * 1e-3) / 1e12
     total_kernel_ms = sum(sum(v) for v in prof.values())
-    sv_ms = statistics.mean(prof["palu_softmax_value"])
+    sv_ms = statistics.mean(prof["palu_softmax_value"]) if "palu_softmax_value" in prof else 0.0
     latent_total = T1 * n_groups * (args.rank_k + args.rank_v) * 2 * args.batch
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
                 "frac": achieved_tf / tf_sus, "traffic": None, "peak_source": f"{src} sustained bf16",
                 "kernel": score_name, "kernel_ms": score_ms,
                 "share_of_step": sum(prof[score_name]) / total_kernel_ms,
-                "score_hbm_gbs": lat_bytes / (score_ms * 1e-3) / 1e9,
+                "score_hbm_gbs": (latent_total if sv_ms == 0.0 else lat_bytes) / (score_ms * 1e-3) / 1e9,
                 "latent_stream_gbs": latent_total / ((score_ms + sv_ms) * 1e-3) / 1e9,
                 "hbm_peak_gbs": hbm,
                 "per_kernel_ms": {k: statistics.mean(v) for k, v in prof.items()}}
@@ -397,7 +399,7 @@ def main():
         cpu = cpu_baseline(args.context, args.layers, args.batch)
 
     if rank == 0:
-        launches_per_step = args.layers * 8 + 1
+        launches_per_step = sum(len(v) for v in prof.values())
         line = {
             "metric": METRIC, "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": K,
             "warmup": W, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",

@@ -131,6 +131,25 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
                        size_t plane_stride, void* stream);
 
+/*
+ * Fused RoPE score + softmax + value path (attention.py:433-446, 350-362 up
+ * to wo_fused): one persistent grid whose CTA pairs [0, score_sms/2) run the
+ * tcgen05 score pipeline of palu_rope_score_tc and publish per-tile
+ * readiness, while the remaining CTAs stream H_v (bf16 [B][G][T_cap][Rv_pad])
+ * with TMA bulk copies, softmax each value chunk and merge them -- the value
+ * stream overlaps the tensor-bound reconstruction.  Output as
+ * palu_softmax_value (ctx[b][o_off[i] + c]); logits is scratch.  K and V
+ * must share the group size s.  score_sms <= 0 picks the split from a
+ * per-SM throughput model.  workspace: palu_rope_attend_workspace() bytes,
+ * zero-initialised once (all counters reset themselves).
+ */
+size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap);
+int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int s, int G,
+                        int Rk_pad, int Rv_pad, int T_cap, const void* uw, const float* rope_tab,
+                        const int* t_dev, float* logits, int ld_logits, const int* ranks_v,
+                        const int* o_off, float* ctx, int ld_ctx, void* workspace,
+                        int score_sms, void* stream);
+
 /* cos/sin tables for palu_rope_score_tc: [T_cap/128 + 1][64 pairs] tile bases
  * (fp64-reduced) followed by [128][64] in-tile offsets, float2 each. */
 int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, void* stream);

@@ -367,8 +367,8 @@ class LatentKVCache:
                            self.device),
                 _SideStore(rv, v_bits, _rank_pad(max(rv), dtype, v_bits), batch, cap, dtype,
                            self.device)))
-        if score_kernel not in ("auto", "simt", "tcgen05"):
-            raise ValidationError(f"score_kernel must be auto|simt|tcgen05, got {score_kernel!r}")
+        if score_kernel not in ("auto", "simt", "tcgen05", "fused"):
+            raise ValidationError(f"score_kernel must be auto|simt|tcgen05|fused, got {score_kernel!r}")
         self.score_kernel = score_kernel
         self._session = None
 
@@ -457,7 +457,7 @@ class _Session:
             K = cache._stores[li][0]
             ok = (fused.dtype == "bfloat16" and K.bits == FP_BITS and self.dh == 128
                   and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
-            if score_kernel == "tcgen05" and not ok:
+            if score_kernel in ("tcgen05", "fused") and not ok:
                 raise ValidationError(f"layer {li}: shape not supported by the tcgen05 score kernel")
             ks = _lib.call("palu_rope_score_tc_splits", L.s_k, K.r_pad) if ok else 0
             ok = ok and 1 <= ks <= 2
@@ -466,6 +466,21 @@ class _Session:
             self.tc_layers.append(ok and score_kernel != "simt")
         self.planes = [(_lib.call("palu_rope_score_tc_splits", L.s_k, c._stores[li][0].r_pad)
                         if self.tc_layers[li] else 1) for li, L in enumerate(fused.layers)]
+        # fused score + softmax + value (grid-level role split): bf16 raw K and V,
+        # K and V sharing the head grouping
+        self.fused_layers = []
+        for li, L in enumerate(fused.layers):
+            K, V = c._stores[li]
+            ok = (self.tc_layers[li] and V.bits == FP_BITS and L.s_v == L.s_k
+                  and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512
+                  and score_kernel in ("auto", "fused"))
+            self.fused_layers.append(ok)
+        self.ws_fused = None
+        if any(self.fused_layers):
+            nbytes = max(_lib.call("palu_rope_attend_workspace", self.B, self.n, V.G, V.r_pad, self.cap)
+                         for (K, V) in c._stores)
+            self.ws_fused = torch.zeros(nbytes // 4 + 1, dtype=torch.float32, device=dev)
+        self.score_sms = int(os.environ.get("PALU_SCORE_SMS", "0"))
         self.uw_bf = None
         self.rope_tab = None
         if any(self.tc_layers):
@@ -498,6 +513,17 @@ class _Session:
         _lib.call("palu_latent_append", code, V.bits, yp + 4 * (d + sk_sum), B, self.n1, V.G,
                   _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev), _ptr(V.rows), _ptr(V.scales),
                   _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64), V.r_pad, V.cap, _ptr(self.t_dev), st)
+        if self.fused_layers[li]:
+            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
+                      L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
+                      _ptr(self.uw_bf), 1, st)
+            _lib.call("palu_rope_attend_tc", _ptr(K.rows), _ptr(V.rows), B, n, L.s_k, K.G, K.r_pad,
+                      V.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab), _ptr(self.t_dev),
+                      _ptr(self.logits), self.ld_logits, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev),
+                      _ptr(self.ctx), self.ko, _ptr(self.ws_fused), self.score_sms, st)
+            _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
+                      _ptr(x), d, 0, st)
+            return
         if self.tc_layers[li]:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),

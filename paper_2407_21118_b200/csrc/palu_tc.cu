@@ -32,8 +32,12 @@ constexpr int BASE_BYTES = 64 * 8; // 64 float2
 constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
 constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16
 
+struct VParams;  // value role of the fused kernel (below)
+
 struct Params {
   int B, n_heads, s_k, G, R_pad, T_cap, ld_logits, n_tab, stages;
+  int score_pairs;  // CTA pairs running the score role (fused kernel); all pairs otherwise
+  int* ready;       // fused: per work item, epilogue warps that published its logits
   int mode;     // profiling only (bit flags): 1 epilogue skips math; 2 MMA skips TMA waits; 4 MMA skips TMEM-empty waits
   int pf_dist;  // L2 prefetch distance in work items (0 = off)
   const float2* rope_tab;  // [n_tab + 128][64]
@@ -49,12 +53,8 @@ struct Params {
 // whose rows 128 r .. land in SM r's TMEM.  Each SM's epilogue reduces its
 // own 128 tokens x 2 heads per head pair.  Every latent byte crosses L2 -> SM
 // once and both SMs' tensor pipes run at the 2-SM rate.
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
-                     const __grid_constant__ CUtensorMap map_uw, const Params p) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+__device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUtensorMap& map_uw,
+                                           const Params& p, uint8_t* smem) {
   const int kblocks = p.R_pad / KB;
   const int halves = p.s_k / 2;
   uint8_t* s_uw = smem;                                  // [kblocks][halves] x 16 KB
@@ -75,7 +75,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
-  const int pair_id = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+  const int pair_id = blockIdx.x >> 1, n_pairs = p.score_pairs;
   const int T_rows = *p.t_dev + 1;
   const int n_super = (T_rows + SUPER - 1) / SUPER;
   const int total = p.B * p.G * n_super;
@@ -277,6 +277,12 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
             lg[0] = v0;
             lg[p.ld_logits] = v1;
           }
+          if (p.ready != nullptr && h == halves - 1) {
+            // publish this warp's logits of the item to the value role
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(&p.ready[i], 1);
+          }
         }
       }
     }
@@ -287,6 +293,302 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
+                     const __grid_constant__ CUtensorMap map_uw, const Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  score_role(map_h, map_uw, p, smem);
+}
+
+// ===========================================================================
+// Fused score + softmax + value kernel (grid-level role split).
+//
+// The reconstruction is tensor-bound and the value stream is HBM-bound, so
+// one persistent grid runs both concurrently on disjoint SMs: CTA pairs
+// [0, score_pairs) run score_role and publish per-item readiness; the other
+// CTAs run value_role: they walk the value chunks in the order the score
+// pairs complete them, wait for their items, and stream the chunk's H_v rows
+// through a deep TMA bulk-copy ring while computing the chunk softmax
+// statistics and p . H_v partials; the last chunk of each (sequence, group)
+// merges them in a fixed order (deterministic).  attention.py:433-446.
+// ===========================================================================
+struct VParams {
+  const uint8_t* hv;  // [B][G][T_cap][Rv_pad] bf16
+  int Rv_pad, vc;     // value row width; score items per value chunk
+  int v_stages;       // TMA ring depth of the value role
+  unsigned* tickets;  // [B*G]
+  float *pm, *pl, *pctx;  // partials [B][n][NCmax] / [B][n][NCmax][Rv_pad]
+  int nc_max;
+  const int* ranks_v;
+  const int* o_off;
+  float* ctx_out;
+  int ld_ctx;
+};
+
+constexpr int V_STAGE = 16384;
+constexpr int V_HP = 4;
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int NSEG>
+__device__ void value_role(const Params& p, const VParams& vp, uint8_t* smem, int vcta,
+                           int n_vctas) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int T_rows = *p.t_dev + 1;
+  const int n_super = (T_rows + SUPER - 1) / SUPER;
+  const int total = p.B * p.G * n_super;
+  const int per = (total + p.score_pairs - 1) / p.score_pairs;
+  const int n_vc = (n_super + vp.vc - 1) / vp.vc;  // value chunks per (b, g)
+  const int s_v = p.s_k;
+  const int row_bytes = vp.Rv_pad * 2;
+  const int segs = row_bytes / 16;
+  const int Lr = 32;  // one row per warp step (segs <= 64 -> NSEG <= 2)
+  const int stage_rows = V_STAGE / row_bytes;
+  const int max_tok = vp.vc * SUPER;
+  uint8_t* ring = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + vp.v_stages * V_STAGE);
+  uint64_t* empty = full + vp.v_stages;
+  float* ps = reinterpret_cast<float*>(empty + vp.v_stages);  // [V_HP][max_tok]
+  __shared__ float red_m[8][V_HP], red_l[8][V_HP], m_sh[V_HP];
+  __shared__ unsigned ticket_sh;
+
+  if (tid == 0) {
+    for (int st = 0; st < vp.v_stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+
+  int load_ctr = 0, k = 0;
+  for (int off = 0; off < per; ++off) {
+    for (int pr = 0; pr < p.score_pairs; ++pr) {
+      const int L = pr * per + off;
+      if (L >= total || L >= (pr + 1) * per) continue;
+      const int st_last = L % n_super;
+      if ((st_last + 1) % vp.vc != 0 && st_last != n_super - 1) continue;  // not a chunk end
+      if ((k++) % n_vctas != vcta) continue;
+      const int bg = L / n_super, b = bg / p.G, g = bg - b * p.G;
+      const int c = st_last / vp.vc;
+      const int item0 = bg * n_super + c * vp.vc;
+      const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
+      // ---- wait until the score role published every item of the chunk
+      if (tid == 0) {
+        for (int it = item0; it <= L; ++it)
+          while (ld_acquire_u32(&p.ready[it]) < 2u * (EPI_WARPS / 2)) __nanosleep(200);
+      }
+      __syncthreads();
+      const uint8_t* src0 = vp.hv + ((size_t)bg * p.T_cap + c0) * row_bytes;
+      const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
+      for (int p0 = 0; p0 < s_v; p0 += V_HP) {
+        const int hp = min(V_HP, s_v - p0);
+        if (warp == 8) {
+          if (lane == 0) {
+            for (int l = 0; l < n_loads; ++l) {
+              const int ctr = load_ctr + l;
+              const int st = ctr % vp.v_stages;
+              mbar_wait(&empty[st], ((ctr / vp.v_stages) & 1) ^ 1);
+              const int nr = min(stage_rows, (c1 - c0) - l * stage_rows);
+              mbar_expect_tx(&full[st], (uint32_t)(nr * row_bytes));
+              bulk_load(ring + st * V_STAGE, src0 + (size_t)l * stage_rows * row_bytes,
+                        (uint32_t)(nr * row_bytes), &full[st]);
+            }
+          }
+        } else if (warp < 8) {
+          // (1) chunk softmax statistics for hp heads (logits via L2: written by
+          //     the score role in this launch)
+          float m[V_HP];
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
+          for (int t = c0 + tid; t < c1; t += 256) {
+#pragma unroll
+            for (int h = 0; h < V_HP; ++h) {
+              const int hh = min(h, hp - 1);
+              const float v = __ldcg(p.logits + ((size_t)b * p.n_heads + g * s_v + p0 + hh) *
+                                                    p.ld_logits + t);
+              ps[h * max_tok + (t - c0)] = v;
+              m[h] = fmaxf(m[h], v);
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) {
+            m[h] = warp_reduce(m[h], [](float x, float y) { return fmaxf(x, y); });
+            if (lane == 0) red_m[warp][h] = m[h];
+          }
+          named_bar_sync(1, 256);
+          if (tid < V_HP) {
+            float mm = red_m[0][tid];
+            for (int w = 1; w < 8; ++w) mm = fmaxf(mm, red_m[w][tid]);
+            m_sh[tid] = mm;
+          }
+          named_bar_sync(1, 256);
+          float l[V_HP];
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) {
+            m[h] = m_sh[h];
+            l[h] = 0.f;
+          }
+          for (int t = c0 + tid; t < c1; t += 256) {
+#pragma unroll
+            for (int h = 0; h < V_HP; ++h) {
+              const float e = __expf(ps[h * max_tok + (t - c0)] - m[h]);
+              ps[h * max_tok + (t - c0)] = e;
+              l[h] += e;
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) {
+            l[h] = warp_reduce(l[h], [](float x, float y) { return x + y; });
+            if (lane == 0) red_l[warp][h] = l[h];
+          }
+          named_bar_sync(1, 256);
+          const size_t chunk_id = (size_t)bg * vp.nc_max + c;
+          if (tid < hp) {
+            float ll = 0.f;
+            for (int w = 0; w < 8; ++w) ll += red_l[w][tid];
+            const size_t pi = ((size_t)b * p.n_heads + g * s_v + p0 + tid) * vp.nc_max + c;
+            vp.pm[pi] = m_sh[tid];
+            vp.pl[pi] = ll;
+          }
+          (void)chunk_id;
+          // (2) stream the staged rows: one row per warp step, lanes over 16-B segments
+          float2 acc[V_HP][NSEG][4];
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h)
+#pragma unroll
+            for (int q2 = 0; q2 < NSEG; ++q2)
+#pragma unroll
+              for (int e = 0; e < 4; ++e) acc[h][q2][e] = make_float2(0.f, 0.f);
+          for (int l2 = 0; l2 < n_loads; ++l2) {
+            const int ctr = load_ctr + l2;
+            const int st = ctr % vp.v_stages;
+            mbar_wait(&full[st], (ctr / vp.v_stages) & 1);
+            const int r0 = l2 * stage_rows;
+            const int nr = min(stage_rows, (c1 - c0) - r0);
+            const uint8_t* sbase = ring + st * V_STAGE;
+            const float* pst = ps + r0;
+            for (int r = warp; r < nr; r += 8) {
+              const uint8_t* row = sbase + (size_t)r * row_bytes;
+              float pv[V_HP];
+#pragma unroll
+              for (int h = 0; h < V_HP; ++h) pv[h] = pst[h * max_tok + r];
+#pragma unroll
+              for (int q2 = 0; q2 < NSEG; ++q2) {
+                const int sg = lane + q2 * Lr;
+                if (NSEG == 1 || sg < segs) {
+                  const uint4 v = *reinterpret_cast<const uint4*>(row + sg * 16);
+                  float f[8];
+                  Vec16<bf16>::unpack(v, f);
+#pragma unroll
+                  for (int h = 0; h < V_HP; ++h) {
+                    const float2 p2 = make_float2(pv[h], pv[h]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e)
+                      acc[h][q2][e] = ffma2(p2, make_float2(f[2 * e], f[2 * e + 1]), acc[h][q2][e]);
+                  }
+                }
+              }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+          }
+          // (3) cross-warp reduction through the (fully consumed) ring
+          named_bar_sync(1, 256);
+          float* red = reinterpret_cast<float*>(ring);
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h)
+#pragma unroll
+            for (int q2 = 0; q2 < NSEG; ++q2) {
+              const int sg = lane + q2 * Lr;
+              if (sg < segs)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e] = acc[h][q2][e].x;
+                  red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e + 1] = acc[h][q2][e].y;
+                }
+            }
+          named_bar_sync(1, 256);
+          for (int idx = tid; idx < hp * vp.Rv_pad; idx += 256) {
+            const int h = idx / vp.Rv_pad, col = idx - h * vp.Rv_pad;
+            float v = 0.f;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
+            vp.pctx[(((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max + c) * vp.Rv_pad + col] = v;
+          }
+          named_bar_sync(1, 256);
+        }
+        load_ctr += n_loads;
+        __syncthreads();  // the ring is reused by the next pass / chunk
+      }
+      // ---- consume readiness (reset for the next launch) and merge if last
+      if (tid == 0)
+        for (int it = item0; it <= L; ++it) p.ready[it] = 0;
+      __threadfence();
+      __syncthreads();
+      if (tid == 0) ticket_sh = atomicAdd(&vp.tickets[bg], 1u);
+      __syncthreads();
+      if (ticket_sh == (unsigned)(n_vc - 1)) {
+        __threadfence();
+        const int r = vp.ranks_v[g];
+        float* wsm = reinterpret_cast<float*>(ring);
+        for (int hh = 0; hh < s_v; ++hh) {
+          const int head = g * s_v + hh;
+          const size_t base = ((size_t)b * p.n_heads + head) * vp.nc_max;
+          __shared__ float inv_l;
+          if (warp == 0) {
+            float M = -INFINITY;
+            for (int cc = lane; cc < n_vc; cc += 32) M = fmaxf(M, __ldcg(vp.pm + base + cc));
+            M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
+            float Ls = 0.f;
+            for (int cc = lane; cc < n_vc; cc += 32) {
+              const float w = __expf(__ldcg(vp.pm + base + cc) - M);
+              wsm[cc] = w;
+              Ls += w * __ldcg(vp.pl + base + cc);
+            }
+            Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
+            if (lane == 0) inv_l = 1.f / Ls;
+          }
+          __syncthreads();
+          float* dst = vp.ctx_out + (size_t)b * vp.ld_ctx + vp.o_off[head];
+          for (int col = tid; col < r; col += blockDim.x) {
+            float v = 0.f;
+            for (int cc = 0; cc < n_vc; ++cc)
+              v = fmaf(wsm[cc], __ldcg(vp.pctx + (base + cc) * vp.Rv_pad + col), v);
+            dst[col] = v * inv_l;
+          }
+          __syncthreads();
+        }
+        if (tid == 0) vp.tickets[bg] = 0u;
+        __syncthreads();
+      }
+    }
+  }
+}
+
+template <int NSEG>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
+                      const __grid_constant__ CUtensorMap map_uw, const Params p,
+                      const VParams vp) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  if ((int)(blockIdx.x >> 1) < p.score_pairs) {
+    score_role(map_h, map_uw, p, smem);
+  } else {
+    const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
+    value_role<NSEG>(p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
   }
 }
 
@@ -417,12 +719,137 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.ld_logits = ld_logits;
   prm.n_tab = (T_cap + 127) / 128 + 1;
   prm.stages = stages;
+  prm.score_pairs = (sms & ~1) / 2;
+  prm.ready = nullptr;
   prm.mode = getenv("PALU_TC_PROFILE_MODE") ? atoi(getenv("PALU_TC_PROFILE_MODE")) : 0;
   prm.pf_dist = getenv("PALU_TC_PF") ? atoi(getenv("PALU_TC_PF")) : PF_DIST;
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
   rope_score_tc_kernel<<<dim3(sms & ~1), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+// ---- fused score + softmax + value ------------------------------------------
+static int fused_nc_max(int T_cap, int vc) {
+  using palu::tc::SUPER;
+  const int n_super = (T_cap + SUPER - 1) / SUPER;
+  return (n_super + vc - 1) / vc;
+}
+
+size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap) {
+  using palu::tc::SUPER;
+  const int vc = 4;
+  const int nc = fused_nc_max(T_cap, vc);
+  const size_t items = (size_t)B * G * ((T_cap + SUPER - 1) / SUPER);
+  const size_t head = (size_t)B * n_heads * nc;
+  return 256 + sizeof(unsigned) * (size_t)B * G + sizeof(int) * items + sizeof(float) * head * 2 +
+         sizeof(float) * head * (size_t)Rv_pad + 1024;
+}
+
+int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int s, int G,
+                        int Rk_pad, int Rv_pad, int T_cap, const void* uw, const float* rope_tab,
+                        const int* t_dev, float* logits, int ld_logits, const int* ranks_v,
+                        const int* o_off, float* ctx, int ld_ctx, void* workspace,
+                        int score_sms, void* stream) {
+  using namespace palu::tc;
+  if (!palu_rope_score_tc_splits(s, Rk_pad) || G * s != n_heads || (Rv_pad * 2) % 16 != 0 ||
+      Rv_pad > 512) {
+    set_error("palu_rope_attend_tc: unsupported shape (Rk %d, Rv %d, s %d)", Rk_pad, Rv_pad, s);
+    return PALU_EUNSUPPORTED;
+  }
+  PALU_REQUIRE(((uintptr_t)hk & 15) == 0 && ((uintptr_t)uw & 15) == 0 && ((uintptr_t)hv & 15) == 0,
+               "tc: unaligned operands");
+  CUtensorMap map_h, map_uw;
+  int rc = make_map_2d(&map_h, hk, Rk_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  if (rc) return rc;
+  rc = make_map_2d(&map_uw, uw, Rk_pad, (uint64_t)B * G * s * 128, KB, TILE_M);
+  if (rc) return rc;
+  const int kblocks = Rk_pad / KB;
+  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + BASE_RING * BASE_BYTES + 1024 +
+                    2 * 2 * TILE_M * 4;
+  int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
+  if (stages > 12) stages = 12;
+  PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
+  const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  sms &= ~1;
+  if (score_sms <= 0) {
+    // balance tensor time against value-stream time (per-SM rates measured on B200:
+    // ~8.5 TFLOP/s of reconstruction, ~100 GB/s of value streaming per SM)
+    const double flops = 2.0 * n_heads * (double)Rk_pad * 128.0;   // per token
+    const double bytes = (double)G * Rv_pad * 2.0;                  // per token
+    const double ts = flops / 8.5e12, tv = bytes / 1.0e11;
+    score_sms = (int)(sms * ts / (ts + tv) + 0.5);
+  }
+  score_sms &= ~1;
+  if (score_sms < 2) score_sms = 2;
+  if (score_sms > sms - 2) score_sms = sms - 2;
+  const int vc = 4;
+  const int nc_max = fused_nc_max(T_cap, vc);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  unsigned* tickets = reinterpret_cast<unsigned*>(ws + 256);
+  int* ready = reinterpret_cast<int*>(tickets + (size_t)B * G);
+  const size_t items = (size_t)B * G * ((T_cap + SUPER - 1) / SUPER);
+  float* pm = reinterpret_cast<float*>(ready + items);
+  float* pl = pm + (size_t)B * n_heads * nc_max;
+  float* pctx = pl + (size_t)B * n_heads * nc_max;
+  Params prm;
+  prm.B = B;
+  prm.n_heads = n_heads;
+  prm.s_k = s;
+  prm.G = G;
+  prm.R_pad = Rk_pad;
+  prm.T_cap = T_cap;
+  prm.ld_logits = ld_logits;
+  prm.n_tab = (T_cap + 127) / 128 + 1;
+  prm.stages = stages;
+  prm.score_pairs = score_sms / 2;
+  prm.ready = ready;
+  prm.mode = 0;
+  prm.pf_dist = PF_DIST;
+  prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
+  prm.t_dev = t_dev;
+  prm.logits = logits;
+  VParams vp;
+  vp.hv = reinterpret_cast<const uint8_t*>(hv);
+  vp.Rv_pad = Rv_pad;
+  vp.vc = vc;
+  const size_t ps_bytes = (size_t)V_HP * vc * SUPER * sizeof(float);
+  vp.v_stages = (int)((smem - 1024 - ps_bytes - 1024) / V_STAGE);
+  PALU_REQUIRE(vp.v_stages >= 3 && (size_t)8 * V_HP * Rv_pad * 4 <= (size_t)vp.v_stages * V_STAGE,
+               "palu_rope_attend_tc: value ring too small");
+  vp.tickets = tickets;
+  vp.pm = pm;
+  vp.pl = pl;
+  vp.pctx = pctx;
+  vp.nc_max = nc_max;
+  vp.ranks_v = ranks_v;
+  vp.o_off = o_off;
+  vp.ctx_out = ctx;
+  vp.ld_ctx = ld_ctx;
+  const int nseg = (Rv_pad * 2 / 16 + 31) / 32;
+  static bool attr1 = false, attr2 = false;
+  if (nseg == 1) {
+    if (!attr1) {
+      PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<1>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+      attr1 = true;
+    }
+    rope_attend_tc_kernel<1><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
+                                                                                 prm, vp);
+  } else {
+    if (!attr2) {
+      PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<2>,
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+      attr2 = true;
+    }
+    rope_attend_tc_kernel<2><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
+                                                                                 prm, vp);
+  }
   PALU_LAUNCHED();
   return PALU_OK;
 }

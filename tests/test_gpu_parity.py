@@ -269,3 +269,30 @@ def test_reference_decode_uncompressed_baseline(P, golden):
         assert worst < 1e-5, (name, worst)
         done += 1
     assert done >= 2
+
+
+@pytest.mark.parametrize("which", ["c1", "med_preset_k128_v384", "med_g4_r256"])
+def test_fused_attend_matches_oracle(P, golden, which):
+    """Grid-level fused score + softmax + value kernel (palu_rope_attend_tc)
+    against the fp64 oracle and the unfused tcgen05 path, over two steps."""
+    from paper_2407_21118_b200.harness import fill_cache_direct, set_cache_t
+    if which == "c1":
+        case = c1_case(golden("c1_step.npz"), "b16")
+    else:
+        g = golden("medium_step.npz")
+        case = medium_case(g, list(g["names"]).index(which))
+    w, dec, cfg = _to_types(P, [case["layer"]], case["n"], case["dh"], True, case["base"])
+    fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
+    outs = {}
+    for sk in ("tcgen05", "fused"):
+        cache = P.LatentKVCache(dec, cfg, 16, dtype="bfloat16", capacity=case["T"] + 8,
+                                score_kernel=sk)
+        fill_cache_direct(cache, 0, case["x_rows"])
+        set_cache_t(cache, case["T"])
+        y1 = P.palu_decode_step_rope(w, fused, cache, case["x_t"])
+        y2 = P.palu_decode_step_rope(w, fused, cache, y1)  # second step: graph replay path
+        assert any(cache._session.fused_layers) == (sk == "fused")
+        outs[sk] = (y1, y2)
+    assert rel_err(outs["fused"][0], case["out1"]) < TOL["bfloat16"]
+    assert rel_err(outs["fused"][0], outs["tcgen05"][0]) < 2e-3
+    assert rel_err(outs["fused"][1], outs["tcgen05"][1]) < 5e-3
