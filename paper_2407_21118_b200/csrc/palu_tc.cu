@@ -769,7 +769,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   const int kblocks = Rk_pad / KB;
   const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + BASE_RING * BASE_BYTES + 1024 +
                     2 * 2 * TILE_M * 4;
-  int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
+  const int dyn_limit = SMEM_LIMIT - 2048;  // the value role has ~1 KB of static smem
+  int stages = (dyn_limit - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
   PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
   const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
@@ -836,7 +837,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   if (nseg == 1) {
     if (!attr1) {
       PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
       attr1 = true;
     }
     rope_attend_tc_kernel<1><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
@@ -844,7 +845,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   } else {
     if (!attr2) {
       PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
       attr2 = true;
     }
     rope_attend_tc_kernel<2><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
