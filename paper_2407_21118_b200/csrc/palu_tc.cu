@@ -339,6 +339,29 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   return v;
 }
 
+// Completion-ordered list of this value CTA's chunks: chunk ends are score
+// items L = pr * per + off visited offset-major, so the k-th chunk of the list
+// becomes ready at about the k-th fraction of the score role's run.
+struct VChunkIter {
+  int per, total, pairs, n_super, vc, vcta, n_vctas;
+  int off, pr, k;
+  __device__ bool next(int& L) {
+    for (; off < per; ++off, pr = 0) {
+      for (; pr < pairs; ++pr) {
+        const int cand = pr * per + off;
+        if (cand >= total || cand >= (pr + 1) * per) continue;
+        const int st = cand % n_super;
+        if ((st + 1) % vc != 0 && st != n_super - 1) continue;
+        if ((k++) % n_vctas != vcta) continue;
+        L = cand;
+        ++pr;
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
 template <int NSEG>
 __device__ void value_role(const Params& p, const VParams& vp, uint8_t* smem, int vcta,
                            int n_vctas) {
@@ -351,14 +374,16 @@ __device__ void value_role(const Params& p, const VParams& vp, uint8_t* smem, in
   const int s_v = p.s_k;
   const int row_bytes = vp.Rv_pad * 2;
   const int segs = row_bytes / 16;
-  const int Lr = 32;  // one row per warp step (segs <= 64 -> NSEG <= 2)
   const int stage_rows = V_STAGE / row_bytes;
   const int max_tok = vp.vc * SUPER;
+  // smem: ring | red [8][V_HP][Rv_pad] | ps [V_HP][max_tok] | wsm [V_HP][n_vc] | barriers
   uint8_t* ring = smem;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ring + vp.v_stages * V_STAGE);
+  float* red = reinterpret_cast<float*>(ring + vp.v_stages * V_STAGE);
+  float* ps = red + 8 * V_HP * vp.Rv_pad;
+  float* wsm = ps + V_HP * max_tok;
+  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + V_HP * vp.nc_max);
   uint64_t* empty = full + vp.v_stages;
-  float* ps = reinterpret_cast<float*>(empty + vp.v_stages);  // [V_HP][max_tok]
-  __shared__ float red_m[8][V_HP], red_l[8][V_HP], m_sh[V_HP];
+  __shared__ float red_m[8][V_HP], red_l[8][V_HP], m_sh[V_HP], inv_l[V_HP];
   __shared__ unsigned ticket_sh;
 
   if (tid == 0) {
@@ -370,209 +395,232 @@ __device__ void value_role(const Params& p, const VParams& vp, uint8_t* smem, in
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   __syncthreads();
+  VChunkIter iter{per, total, p.score_pairs, n_super, vp.vc, vcta, n_vctas, 0, 0, 0};
 
-  int load_ctr = 0, k = 0;
-  for (int off = 0; off < per; ++off) {
-    for (int pr = 0; pr < p.score_pairs; ++pr) {
-      const int L = pr * per + off;
-      if (L >= total || L >= (pr + 1) * per) continue;
-      const int st_last = L % n_super;
-      if ((st_last + 1) % vp.vc != 0 && st_last != n_super - 1) continue;  // not a chunk end
-      if ((k++) % n_vctas != vcta) continue;
-      const int bg = L / n_super, b = bg / p.G, g = bg - b * p.G;
-      const int c = st_last / vp.vc;
-      const int item0 = bg * n_super + c * vp.vc;
-      const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
-      // ---- wait until the score role published every item of the chunk
-      if (tid == 0) {
-        for (int it = item0; it <= L; ++it)
-          while (ld_acquire_u32(&p.ready[it]) < 2u * (EPI_WARPS / 2)) __nanosleep(200);
-      }
-      __syncthreads();
-      const uint8_t* src0 = vp.hv + ((size_t)bg * p.T_cap + c0) * row_bytes;
-      const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
-      for (int p0 = 0; p0 < s_v; p0 += V_HP) {
-        const int hp = min(V_HP, s_v - p0);
-        if (warp == 8) {
-          if (lane == 0) {
-            for (int l = 0; l < n_loads; ++l) {
-              const int ctr = load_ctr + l;
-              const int st = ctr % vp.v_stages;
-              mbar_wait(&empty[st], ((ctr / vp.v_stages) & 1) ^ 1);
-              const int nr = min(stage_rows, (c1 - c0) - l * stage_rows);
-              mbar_expect_tx(&full[st], (uint32_t)(nr * row_bytes));
-              bulk_load(ring + st * V_STAGE, src0 + (size_t)l * stage_rows * row_bytes,
-                        (uint32_t)(nr * row_bytes), &full[st]);
-            }
-          }
-        } else if (warp < 8) {
-          // (1) chunk softmax statistics for hp heads (logits via L2: written by
-          //     the score role in this launch)
-          float m[V_HP];
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
-          for (int t = c0 + tid; t < c1; t += 256) {
-#pragma unroll
-            for (int h = 0; h < V_HP; ++h) {
-              const int hh = min(h, hp - 1);
-              const float v = __ldcg(p.logits + ((size_t)b * p.n_heads + g * s_v + p0 + hh) *
-                                                    p.ld_logits + t);
-              ps[h * max_tok + (t - c0)] = v;
-              m[h] = fmaxf(m[h], v);
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) {
-            m[h] = warp_reduce(m[h], [](float x, float y) { return fmaxf(x, y); });
-            if (lane == 0) red_m[warp][h] = m[h];
-          }
-          named_bar_sync(1, 256);
-          if (tid < V_HP) {
-            float mm = red_m[0][tid];
-            for (int w = 1; w < 8; ++w) mm = fmaxf(mm, red_m[w][tid]);
-            m_sh[tid] = mm;
-          }
-          named_bar_sync(1, 256);
-          float l[V_HP];
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) {
-            m[h] = m_sh[h];
-            l[h] = 0.f;
-          }
-          for (int t = c0 + tid; t < c1; t += 256) {
-#pragma unroll
-            for (int h = 0; h < V_HP; ++h) {
-              const float e = __expf(ps[h * max_tok + (t - c0)] - m[h]);
-              ps[h * max_tok + (t - c0)] = e;
-              l[h] += e;
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) {
-            l[h] = warp_reduce(l[h], [](float x, float y) { return x + y; });
-            if (lane == 0) red_l[warp][h] = l[h];
-          }
-          named_bar_sync(1, 256);
-          const size_t chunk_id = (size_t)bg * vp.nc_max + c;
-          if (tid < hp) {
-            float ll = 0.f;
-            for (int w = 0; w < 8; ++w) ll += red_l[w][tid];
-            const size_t pi = ((size_t)b * p.n_heads + g * s_v + p0 + tid) * vp.nc_max + c;
-            vp.pm[pi] = m_sh[tid];
-            vp.pl[pi] = ll;
-          }
-          (void)chunk_id;
-          // (2) stream the staged rows: one row per warp step, lanes over 16-B segments
-          float2 acc[V_HP][NSEG][4];
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h)
-#pragma unroll
-            for (int q2 = 0; q2 < NSEG; ++q2)
-#pragma unroll
-              for (int e = 0; e < 4; ++e) acc[h][q2][e] = make_float2(0.f, 0.f);
-          for (int l2 = 0; l2 < n_loads; ++l2) {
-            const int ctr = load_ctr + l2;
+  if (warp == 8) {
+    // ---------------- producer: H_v rows do not depend on the score role, so
+    // stream every chunk of the list back to back (bounded by the ring)
+    if (lane == 0) {
+      int L, ctr = 0;
+      while (iter.next(L)) {
+        const int bg = L / n_super, st_last = L % n_super, c = st_last / vp.vc;
+        const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
+        const uint8_t* src0 = vp.hv + ((size_t)bg * p.T_cap + c0) * row_bytes;
+        const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
+        for (int pass = 0; pass < s_v; pass += V_HP) {
+          for (int l = 0; l < n_loads; ++l, ++ctr) {
             const int st = ctr % vp.v_stages;
-            mbar_wait(&full[st], (ctr / vp.v_stages) & 1);
-            const int r0 = l2 * stage_rows;
-            const int nr = min(stage_rows, (c1 - c0) - r0);
-            const uint8_t* sbase = ring + st * V_STAGE;
-            const float* pst = ps + r0;
-            for (int r = warp; r < nr; r += 8) {
-              const uint8_t* row = sbase + (size_t)r * row_bytes;
-              float pv[V_HP];
-#pragma unroll
-              for (int h = 0; h < V_HP; ++h) pv[h] = pst[h * max_tok + r];
-#pragma unroll
-              for (int q2 = 0; q2 < NSEG; ++q2) {
-                const int sg = lane + q2 * Lr;
-                if (NSEG == 1 || sg < segs) {
-                  const uint4 v = *reinterpret_cast<const uint4*>(row + sg * 16);
-                  float f[8];
-                  Vec16<bf16>::unpack(v, f);
-#pragma unroll
-                  for (int h = 0; h < V_HP; ++h) {
-                    const float2 p2 = make_float2(pv[h], pv[h]);
-#pragma unroll
-                    for (int e = 0; e < 4; ++e)
-                      acc[h][q2][e] = ffma2(p2, make_float2(f[2 * e], f[2 * e + 1]), acc[h][q2][e]);
-                  }
-                }
-              }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
+            mbar_wait(&empty[st], ((ctr / vp.v_stages) & 1) ^ 1);
+            const int nr = min(stage_rows, (c1 - c0) - l * stage_rows);
+            mbar_expect_tx(&full[st], (uint32_t)(nr * row_bytes));
+            bulk_load(ring + st * V_STAGE, src0 + (size_t)l * stage_rows * row_bytes,
+                      (uint32_t)(nr * row_bytes), &full[st]);
           }
-          // (3) cross-warp reduction through the (fully consumed) ring
-          named_bar_sync(1, 256);
-          float* red = reinterpret_cast<float*>(ring);
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h)
-#pragma unroll
-            for (int q2 = 0; q2 < NSEG; ++q2) {
-              const int sg = lane + q2 * Lr;
-              if (sg < segs)
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e] = acc[h][q2][e].x;
-                  red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e + 1] = acc[h][q2][e].y;
-                }
-            }
-          named_bar_sync(1, 256);
-          for (int idx = tid; idx < hp * vp.Rv_pad; idx += 256) {
-            const int h = idx / vp.Rv_pad, col = idx - h * vp.Rv_pad;
-            float v = 0.f;
-#pragma unroll
-            for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
-            vp.pctx[(((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max + c) * vp.Rv_pad + col] = v;
-          }
-          named_bar_sync(1, 256);
         }
-        load_ctr += n_loads;
-        __syncthreads();  // the ring is reused by the next pass / chunk
-      }
-      // ---- consume readiness (reset for the next launch) and merge if last
-      if (tid == 0)
-        for (int it = item0; it <= L; ++it) p.ready[it] = 0;
-      __threadfence();
-      __syncthreads();
-      if (tid == 0) ticket_sh = atomicAdd(&vp.tickets[bg], 1u);
-      __syncthreads();
-      if (ticket_sh == (unsigned)(n_vc - 1)) {
-        __threadfence();
-        const int r = vp.ranks_v[g];
-        float* wsm = reinterpret_cast<float*>(ring);
-        for (int hh = 0; hh < s_v; ++hh) {
-          const int head = g * s_v + hh;
-          const size_t base = ((size_t)b * p.n_heads + head) * vp.nc_max;
-          __shared__ float inv_l;
-          if (warp == 0) {
-            float M = -INFINITY;
-            for (int cc = lane; cc < n_vc; cc += 32) M = fmaxf(M, __ldcg(vp.pm + base + cc));
-            M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
-            float Ls = 0.f;
-            for (int cc = lane; cc < n_vc; cc += 32) {
-              const float w = __expf(__ldcg(vp.pm + base + cc) - M);
-              wsm[cc] = w;
-              Ls += w * __ldcg(vp.pl + base + cc);
-            }
-            Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
-            if (lane == 0) inv_l = 1.f / Ls;
-          }
-          __syncthreads();
-          float* dst = vp.ctx_out + (size_t)b * vp.ld_ctx + vp.o_off[head];
-          for (int col = tid; col < r; col += blockDim.x) {
-            float v = 0.f;
-            for (int cc = 0; cc < n_vc; ++cc)
-              v = fmaf(wsm[cc], __ldcg(vp.pctx + (base + cc) * vp.Rv_pad + col), v);
-            dst[col] = v * inv_l;
-          }
-          __syncthreads();
-        }
-        if (tid == 0) vp.tickets[bg] = 0u;
-        __syncthreads();
       }
     }
+    return;
+  }
+  if (warp > 8) return;
+  // ---------------- consumers (warps 0..7) ----------------
+  int L, ctr = 0;
+  while (iter.next(L)) {
+    const int bg = L / n_super, b = bg / p.G, g = bg - b * p.G;
+    const int st_last = L % n_super, c = st_last / vp.vc;
+    const int item0 = bg * n_super + c * vp.vc;
+    const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
+    const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
+    if (tid == 0) {
+      for (int it = item0; it <= L; ++it)
+        while (ld_acquire_u32(&p.ready[it]) < 2u * (EPI_WARPS / 2)) __nanosleep(128);
+    }
+    named_bar_sync(1, 256);
+    for (int p0 = 0; p0 < s_v; p0 += V_HP) {
+      const int hp = min(V_HP, s_v - p0);
+      // (1) chunk softmax statistics (logits via L2: written by the score role)
+      const float* lg[V_HP];
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+        lg[h] = p.logits + ((size_t)b * p.n_heads + g * s_v + p0 + min(h, hp - 1)) * p.ld_logits;
+      float m[V_HP];
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
+      for (int t0 = c0 + tid; t0 < c1; t0 += 4 * 256) {
+        float v[4][V_HP];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h)
+            v[u][h] = (t0 + u * 256 < c1) ? __ldcg(lg[h] + t0 + u * 256) : -INFINITY;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) {
+            if (t0 + u * 256 < c1) ps[h * max_tok + (t0 + u * 256 - c0)] = v[u][h];
+            m[h] = fmaxf(m[h], v[u][h]);
+          }
+      }
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) {
+        m[h] = warp_reduce(m[h], [](float x, float y) { return fmaxf(x, y); });
+        if (lane == 0) red_m[warp][h] = m[h];
+      }
+      named_bar_sync(1, 256);
+      if (tid < V_HP) {
+        float mm = red_m[0][tid];
+        for (int w = 1; w < 8; ++w) mm = fmaxf(mm, red_m[w][tid]);
+        m_sh[tid] = mm;
+      }
+      named_bar_sync(1, 256);
+      float l[V_HP];
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) {
+        m[h] = m_sh[h];
+        l[h] = 0.f;
+      }
+      for (int t = c0 + tid; t < c1; t += 256) {
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h) {
+          const float e = __expf(ps[h * max_tok + (t - c0)] - m[h]);
+          ps[h * max_tok + (t - c0)] = e;
+          l[h] += e;
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) {
+        l[h] = warp_reduce(l[h], [](float x, float y) { return x + y; });
+        if (lane == 0) red_l[warp][h] = l[h];
+      }
+      named_bar_sync(1, 256);
+      if (tid < hp) {
+        float ll = 0.f;
+        for (int w = 0; w < 8; ++w) ll += red_l[w][tid];
+        const size_t pi = ((size_t)b * p.n_heads + g * s_v + p0 + tid) * vp.nc_max + c;
+        vp.pm[pi] = m_sh[tid];
+        vp.pl[pi] = ll;
+      }
+      // (2) reduce the staged rows: one row per warp step, lanes over 16-B segments
+      float2 acc[V_HP][NSEG][4];
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+#pragma unroll
+        for (int q2 = 0; q2 < NSEG; ++q2)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[h][q2][e] = make_float2(0.f, 0.f);
+      for (int l2 = 0; l2 < n_loads; ++l2, ++ctr) {
+        const int st = ctr % vp.v_stages;
+        mbar_wait(&full[st], (ctr / vp.v_stages) & 1);
+        const int r0 = l2 * stage_rows;
+        const int nr = min(stage_rows, (c1 - c0) - r0);
+        const uint8_t* sbase = ring + st * V_STAGE;
+        const float* pst = ps + r0;
+        for (int r = warp; r < nr; r += 8) {
+          const uint8_t* row = sbase + (size_t)r * row_bytes;
+          float pv[V_HP];
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) pv[h] = pst[h * max_tok + r];
+#pragma unroll
+          for (int q2 = 0; q2 < NSEG; ++q2) {
+            const int sg = lane + q2 * 32;
+            if (NSEG == 1 || sg < segs) {
+              const uint4 v = *reinterpret_cast<const uint4*>(row + sg * 16);
+              float f[8];
+              Vec16<bf16>::unpack(v, f);
+#pragma unroll
+              for (int h = 0; h < V_HP; ++h) {
+                const float2 p2 = make_float2(pv[h], pv[h]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                  acc[h][q2][e] = ffma2(p2, make_float2(f[2 * e], f[2 * e + 1]), acc[h][q2][e]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+      }
+      // (3) cross-warp reduction -> chunk partial
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+#pragma unroll
+        for (int q2 = 0; q2 < NSEG; ++q2) {
+          const int sg = lane + q2 * 32;
+          if (sg < segs)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e] = acc[h][q2][e].x;
+              red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e + 1] = acc[h][q2][e].y;
+            }
+        }
+      named_bar_sync(1, 256);
+      for (int idx = tid; idx < hp * vp.Rv_pad; idx += 256) {
+        const int h = idx / vp.Rv_pad, col = idx - h * vp.Rv_pad;
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
+        vp.pctx[(((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max + c) * vp.Rv_pad + col] = v;
+      }
+      named_bar_sync(1, 256);
+    }
+    // ---- consume readiness (reset for the next launch) and merge if last
+    if (tid == 0)
+      for (int it = item0; it <= L; ++it) p.ready[it] = 0;
+    __threadfence();
+    named_bar_sync(1, 256);
+    if (tid == 0) ticket_sh = atomicAdd(&vp.tickets[bg], 1u);
+    named_bar_sync(1, 256);
+    if (ticket_sh != (unsigned)(n_vc - 1)) continue;
+    __threadfence();
+    const int r = vp.ranks_v[g];
+    for (int p0 = 0; p0 < s_v; p0 += V_HP) {
+      const int hp = min(V_HP, s_v - p0);
+      if (warp < hp) {
+        const size_t base = ((size_t)b * p.n_heads + g * s_v + p0 + warp) * vp.nc_max;
+        float M = -INFINITY;
+        for (int cc = lane; cc < n_vc; cc += 32) M = fmaxf(M, __ldcg(vp.pm + base + cc));
+        M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
+        float Ls = 0.f;
+        for (int cc = lane; cc < n_vc; cc += 32) {
+          const float w = __expf(__ldcg(vp.pm + base + cc) - M);
+          wsm[warp * vp.nc_max + cc] = w;
+          Ls += w * __ldcg(vp.pl + base + cc);
+        }
+        Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
+        if (lane == 0) inv_l[warp] = 1.f / Ls;
+      }
+      named_bar_sync(1, 256);
+      // chunk-parallel: warp w sums chunks w, w + 8, ...; lanes over columns
+      for (int h = 0; h < hp; ++h) {
+        const float* src =
+            vp.pctx + ((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max * (size_t)vp.Rv_pad;
+        for (int col0 = 0; col0 < r; col0 += 128) {
+          float a4[4] = {0.f, 0.f, 0.f, 0.f};
+          for (int cc = warp; cc < n_vc; cc += 8) {
+            const float w = wsm[h * vp.nc_max + cc];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int col = col0 + lane + 32 * q;
+              if (col < r) a4[q] = fmaf(w, __ldcg(src + (size_t)cc * vp.Rv_pad + col), a4[q]);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int col = col0 + lane + 32 * q;
+            if (col < r) red[((size_t)warp * V_HP + h) * vp.Rv_pad + col] = a4[q];
+          }
+        }
+      }
+      named_bar_sync(1, 256);
+      for (int idx = tid; idx < hp * r; idx += 256) {
+        const int h = idx / r, col = idx - h * r;
+        float v = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
+        vp.ctx_out[(size_t)b * vp.ld_ctx + vp.o_off[g * s_v + p0 + h] + col] = v * inv_l[h];
+      }
+      named_bar_sync(1, 256);
+    }
+    if (tid == 0) vp.tickets[bg] = 0u;
   }
 }
 
@@ -819,10 +867,11 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   vp.hv = reinterpret_cast<const uint8_t*>(hv);
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
-  const size_t ps_bytes = (size_t)V_HP * vc * SUPER * sizeof(float);
-  vp.v_stages = (int)((smem - 1024 - ps_bytes - 1024) / V_STAGE);
-  PALU_REQUIRE(vp.v_stages >= 3 && (size_t)8 * V_HP * Rv_pad * 4 <= (size_t)vp.v_stages * V_STAGE,
-               "palu_rope_attend_tc: value ring too small");
+  const size_t side = sizeof(float) * ((size_t)8 * V_HP * Rv_pad + (size_t)V_HP * vc * SUPER +
+                                       (size_t)V_HP * nc_max) + 64 * 16 + 1024;
+  vp.v_stages = (int)(((long long)smem - 1024 - (long long)side) / V_STAGE);
+  PALU_REQUIRE(vp.v_stages >= 3, "palu_rope_attend_tc: value ring too small (%d)", vp.v_stages);
+  if (vp.v_stages > 32) vp.v_stages = 32;
   vp.tickets = tickets;
   vp.pm = pm;
   vp.pl = pl;
