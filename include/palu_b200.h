@@ -135,13 +135,16 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
  * Fused RoPE score + softmax + value path (attention.py:433-446, 350-362 up
  * to wo_fused): one persistent grid whose CTA pairs [0, score_sms/2) run the
  * tcgen05 score pipeline of palu_rope_score_tc and publish per-tile
- * readiness, while the remaining CTAs stream H_v (bf16 [B][G][T_cap][Rv_pad])
- * with TMA bulk copies, softmax each value chunk and merge them -- the value
- * stream overlaps the tensor-bound reconstruction.  Output as
- * palu_softmax_value (ctx[b][o_off[i] + c]); logits is scratch.  K and V
- * must share the group size s.  score_sms <= 0 picks the split from a
- * per-SM throughput model.  workspace: palu_rope_attend_workspace() bytes,
- * zero-initialised once (all counters reset themselves).
+ * readiness, while the remaining CTAs stream H_v (bf16 [B][G][T_cap][Rv_pad],
+ * Rv_pad % 64 == 0, <= 512) as swizzled 2-D TMA boxes and reduce it on
+ * tcgen05 (D[128 cols x 16] += H_v^T x P^T, P = hi + lo bf16 probabilities
+ * written by CUDA cores), merging per-unit partials in a fixed order.
+ * Output as palu_softmax_value (ctx[b][o_off[i] + c]); logits is scratch.  K
+ * and V must share the group size s (<= 4).  score_sms <= 0 picks the split
+ * from a per-SM throughput model.  workspace: palu_rope_attend_workspace()
+ * bytes, zero-initialised once (all counters reset themselves).  Selected
+ * only with score_kernel="fused" (the unfused tcgen05 path is faster on
+ * B200 at the bench shapes).
  */
 size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap);
 int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int s, int G,
@@ -149,6 +152,15 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
                         const int* t_dev, float* logits, int ld_logits, const int* ranks_v,
                         const int* o_off, float* ctx, int ld_ctx, void* workspace,
                         int score_sms, void* stream);
+
+/* Diagnostics for the fused kernel (not on the product path): with
+ * PALU_FUSED_TRACE set, palu_rope_attend_tc records a per-CTA timeline
+ * ([CTA][512] u64: start ns, end ns, SM id, role/count, event times) that
+ * palu_fused_trace copies to host (returns the CTA count);
+ * palu_fused_max_clusters reports how many 2-CTA clusters of the fused
+ * kernel can be co-resident at the given dynamic shared memory size. */
+int palu_fused_trace(unsigned long long* host, size_t max_ctas);
+int palu_fused_max_clusters(int smem_bytes);
 
 /* cos/sin tables for palu_rope_score_tc: [T_cap/128 + 1][64 pairs] tile bases
  * (fp64-reduced) followed by [128][64] in-tile offsets, float2 each. */

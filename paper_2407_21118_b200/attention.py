@@ -472,8 +472,8 @@ class _Session:
         for li, L in enumerate(fused.layers):
             K, V = c._stores[li]
             ok = (self.tc_layers[li] and V.bits == FP_BITS and L.s_v == L.s_k
-                  and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512
-                  and score_kernel in ("auto", "fused"))
+                  and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512 and V.r_pad % 64 == 0
+                  and score_kernel == "fused")
             self.fused_layers.append(ok)
         self.ws_fused = None
         if any(self.fused_layers):

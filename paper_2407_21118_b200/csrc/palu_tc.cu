@@ -43,7 +43,20 @@ struct Params {
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
+  unsigned long long* trace;  // diagnostics only (PALU_FUSED_TRACE): [CTA][TRACE_STRIDE]
 };
+
+constexpr int TRACE_STRIDE = 512;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid_u32() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 
 // Work item = (sequence b, key group g, 256-token super-tile) for a CTA pair
 // (cluster of 2, cta_group::2).  SM r of the pair loads tokens
@@ -277,6 +290,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             lg[0] = v0;
             lg[p.ld_logits] = v1;
           }
+          if (p.trace != nullptr && warp == 2 && lane == 0 && h == halves - 1 && it < TRACE_STRIDE - 8)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + it] = gtimer();
           if (p.ready != nullptr && h == halves - 1) {
             // publish this warp's logits of the item to the value role
             __threadfence();
@@ -293,6 +308,10 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   if (warp == 1) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 1] = gtimer();
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 3] = i1 - i0;
   }
 }
 
@@ -311,27 +330,31 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
 // The reconstruction is tensor-bound and the value stream is HBM-bound, so
 // one persistent grid runs both concurrently on disjoint SMs: CTA pairs
 // [0, score_pairs) run score_role and publish per-item readiness; the other
-// CTAs run value_role: they walk the value chunks in the order the score
-// pairs complete them, wait for their items, and stream the chunk's H_v rows
-// through a deep TMA bulk-copy ring while computing the chunk softmax
-// statistics and p . H_v partials; the last chunk of each (sequence, group)
-// merges them in a fixed order (deterministic).  attention.py:433-446.
+// CTAs run value_role.  A value CTA walks its sub-units (VSched) in the order
+// the score pairs complete them; per sub-unit its 8 worker warps turn the
+// logits into softmax statistics and bf16 probabilities P (written straight
+// into a K-major SW128 smem operand), a TMA warp streams H_v as 2-D swizzled
+// boxes {64 columns, 128 tokens}, and one thread issues
+//   D[128 columns x 16 heads] += H_v^T (MN-major) x P^T     (tcgen05, TMEM)
+// per 128-column pair.  The workers read D back (double-buffered) into a
+// per-sub-unit partial; the sub-unit that completes a (sequence, group)
+// merges its partials in token order (deterministic).  attention.py:433-446.
 // ===========================================================================
 struct VParams {
-  const uint8_t* hv;  // [B][G][T_cap][Rv_pad] bf16
-  int Rv_pad, vc;     // value row width; score items per value chunk
-  int v_stages;       // TMA ring depth of the value role
-  unsigned* tickets;  // [B*G]
-  float *pm, *pl, *pctx;  // partials [B][n][NCmax] / [B][n][NCmax][Rv_pad]
-  int nc_max;
+  int Rv_pad, vc;     // value row width; score items per value unit window
+  int v_stages;       // TMA ring depth of the value role (32 KB stages)
+  unsigned* tickets;  // [B*G] super-tiles merged so far
+  float *pm, *pl, *pctx;  // partials [B][n][ns] / [B][n][ns][Rv_pad]
+  int ns_cap;  // partial slots per head: super-tiles per group at capacity
   const int* ranks_v;
   const int* o_off;
   float* ctx_out;
   int ld_ctx;
 };
 
-constexpr int V_STAGE = 16384;
-constexpr int V_HP = 4;
+constexpr int V_STAGE = 32768;  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
+constexpr int V_HP = 4;         // heads per group handled by the value role
+constexpr int V_TMEM_COLS = 128;
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   uint32_t v;
@@ -339,304 +362,401 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   return v;
 }
 
-// Completion-ordered list of this value CTA's chunks: chunk ends are score
-// items L = pr * per + off visited offset-major, so the k-th chunk of the list
-// becomes ready at about the k-th fraction of the score role's run.
-struct VChunkIter {
-  int per, total, pairs, n_super, vc, vcta, n_vctas;
-  int off, pr, k;
-  __device__ bool next(int& L) {
-    for (; off < per; ++off, pr = 0) {
-      for (; pr < pairs; ++pr) {
-        const int cand = pr * per + off;
-        if (cand >= total || cand >= (pr + 1) * per) continue;
-        const int st = cand % n_super;
-        if ((st + 1) % vc != 0 && st != n_super - 1) continue;
-        if ((k++) % n_vctas != vcta) continue;
-        L = cand;
-        ++pr;
-        return true;
-      }
-    }
-    return false;
+struct VUnit {
+  int bg, st0, st1, item0;
+};
+
+// Value units.  The score role gives pair pr the contiguous items
+// [pr * per, (pr + 1) * per) and walks them in order, so unit window (pr, w)
+// = items [pr * per + w * vc, + vc) clipped to the pair's block becomes ready
+// at about (w + 1) / W of the score run.  Windows are handed out w-major
+// (round robin over value CTAs) and split at (sequence, group) boundaries;
+// a sub-unit's partial lives at slot = its first super-tile within the group.
+struct VSched {
+  int per, total, pairs, n_super, vc, W;
+  __device__ __forceinline__ int win_end(int a) const {
+    const int pr = a / per;
+    const int w = (a - pr * per) / vc;
+    return min(min(pr * per + (w + 1) * vc, (pr + 1) * per), total);
   }
 };
 
-template <int NSEG>
-__device__ void value_role(const Params& p, const VParams& vp, uint8_t* smem, int vcta,
-                           int n_vctas) {
+// This value CTA's sub-units, in order (every role of the CTA runs its own copy)
+struct VIter {
+  VSched s;
+  int step, u, a, e;
+  __device__ VIter(const VSched& sch, int vcta, int n_vctas)
+      : s(sch), step(n_vctas), u(vcta - n_vctas), a(0), e(0) {}
+  __device__ __forceinline__ bool next(VUnit& o) {
+    while (a >= e) {
+      u += step;
+      if (u >= s.W * s.pairs) return false;
+      const int w = u / s.pairs, pr = u - w * s.pairs;
+      a = pr * s.per + w * s.vc;
+      e = min(min(a + s.vc, (pr + 1) * s.per), s.total);
+    }
+    const int bg = a / s.n_super;
+    const int se = min(e, (bg + 1) * s.n_super);
+    o = VUnit{bg, a - bg * s.n_super, se - bg * s.n_super, a};
+    a = se;
+    return true;
+  }
+};
+
+__device__ void value_role(const CUtensorMap& map_v, const Params& p, const VParams& vp,
+                           uint8_t* smem, int vcta, int n_vctas) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int T_rows = *p.t_dev + 1;
   const int n_super = (T_rows + SUPER - 1) / SUPER;
   const int total = p.B * p.G * n_super;
   const int per = (total + p.score_pairs - 1) / p.score_pairs;
-  const int n_vc = (n_super + vp.vc - 1) / vp.vc;  // value chunks per (b, g)
+  const VSched sch{per, total, p.score_pairs, n_super, vp.vc, (per + vp.vc - 1) / vp.vc};
   const int s_v = p.s_k;
-  const int row_bytes = vp.Rv_pad * 2;
-  const int segs = row_bytes / 16;
-  const int stage_rows = V_STAGE / row_bytes;
+  const int NJ = (vp.Rv_pad + 127) / 128;  // 128-column pairs of 64-column boxes
+  const int ns = vp.ns_cap;
+  const int vs = vp.v_stages;
   const int max_tok = vp.vc * SUPER;
-  // smem: ring | red [8][V_HP][Rv_pad] | ps [V_HP][max_tok] | wsm [V_HP][n_vc] | barriers
+  const int PB = max_tok / 64 * 1024;  // P bytes per buffer: 1 KB per 64 tokens
+  // smem: ring | P[2] (+1 KB: rows 8..15 of the last block alias past it) |
+  //       logits [2][V_HP][max_tok] | wsm [V_HP][ns] | ulist [ns] | red [4][128] |
+  //       barriers | TMEM slot
   uint8_t* ring = smem;
-  float* red = reinterpret_cast<float*>(ring + vp.v_stages * V_STAGE);
-  float* ps = red + 8 * V_HP * vp.Rv_pad;
-  float* wsm = ps + V_HP * max_tok;
-  uint64_t* full = reinterpret_cast<uint64_t*>(wsm + V_HP * vp.nc_max);
-  uint64_t* empty = full + vp.v_stages;
-  __shared__ float red_m[8][V_HP], red_l[8][V_HP], m_sh[V_HP], inv_l[V_HP];
+  uint8_t* pbuf = ring + vs * V_STAGE;
+  float* lbuf = reinterpret_cast<float*>(pbuf + 2 * PB + 1024);
+  float* wsm = lbuf + 2 * V_HP * max_tok;
+  int* ulist = reinterpret_cast<int*>(wsm + V_HP * ns);
+  float* red = reinterpret_cast<float*>(ulist + ((ns + 3) & ~3));
+  uint64_t* full = reinterpret_cast<uint64_t*>(red + 4 * 128);
+  uint64_t* empty = full + vs;
+  uint64_t* pfull = empty + vs;   // [2] P buffer written
+  uint64_t* dfull = pfull + 2;    // [2] accumulator complete
+  uint64_t* dempty = dfull + 2;   // [2] accumulator read back
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  __shared__ float red_m[4][V_HP], red_l[4][V_HP], inv_l[V_HP];
   __shared__ unsigned ticket_sh;
+  __shared__ int nu_sh, go_sh;
 
   if (tid == 0) {
-    for (int st = 0; st < vp.v_stages; ++st) {
+    for (int st = 0; st < vs; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 8);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&pfull[a], 1);
+      mbar_init(&dfull[a], 1);
+      mbar_init(&dempty[a], 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tslot)),
+                 "r"(V_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
   __syncthreads();
-  VChunkIter iter{per, total, p.score_pairs, n_super, vp.vc, vcta, n_vctas, 0, 0, 0};
+  fence_after();
+  const uint32_t tmem = *tslot;
+  VIter it(sch, vcta, n_vctas);
+  VUnit u;
 
   if (warp == 8) {
-    // ---------------- producer: H_v rows do not depend on the score role, so
-    // stream every chunk of the list back to back (bounded by the ring)
+    // ---------------- TMA producer: H_v does not depend on the score role,
+    // so it streams every sub-unit back to back, bounded by the ring
     if (lane == 0) {
-      int L, ctr = 0;
-      while (iter.next(L)) {
-        const int bg = L / n_super, st_last = L % n_super, c = st_last / vp.vc;
-        const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
-        const uint8_t* src0 = vp.hv + ((size_t)bg * p.T_cap + c0) * row_bytes;
-        const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
-        for (int pass = 0; pass < s_v; pass += V_HP) {
-          for (int l = 0; l < n_loads; ++l, ++ctr) {
-            const int st = ctr % vp.v_stages;
-            mbar_wait(&empty[st], ((ctr / vp.v_stages) & 1) ^ 1);
-            const int nr = min(stage_rows, (c1 - c0) - l * stage_rows);
-            mbar_expect_tx(&full[st], (uint32_t)(nr * row_bytes));
-            bulk_load(ring + st * V_STAGE, src0 + (size_t)l * stage_rows * row_bytes,
-                      (uint32_t)(nr * row_bytes), &full[st]);
+      prefetch_map(&map_v);
+      int ctr = 0;
+      while (it.next(u)) {
+        const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
+        const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
+        for (int blk = 0; blk < nblk; ++blk)
+          for (int j = 0; j < NJ; ++j, ++ctr) {
+            const int st = ctr % vs;
+            mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
+            mbar_expect_tx(&full[st], V_STAGE);
+            const int row = u.bg * p.T_cap + c0 + blk * TILE_M;
+            tma_load_2d(&map_v, &full[st], ring + st * V_STAGE, j * 128, row);
+            tma_load_2d(&map_v, &full[st], ring + st * V_STAGE + V_STAGE / 2, j * 128 + 64, row);
           }
-        }
       }
     }
     return;
   }
-  if (warp > 8) return;
-  // ---------------- consumers (warps 0..7) ----------------
-  int L, ctr = 0;
-  while (iter.next(L)) {
-    const int bg = L / n_super, b = bg / p.G, g = bg - b * p.G;
-    const int st_last = L % n_super, c = st_last / vp.vc;
-    const int item0 = bg * n_super + c * vp.vc;
-    const int c0 = c * vp.vc * SUPER, c1 = min(T_rows, (st_last + 1) * SUPER);
-    const int n_loads = (c1 - c0 + stage_rows - 1) / stage_rows;
-    if (tid == 0) {
-      for (int it = item0; it <= L; ++it)
-        while (ld_acquire_u32(&p.ready[it]) < 2u * (EPI_WARPS / 2)) __nanosleep(128);
-    }
-    named_bar_sync(1, 256);
-    for (int p0 = 0; p0 < s_v; p0 += V_HP) {
-      const int hp = min(V_HP, s_v - p0);
-      // (1) chunk softmax statistics (logits via L2: written by the score role)
-      const float* lg[V_HP];
+  if (warp == 9) {
+    // ---------------- MMA issuer: D[buf][j] += V^T x P^T per 128-token block
+    if (lane == 0) {
+      int ctr = 0, k = 0;
+      while (it.next(u)) {
+        const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
+        const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
+        const int buf = k & 1;
+        mbar_wait(&pfull[buf], (k >> 1) & 1);
+        if (k >= 2) mbar_wait(&dempty[buf], ((k >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t pb = smem_u32(pbuf + buf * PB);
+        for (int blk = 0; blk < nblk; ++blk)
+          for (int j = 0; j < NJ; ++j, ++ctr) {
+            const int st = ctr % vs;
+            mbar_wait(&full[st], (ctr / vs) & 1);
+            fence_after();
+            const uint32_t a0 = smem_u32(ring + st * V_STAGE);
+            const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h)
-        lg[h] = p.logits + ((size_t)b * p.n_heads + g * s_v + p0 + min(h, hp - 1)) * p.ld_logits;
+            for (int kk = 0; kk < TILE_M / 16; ++kk)
+              umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, V_STAGE / 2, 1024),
+                           sdesc(pb + (blk * 2 + kk / 4) * 1024 + (kk % 4) * 32), IDESC_V,
+                           (blk | kk) != 0);
+            umma_commit(&empty[st]);
+          }
+        umma_commit(&dfull[buf]);
+        ++k;
+      }
+    }
+    __syncwarp();
+    named_bar_sync(2, 288);
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(V_TMEM_COLS));
+    return;
+  }
+
+  if (warp < 4) {
+    // ======== group A (warps 0-3): logits -> statistics -> P operand ========
+    const int ta = tid;  // 0..127
+    int kk_trace = 0;
+    auto trace = [&](int slot) {
+      if (p.trace != nullptr && ta == 0 && 5 * kk_trace + 8 < TRACE_STRIDE)
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 5 * kk_trace + slot] = gtimer();
+    };
+    // wait for the unit's score items, then cp.async its logits (V_HP rows of
+    // the padded token range) into lbuf[buf]; one commit group per unit
+    auto fetch = [&](const VUnit& x, int buf) {
+      if (ta == 0) {
+        for (int i = x.item0; i < x.item0 + (x.st1 - x.st0); ++i)
+          while (ld_acquire_u32(&p.ready[i]) < 2u * (EPI_WARPS / 2)) __nanosleep(64);
+      }
+      named_bar_sync(3, 128);
+      const int b = x.bg / p.G, g = x.bg - b * p.G;
+      const int c0 = x.st0 * SUPER, c1 = min(T_rows, x.st1 * SUPER);
+      const int n16 = (c1 - c0 + 3) / 4;  // 16-byte granules per head row
+      const float* src = p.logits + ((size_t)b * p.n_heads + g * s_v) * p.ld_logits + c0;
+      float* dst = lbuf + buf * V_HP * max_tok;
+      for (int i = ta; i < s_v * n16; i += 128) {
+        const int h = i / n16, q = i - h * n16;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                         smem_u32(dst + h * max_tok + 4 * q)),
+                     "l"(src + (size_t)h * p.ld_logits + 4 * q)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int k = 0;
+    VUnit nx;
+    bool have = it.next(u);
+    if (have) fetch(u, 0);
+    while (have) {
+      const bool more = it.next(nx);
+      if (more) fetch(nx, (k + 1) & 1);
+      if (more)
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+      else
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+      named_bar_sync(3, 128);
+      trace(0);
+      const int b = u.bg / p.G, g = u.bg - b * p.G;
+      const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
+      const int nt = c1 - c0;
+      const int ntok = (nt + TILE_M - 1) / TILE_M * TILE_M;  // padded to whole blocks
+      const int buf = k & 1;
+      const float* lg = lbuf + buf * V_HP * max_tok;
+      // (1) per-head max over the unit (thread = token pairs)
       float m[V_HP];
 #pragma unroll
       for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
-      for (int t0 = c0 + tid; t0 < c1; t0 += 4 * 256) {
-        float v[4][V_HP];
+      for (int t = 2 * ta; t < nt; t += 256) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h)
-            v[u][h] = (t0 + u * 256 < c1) ? __ldcg(lg[h] + t0 + u * 256) : -INFINITY;
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) {
-            if (t0 + u * 256 < c1) ps[h * max_tok + (t0 + u * 256 - c0)] = v[u][h];
-            m[h] = fmaxf(m[h], v[u][h]);
+        for (int h = 0; h < V_HP; ++h)
+          if (h < s_v) {
+            const float2 v = *reinterpret_cast<const float2*>(lg + h * max_tok + t);
+            m[h] = fmaxf(m[h], t + 1 < nt ? fmaxf(v.x, v.y) : v.x);
           }
       }
 #pragma unroll
       for (int h = 0; h < V_HP; ++h) {
-        m[h] = warp_reduce(m[h], [](float x, float y) { return fmaxf(x, y); });
+        m[h] = warp_reduce(m[h], [](float a, float c) { return fmaxf(a, c); });
         if (lane == 0) red_m[warp][h] = m[h];
       }
-      named_bar_sync(1, 256);
-      if (tid < V_HP) {
-        float mm = red_m[0][tid];
-        for (int w = 1; w < 8; ++w) mm = fmaxf(mm, red_m[w][tid]);
-        m_sh[tid] = mm;
-      }
-      named_bar_sync(1, 256);
+      // P buffer `buf` is free once the MMAs of unit k - 2 are read back
+      if (k >= 2) mbar_wait(&dempty[buf], ((k >> 1) - 1) & 1);
+      named_bar_sync(3, 128);
+      trace(2);
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+        m[h] = fmaxf(fmaxf(red_m[0][h], red_m[1][h]), fmaxf(red_m[2][h], red_m[3][h]));
+      // (2) P = hi + lo bf16 (rows h and h + 4 of the K-major SW128 operand:
+      // ~16 mantissa bits of p at no extra tensor work); zeros past the last
+      // token; l sums the fp32 probabilities
+      uint8_t* pb = pbuf + buf * PB;
       float l[V_HP];
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h) {
-        m[h] = m_sh[h];
-        l[h] = 0.f;
-      }
-      for (int t = c0 + tid; t < c1; t += 256) {
+      for (int h = 0; h < V_HP; ++h) l[h] = 0.f;
+      for (int t = 2 * ta; t < ntok; t += 256) {
+        const int blk = t >> 6, w = t & 63;
+        const uint32_t rowb = blk * 1024 + (w & 7) * 2;
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
-          const float e = __expf(ps[h * max_tok + (t - c0)] - m[h]);
-          ps[h * max_tok + (t - c0)] = e;
-          l[h] += e;
+          if (h < s_v) {
+            const float2 v = t < nt ? *reinterpret_cast<const float2*>(lg + h * max_tok + t)
+                                    : make_float2(-INFINITY, -INFINITY);
+            const float p0 = __expf(v.x - m[h]), p1 = t + 1 < nt ? __expf(v.y - m[h]) : 0.f;
+            const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
+            const float2 hf = __bfloat1622float2(hi);
+            const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+            l[h] += p0 + p1;
+            *reinterpret_cast<__nv_bfloat162*>(pb + rowb + h * 128 + ((((w >> 3) ^ h) & 7) << 4)) = hi;
+            *reinterpret_cast<__nv_bfloat162*>(pb + rowb + (h + 4) * 128 +
+                                               ((((w >> 3) ^ (h + 4)) & 7) << 4)) = lo;
+          }
         }
       }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
       for (int h = 0; h < V_HP; ++h) {
-        l[h] = warp_reduce(l[h], [](float x, float y) { return x + y; });
+        l[h] = warp_reduce(l[h], [](float a, float c) { return a + c; });
         if (lane == 0) red_l[warp][h] = l[h];
       }
-      named_bar_sync(1, 256);
-      if (tid < hp) {
-        float ll = 0.f;
-        for (int w = 0; w < 8; ++w) ll += red_l[w][tid];
-        const size_t pi = ((size_t)b * p.n_heads + g * s_v + p0 + tid) * vp.nc_max + c;
-        vp.pm[pi] = m_sh[tid];
-        vp.pl[pi] = ll;
-      }
-      // (2) reduce the staged rows: one row per warp step, lanes over 16-B segments
-      float2 acc[V_HP][NSEG][4];
+      named_bar_sync(3, 128);
+      if (ta == 0) mbar_arrive(&pfull[buf]);
 #pragma unroll
       for (int h = 0; h < V_HP; ++h)
-#pragma unroll
-        for (int q2 = 0; q2 < NSEG; ++q2)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[h][q2][e] = make_float2(0.f, 0.f);
-      for (int l2 = 0; l2 < n_loads; ++l2, ++ctr) {
-        const int st = ctr % vp.v_stages;
-        mbar_wait(&full[st], (ctr / vp.v_stages) & 1);
-        const int r0 = l2 * stage_rows;
-        const int nr = min(stage_rows, (c1 - c0) - r0);
-        const uint8_t* sbase = ring + st * V_STAGE;
-        const float* pst = ps + r0;
-        for (int r = warp; r < nr; r += 8) {
-          const uint8_t* row = sbase + (size_t)r * row_bytes;
-          float pv[V_HP];
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) pv[h] = pst[h * max_tok + r];
-#pragma unroll
-          for (int q2 = 0; q2 < NSEG; ++q2) {
-            const int sg = lane + q2 * 32;
-            if (NSEG == 1 || sg < segs) {
-              const uint4 v = *reinterpret_cast<const uint4*>(row + sg * 16);
-              float f[8];
-              Vec16<bf16>::unpack(v, f);
-#pragma unroll
-              for (int h = 0; h < V_HP; ++h) {
-                const float2 p2 = make_float2(pv[h], pv[h]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e)
-                  acc[h][q2][e] = ffma2(p2, make_float2(f[2 * e], f[2 * e + 1]), acc[h][q2][e]);
-              }
-            }
-          }
+        if (ta == h && h < s_v) {
+          const size_t pi = ((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0;
+          vp.pm[pi] = m[h];
+          vp.pl[pi] = red_l[0][h] + red_l[1][h] + red_l[2][h] + red_l[3][h];
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-      }
-      // (3) cross-warp reduction -> chunk partial
-#pragma unroll
-      for (int h = 0; h < V_HP; ++h)
-#pragma unroll
-        for (int q2 = 0; q2 < NSEG; ++q2) {
-          const int sg = lane + q2 * 32;
-          if (sg < segs)
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e] = acc[h][q2][e].x;
-              red[((size_t)warp * V_HP + h) * vp.Rv_pad + sg * 8 + 2 * e + 1] = acc[h][q2][e].y;
-            }
-        }
-      named_bar_sync(1, 256);
-      for (int idx = tid; idx < hp * vp.Rv_pad; idx += 256) {
-        const int h = idx / vp.Rv_pad, col = idx - h * vp.Rv_pad;
-        float v = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
-        vp.pctx[(((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max + c) * vp.Rv_pad + col] = v;
-      }
-      named_bar_sync(1, 256);
+      trace(1);
+      if (p.trace != nullptr) ++kk_trace;
+      u = nx;
+      have = more;
+      ++k;
     }
-    // ---- consume readiness (reset for the next launch) and merge if last
-    if (tid == 0)
-      for (int it = item0; it <= L; ++it) p.ready[it] = 0;
-    __threadfence();
-    named_bar_sync(1, 256);
-    if (tid == 0) ticket_sh = atomicAdd(&vp.tickets[bg], 1u);
-    named_bar_sync(1, 256);
-    if (ticket_sh != (unsigned)(n_vc - 1)) continue;
-    __threadfence();
-    const int r = vp.ranks_v[g];
-    for (int p0 = 0; p0 < s_v; p0 += V_HP) {
-      const int hp = min(V_HP, s_v - p0);
-      if (warp < hp) {
-        const size_t base = ((size_t)b * p.n_heads + g * s_v + p0 + warp) * vp.nc_max;
+  } else {
+    // ======== group B (warps 4-7): accumulator -> partial, ticket, merge ========
+    const int tb = tid - 128, wb = warp - 4;  // wb = TMEM lane quarter
+    int k = 0;
+    while (it.next(u)) {
+      const int buf = k & 1;
+      const int b = u.bg / p.G, g = u.bg - b * p.G;
+      mbar_wait(&dfull[buf], (k >> 1) & 1);
+      fence_after();
+      for (int j = 0; j < NJ; ++j) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(wb * 32) << 16) + (uint32_t)((buf * NJ + j) * 16), v);
+        tmem_wait_ld();
+        const int col = j * 128 + wb * 32 + lane;
+        if (col < vp.Rv_pad) {
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h)
+            if (h < s_v)
+              vp.pctx[(((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0) * vp.Rv_pad + col] =
+                  v[h] + v[h + V_HP];
+        }
+      }
+      fence_before();
+      named_bar_sync(4, 128);
+      if (tb == 0) {
+        mbar_arrive(&dempty[buf]);
+        for (int i = u.item0; i < u.item0 + (u.st1 - u.st0); ++i) p.ready[i] = 0;
+      }
+      ++k;
+      __threadfence();
+      named_bar_sync(4, 128);
+      if (tb == 0) {
+        ticket_sh = atomicAdd(&vp.tickets[u.bg], (unsigned)(u.st1 - u.st0)) + (unsigned)(u.st1 - u.st0);
+        go_sh = ticket_sh == (unsigned)n_super;
+        if (go_sh) {
+          int nu = 0;  // the group's sub-unit slots, in token order (fixed merge order)
+          for (int x = 0; x < n_super;) {
+            ulist[nu++] = x;
+            x = min(sch.win_end(u.bg * n_super + x), (u.bg + 1) * n_super) - u.bg * n_super;
+          }
+          nu_sh = nu;
+        }
+      }
+      named_bar_sync(4, 128);
+      if (!go_sh) continue;
+      __threadfence();
+      const int nu = nu_sh;
+      const int r = vp.ranks_v[g];
+      if (wb < s_v) {
+        const size_t base = ((size_t)b * p.n_heads + g * s_v + wb) * ns;
         float M = -INFINITY;
-        for (int cc = lane; cc < n_vc; cc += 32) M = fmaxf(M, __ldcg(vp.pm + base + cc));
+        for (int q = lane; q < nu; q += 32) M = fmaxf(M, __ldcg(vp.pm + base + ulist[q]));
         M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
         float Ls = 0.f;
-        for (int cc = lane; cc < n_vc; cc += 32) {
-          const float w = __expf(__ldcg(vp.pm + base + cc) - M);
-          wsm[warp * vp.nc_max + cc] = w;
-          Ls += w * __ldcg(vp.pl + base + cc);
+        for (int q = lane; q < nu; q += 32) {
+          const float w = __expf(__ldcg(vp.pm + base + ulist[q]) - M);
+          wsm[wb * ns + q] = w;
+          Ls += w * __ldcg(vp.pl + base + ulist[q]);
         }
         Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
-        if (lane == 0) inv_l[warp] = 1.f / Ls;
+        if (lane == 0) inv_l[wb] = 1.f / Ls;
       }
-      named_bar_sync(1, 256);
-      // chunk-parallel: warp w sums chunks w, w + 8, ...; lanes over columns
-      for (int h = 0; h < hp; ++h) {
+      named_bar_sync(4, 128);
+      // unit-parallel over 4 warps, 128 columns per round, fixed summation order
+      for (int h = 0; h < s_v; ++h) {
         const float* src =
-            vp.pctx + ((size_t)b * p.n_heads + g * s_v + p0 + h) * vp.nc_max * (size_t)vp.Rv_pad;
+            vp.pctx + ((size_t)b * p.n_heads + g * s_v + h) * ns * (size_t)vp.Rv_pad;
         for (int col0 = 0; col0 < r; col0 += 128) {
           float a4[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int cc = warp; cc < n_vc; cc += 8) {
-            const float w = wsm[h * vp.nc_max + cc];
+          for (int q = wb; q < nu; q += 4) {
+            const float w = wsm[h * ns + q];
+            const float* srow = src + (size_t)ulist[q] * vp.Rv_pad;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const int col = col0 + lane + 32 * q;
-              if (col < r) a4[q] = fmaf(w, __ldcg(src + (size_t)cc * vp.Rv_pad + col), a4[q]);
+            for (int qq = 0; qq < 4; ++qq) {
+              const int col = col0 + lane + 32 * qq;
+              if (col < r) a4[qq] = fmaf(w, __ldcg(srow + col), a4[qq]);
             }
           }
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int col = col0 + lane + 32 * q;
-            if (col < r) red[((size_t)warp * V_HP + h) * vp.Rv_pad + col] = a4[q];
+          for (int qq = 0; qq < 4; ++qq) red[wb * 128 + lane + 32 * qq] = a4[qq];
+          named_bar_sync(4, 128);
+          if (col0 + tb < r) {
+            const float v = (red[tb] + red[128 + tb]) + (red[256 + tb] + red[384 + tb]);
+            vp.ctx_out[(size_t)b * vp.ld_ctx + vp.o_off[g * s_v + h] + col0 + tb] = v * inv_l[h];
           }
+          named_bar_sync(4, 128);
         }
       }
-      named_bar_sync(1, 256);
-      for (int idx = tid; idx < hp * r; idx += 256) {
-        const int h = idx / r, col = idx - h * r;
-        float v = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) v += red[((size_t)w * V_HP + h) * vp.Rv_pad + col];
-        vp.ctx_out[(size_t)b * vp.ld_ctx + vp.o_off[g * s_v + p0 + h] + col] = v * inv_l[h];
-      }
-      named_bar_sync(1, 256);
+      if (tb == 0) vp.tickets[u.bg] = 0u;
     }
-    if (tid == 0) vp.tickets[bg] = 0u;
+  }
+  named_bar_sync(2, 288);
+  if (p.trace != nullptr && tid == 0) {
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 1] = gtimer();
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 3] = 1000000ull + 1;
   }
 }
 
-template <int NSEG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
-                      const __grid_constant__ CUtensorMap map_uw, const Params p,
+                      const __grid_constant__ CUtensorMap map_uw,
+                      const __grid_constant__ CUtensorMap map_v, const Params p,
                       const VParams vp) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 0] = gtimer();
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
+  }
   if ((int)(blockIdx.x >> 1) < p.score_pairs) {
     score_role(map_h, map_uw, p, smem);
   } else {
     const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
-    value_role<NSEG>(p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
+    value_role(map_v, p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
   }
 }
 
@@ -774,22 +894,55 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
+  prm.trace = nullptr;
   rope_score_tc_kernel<<<dim3(sms & ~1), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
   PALU_LAUNCHED();
   return PALU_OK;
 }
 
 // ---- fused score + softmax + value ------------------------------------------
-static int fused_nc_max(int T_cap, int vc) {
+static unsigned long long* g_trace = nullptr;  // diagnostics (PALU_FUSED_TRACE)
+static int g_trace_ctas = 0;
+
+// Copies the last traced fused launch's timeline ([CTA][TRACE_STRIDE] u64:
+// start, end, smid, role/count, events...) to host; returns the CTA count.
+int palu_fused_trace(unsigned long long* host, size_t max_ctas) {
+  using palu::tc::TRACE_STRIDE;
+  if (!g_trace) return 0;
+  const size_t n = max_ctas < (size_t)g_trace_ctas ? max_ctas : (size_t)g_trace_ctas;
+  PALU_CK(cudaDeviceSynchronize());
+  PALU_CK(cudaMemcpy(host, g_trace, n * TRACE_STRIDE * 8, cudaMemcpyDeviceToHost));
+  return (int)n;
+}
+
+// Cluster-of-2 residency of the fused kernel at its launch configuration.
+int palu_fused_max_clusters(int smem_bytes) {
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = 2;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.gridDim = dim3(148);
+  cfg.blockDim = dim3(palu::tc::THREADS);
+  cfg.dynamicSmemBytes = smem_bytes;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  PALU_CK(cudaFuncSetAttribute(palu::tc::rope_attend_tc_kernel,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, palu::tc::SMEM_LIMIT - 2048));
+  int n = 0;
+  PALU_CK(cudaOccupancyMaxActiveClusters(&n, palu::tc::rope_attend_tc_kernel, &cfg));
+  return n;
+}
+
+static int fused_ns_cap(int T_cap) {
   using palu::tc::SUPER;
-  const int n_super = (T_cap + SUPER - 1) / SUPER;
-  return (n_super + vc - 1) / vc;
+  return (T_cap + SUPER - 1) / SUPER;
 }
 
 size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap) {
   using palu::tc::SUPER;
-  const int vc = 4;
-  const int nc = fused_nc_max(T_cap, vc);
+  const int nc = fused_ns_cap(T_cap);
   const size_t items = (size_t)B * G * ((T_cap + SUPER - 1) / SUPER);
   const size_t head = (size_t)B * n_heads * nc;
   return 256 + sizeof(unsigned) * (size_t)B * G + sizeof(int) * items + sizeof(float) * head * 2 +
@@ -802,8 +955,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
                         const int* o_off, float* ctx, int ld_ctx, void* workspace,
                         int score_sms, void* stream) {
   using namespace palu::tc;
-  if (!palu_rope_score_tc_splits(s, Rk_pad) || G * s != n_heads || (Rv_pad * 2) % 16 != 0 ||
-      Rv_pad > 512) {
+  if (!palu_rope_score_tc_splits(s, Rk_pad) || G * s != n_heads || Rv_pad % KB != 0 ||
+      Rv_pad > 512 || s > V_HP) {
     set_error("palu_rope_attend_tc: unsupported shape (Rk %d, Rv %d, s %d)", Rk_pad, Rv_pad, s);
     return PALU_EUNSUPPORTED;
   }
@@ -837,8 +990,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   score_sms &= ~1;
   if (score_sms < 2) score_sms = 2;
   if (score_sms > sms - 2) score_sms = sms - 2;
-  const int vc = 4;
-  const int nc_max = fused_nc_max(T_cap, vc);
+  const int vc = getenv("PALU_FUSED_VC") ? atoi(getenv("PALU_FUSED_VC")) : 4;  // tuning only
+  const int nc_max = fused_ns_cap(T_cap);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
   unsigned* tickets = reinterpret_cast<unsigned*>(ws + 256);
   int* ready = reinterpret_cast<int*>(tickets + (size_t)B * G);
@@ -863,43 +1016,44 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
+  prm.trace = nullptr;
+  if (getenv("PALU_FUSED_TRACE")) {
+    if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
+    PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));
+    prm.trace = g_trace;
+    g_trace_ctas = sms;
+  }
+  CUtensorMap map_v;
+  rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  if (rc) return rc;
   VParams vp;
-  vp.hv = reinterpret_cast<const uint8_t*>(hv);
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
-  const size_t side = sizeof(float) * ((size_t)8 * V_HP * Rv_pad + (size_t)V_HP * vc * SUPER +
-                                       (size_t)V_HP * nc_max) + 64 * 16 + 1024;
-  vp.v_stages = (int)(((long long)smem - 1024 - (long long)side) / V_STAGE);
-  PALU_REQUIRE(vp.v_stages >= 3, "palu_rope_attend_tc: value ring too small (%d)", vp.v_stages);
-  if (vp.v_stages > 32) vp.v_stages = 32;
+  const size_t pbytes = (size_t)2 * (vc * SUPER / 64) * 1024 + 1024;
+  const size_t side = pbytes + sizeof(float) * ((size_t)2 * V_HP * vc * SUPER + (size_t)V_HP * nc_max +
+                                                (size_t)((nc_max + 3) & ~3) + 4 * 128) + 16 * 64 + 64;
+  // the value role takes whatever the score role leaves: launch at the limit
+  const size_t smem_launch = (size_t)dyn_limit;
+  vp.v_stages = (int)(((long long)smem_launch - 1024 - (long long)side) / V_STAGE);
+  PALU_REQUIRE(vp.v_stages >= 2, "palu_rope_attend_tc: value ring too small (%d)", vp.v_stages);
+  if (vp.v_stages > 8) vp.v_stages = 8;
   vp.tickets = tickets;
   vp.pm = pm;
   vp.pl = pl;
   vp.pctx = pctx;
-  vp.nc_max = nc_max;
+  vp.ns_cap = nc_max;
   vp.ranks_v = ranks_v;
   vp.o_off = o_off;
   vp.ctx_out = ctx;
   vp.ld_ctx = ld_ctx;
-  const int nseg = (Rv_pad * 2 / 16 + 31) / 32;
-  static bool attr1 = false, attr2 = false;
-  if (nseg == 1) {
-    if (!attr1) {
-      PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<1>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
-      attr1 = true;
-    }
-    rope_attend_tc_kernel<1><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
-                                                                                 prm, vp);
-  } else {
-    if (!attr2) {
-      PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel<2>,
-                                   cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
-      attr2 = true;
-    }
-    rope_attend_tc_kernel<2><<<dim3(sms), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw,
-                                                                                 prm, vp);
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 dyn_limit));
+    attr = true;
   }
+  rope_attend_tc_kernel<<<dim3(sms), THREADS, smem_launch, (cudaStream_t)stream>>>(map_h, map_uw,
+                                                                                  map_v, prm, vp);
   PALU_LAUNCHED();
   return PALU_OK;
 }

@@ -296,3 +296,30 @@ def test_fused_attend_matches_oracle(P, golden, which):
     assert rel_err(outs["fused"][0], case["out1"]) < TOL["bfloat16"]
     assert rel_err(outs["fused"][0], outs["tcgen05"][0]) < 2e-3
     assert rel_err(outs["fused"][1], outs["tcgen05"][1]) < 5e-3
+
+
+@pytest.mark.parametrize("batch,context,rk,rv", [(3, 9000, 256, 256), (2, 20000, 128, 384),
+                                                 (1, 300, 256, 256)])
+def test_fused_attend_long_batched(P, batch, context, rk, rv):
+    """Fused kernel vs the unfused tcgen05 + softmax-value path on the same
+    long, batched synthetic cache (many score items per pair, sub-units
+    straddling sequence/group boundaries, merge ordering)."""
+    import torch
+    from paper_2407_21118_b200.attention import _Session
+    from paper_2407_21118_b200.harness import synthetic_engine
+    _, fused, cache = synthetic_engine(layers=1, batch=batch, context=context, extra=8,
+                                       rank_k=rk, rank_v=rv, seed=99)
+    x0 = torch.randn(batch, 4096, device="cuda") * 0.5
+    outs = {}
+    for sk in ("tcgen05", "fused"):
+        s = _Session(fused, cache, score_kernel=sk, use_graph=False)
+        assert any(s.fused_layers) == (sk == "fused")
+        s.x.copy_(x0)
+        for _ in range(2):  # second launch checks the self-resetting counters
+            s.x.copy_(x0)
+            s.t_dev.fill_(cache.t)
+            s.launch_step()
+        torch.cuda.synchronize()
+        outs[sk] = s.x.double().cpu().numpy()
+    e = rel_err(outs["fused"], outs["tcgen05"])
+    assert e < 2e-3, e

@@ -1,0 +1,180 @@
+// Per-CTA HBM streaming probe (diagnostics, not product): how fast can ONE
+// CTA stream contiguous rows with (a) 1-D TMA bulk copies into a smem ring
+// and (b) plain 16-B loads from registers, as a function of CTA count.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/bw_probe tools/bw_probe.cu
+#include <cstdio>
+#include <cstdint>
+#include <cstdlib>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(c));
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes));
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)));
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t ph) {
+  asm volatile(
+      "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+          su32(b)),
+      "r"(ph));
+}
+__device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          su32(dst)),
+      "l"(src), "r"(bytes), "r"(su32(b))
+      : "memory");
+}
+
+// mode 0: TMA ring, consumers only arrive; mode 1: TMA ring + consumers read smem
+__global__ void __launch_bounds__(288, 1) tma_stream(const uint8_t* src, size_t per_cta, int stages,
+                                                     int chunk, int mode, float* sink) {
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * chunk);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint8_t* base = src + (size_t)blockIdx.x * per_cta;
+  const int n = (int)(per_cta / chunk);
+  const int np = (mode == 2 || mode == 3) ? 4 : 1;  // issuing lanes
+  if (warp == 8) {
+    if (lane < np)
+      for (int i = lane; i < n; i += np) {
+        const int s = i % stages;
+        mb_wait(&empty[s], ((i / stages) & 1) ^ 1);
+        mb_expect(&full[s], chunk);
+        bulk(sm + (size_t)s * chunk, base + (size_t)i * chunk, chunk, &full[s]);
+      }
+    return;
+  }
+  float acc = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const int s = i % stages;
+    mb_wait(&full[s], (i / stages) & 1);
+    if (mode == 4) {
+      // the fused kernel's value loop: 512-B rows, 4 heads, FFMA2, pv per row
+      const uint32_t sb = su32(sm + (size_t)s * chunk);
+      const int nr = chunk / 512;
+      float2 a[4][4];
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a[h][e] = make_float2(0.f, 0.f);
+      for (int rb = warp; rb < nr; rb += 32) {
+        uint4 v[4];
+        float4 pv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = rb + 8 * k;
+          asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v[k].x), "=r"(v[k].y), "=r"(v[k].z), "=r"(v[k].w) : "r"(sb + r * 512 + lane * 16));
+          asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(pv[k].x), "=f"(pv[k].y), "=f"(pv[k].z), "=f"(pv[k].w) : "r"(sb + r * 16));
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float pk[4] = {pv[k].x, pv[k].y, pv[k].z, pv[k].w};
+          const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const float2 f = make_float2(__uint_as_float(w[e] << 16), __uint_as_float(w[e] & 0xffff0000u));
+              a[h][e].x = fmaf(pk[h], f.x, a[h][e].x);
+              a[h][e].y = fmaf(pk[h], f.y, a[h][e].y);
+            }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 4; ++h)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc += a[h][e].x + a[h][e].y;
+    } else if (mode & 1) {
+      const uint4* p = reinterpret_cast<const uint4*>(sm + (size_t)s * chunk);
+      for (int k = warp * 32 + lane; k < chunk / 16; k += 256) {
+        const uint4 v = p[k];
+        acc += __uint_as_float(v.x) + __uint_as_float(v.y) + __uint_as_float(v.z) + __uint_as_float(v.w);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mb_arrive(&empty[s]);
+  }
+  if (acc == 12345.f) sink[0] = acc;
+}
+
+// plain loads: each thread keeps U 16-B loads in flight
+template <int U>
+__global__ void __launch_bounds__(256, 1) ldg_stream(const uint4* src, size_t per_cta16, float* sink) {
+  const uint4* base = src + (size_t)blockIdx.x * per_cta16;
+  float acc = 0.f;
+  for (size_t i = threadIdx.x; i + (U - 1) * 256 < per_cta16; i += U * 256) {
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                   : "l"(base + i + u * 256));
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += __uint_as_float(v[u].x ^ v[u].w);
+  }
+  if (acc == 12345.f) sink[0] = acc;
+}
+
+int main() {
+  const size_t total = (size_t)4 << 30;  // 4 GiB buffer
+  uint8_t* buf;
+  float* sink;
+  cudaMalloc(&buf, total);
+  cudaMalloc(&sink, 64);
+  cudaMemset(buf, 1, total);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  int ctas_list[] = {1, 22, 120};
+  cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  for (int mode : {1, 4})
+    for (int chunk : {32768, 65536})
+      for (int stages : {3, 5}) {
+        if ((size_t)chunk * stages > 200 * 1024) continue;
+        for (int ctas : ctas_list) {
+          const size_t per = (size_t)(32 << 20) / chunk * chunk;  // 32 MiB per CTA
+          if (per * ctas > total) continue;
+          const size_t smem = (size_t)chunk * stages + 16 * stages + 64;
+          tma_stream<<<ctas, 288, smem>>>(buf, per, stages, chunk, mode, sink);
+          cudaEventRecord(a);
+          tma_stream<<<ctas, 288, smem>>>(buf, per, stages, chunk, mode, sink);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          printf("tma mode %d chunk %6d stages %2d ctas %3d: %7.1f GB/s per CTA, %7.1f GB/s total\n",
+                 mode, chunk, stages, ctas, per / (ms * 1e6), per * ctas / (ms * 1e6));
+        }
+      }
+  for (int ctas : {1}) {
+    const size_t per16 = ((size_t)(32 << 20)) / 16;
+    ldg_stream<8><<<ctas, 256>>>(reinterpret_cast<uint4*>(buf), per16, sink);
+    cudaEventRecord(a);
+    ldg_stream<8><<<ctas, 256>>>(reinterpret_cast<uint4*>(buf), per16, sink);
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    float ms;
+    cudaEventElapsedTime(&ms, a, b);
+    printf("ldg U=8 ctas %3d: %7.1f GB/s per CTA, %7.1f total\n", ctas, per16 * 16 / (ms * 1e6),
+           per16 * 16 * ctas / (ms * 1e6));
+  }
+  printf("err: %s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
