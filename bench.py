@@ -376,7 +376,8 @@ def main():
     lat_bytes = T1 * n_groups * args.rank_k * 2 * args.batch  # H_k stream bf16
     achieved_tf = flops / (score_ms * 1e-3) / 1e12
     total_kernel_ms = sum(sum(v) for v in prof.values())
-    sv_ms = statistics.mean(prof["palu_softmax_value"]) if "palu_softmax_value" in prof else 0.0
+    sv_name = next((k for k in ("palu_value_tc", "palu_softmax_value") if k in prof), None)
+    sv_ms = statistics.mean(prof[sv_name]) if sv_name else 0.0
     latent_total = T1 * n_groups * (args.rank_k + args.rank_v) * 2 * args.batch
     roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
                 "frac": achieved_tf / tf_sus, "traffic": None, "peak_source": f"{src} sustained bf16",

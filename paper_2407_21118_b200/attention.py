@@ -475,8 +475,17 @@ class _Session:
                   and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512 and V.r_pad % 64 == 0
                   and score_kernel == "fused")
             self.fused_layers.append(ok)
+        # tcgen05 softmax + value after the tcgen05 score kernel: bf16 raw V,
+        # 64-column-aligned rows, up to 4 heads per value group
+        self.value_tc_layers = []
+        for li, L in enumerate(fused.layers):
+            K, V = c._stores[li]
+            self.value_tc_layers.append(
+                self.tc_layers[li] and not self.fused_layers[li] and V.bits == FP_BITS
+                and V.r_pad % 64 == 0 and V.r_pad <= 512 and L.s_v <= 4
+                and os.environ.get("PALU_VALUE_KERNEL", "tc") == "tc")
         self.ws_fused = None
-        if any(self.fused_layers):
+        if any(self.fused_layers) or any(self.value_tc_layers):
             nbytes = max(_lib.call("palu_rope_attend_workspace", self.B, self.n, V.G, V.r_pad, self.cap)
                          for (K, V) in c._stores)
             self.ws_fused = torch.zeros(nbytes // 4 + 1, dtype=torch.float32, device=dev)
@@ -531,6 +540,13 @@ class _Session:
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, self.plane, st)
+            if self.value_tc_layers[li]:
+                _lib.call("palu_value_tc", _ptr(V.rows), B, n, L.s_v, V.G, V.r_pad, V.cap,
+                          _ptr(self.logits), self.ld_logits, _ptr(self.t_dev), _ptr(L.ranks_v_dev),
+                          _ptr(L.o_off_dev), _ptr(self.ctx), self.ko, _ptr(self.ws_fused), st)
+                _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
+                          _ptr(x), d, 0, st)
+                return
         else:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),

@@ -350,11 +350,14 @@ struct VParams {
   const int* o_off;
   float* ctx_out;
   int ld_ctx;
+  int no_wait;  // standalone value kernel: the logits are complete at launch
 };
 
 constexpr int V_STAGE = 32768;  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
 constexpr int V_HP = 4;         // heads per group handled by the value role
 constexpr int V_TMEM_COLS = 128;
+constexpr int V_PF = 0;     // L2 prefetch distance of the value stream (128-token blocks)
+constexpr int V_SUB = 512;  // tokens per P sub-block (double-buffered)
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   uint32_t v;
@@ -410,31 +413,25 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   const int n_super = (T_rows + SUPER - 1) / SUPER;
   const int total = p.B * p.G * n_super;
   const int per = (total + p.score_pairs - 1) / p.score_pairs;
-  const VSched sch{per, total, p.score_pairs, n_super, vp.vc, (per + vp.vc - 1) / vp.vc};
+  const int vc = vp.vc > 0 ? vp.vc : per;  // vc <= 0: one window per pair (standalone)
+  const VSched sch{per, total, p.score_pairs, n_super, vc, (per + vc - 1) / vc};
   const int s_v = p.s_k;
   const int NJ = (vp.Rv_pad + 127) / 128;  // 128-column pairs of 64-column boxes
   const int ns = vp.ns_cap;
   const int vs = vp.v_stages;
-  const int max_tok = vp.vc * SUPER;
-  const int PB = max_tok / 64 * 1024;  // P bytes per buffer: 1 KB per 64 tokens
+  constexpr int PB = V_SUB / 64 * 1024;  // P bytes per sub-block buffer: 1 KB per 64 tokens
   // smem: ring | P[2] (+1 KB: rows 8..15 of the last block alias past it) |
-  //       logits [2][V_HP][max_tok] | wsm [V_HP][ns] | ulist [ns] | red [4][128] |
   //       barriers | TMEM slot
   uint8_t* ring = smem;
   uint8_t* pbuf = ring + vs * V_STAGE;
-  float* lbuf = reinterpret_cast<float*>(pbuf + 2 * PB + 1024);
-  float* wsm = lbuf + 2 * V_HP * max_tok;
-  int* ulist = reinterpret_cast<int*>(wsm + V_HP * ns);
-  float* red = reinterpret_cast<float*>(ulist + ((ns + 3) & ~3));
-  uint64_t* full = reinterpret_cast<uint64_t*>(red + 4 * 128);
+  float* stat = reinterpret_cast<float*>(pbuf + 2 * PB + 1024);  // [2][2][V_HP] (m, l) per sub-block
+  uint64_t* full = reinterpret_cast<uint64_t*>(stat + 4 * V_HP);
   uint64_t* empty = full + vs;
-  uint64_t* pfull = empty + vs;   // [2] P buffer written
-  uint64_t* dfull = pfull + 2;    // [2] accumulator complete
-  uint64_t* dempty = dfull + 2;   // [2] accumulator read back
+  uint64_t* pfull = empty + vs;   // [2] P sub-block written (+ its statistics)
+  uint64_t* dfull = pfull + 2;    // [2] sub-block accumulator complete (P consumed)
+  uint64_t* dempty = dfull + 2;   // [2] sub-block accumulator read back
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
-  __shared__ float red_m[4][V_HP], red_l[4][V_HP], inv_l[V_HP];
-  __shared__ unsigned ticket_sh;
-  __shared__ int nu_sh, go_sh;
+  __shared__ float red_m[4][V_HP], red_l[4][V_HP];
 
   if (tid == 0) {
     for (int st = 0; st < vs; ++st) {
@@ -474,6 +471,13 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
         for (int blk = 0; blk < nblk; ++blk)
           for (int j = 0; j < NJ; ++j, ++ctr) {
             const int st = ctr % vs;
+            // warm L2 with the rows V_PF blocks ahead: the ring turnaround then
+            // sees L2 rather than loaded-HBM latency
+            if (V_PF > 0 && blk + V_PF < nblk) {
+              const int rowp = u.bg * p.T_cap + c0 + (blk + V_PF) * TILE_M;
+              tma_prefetch_l2(&map_v, j * 128, rowp);
+              tma_prefetch_l2(&map_v, j * 128 + 64, rowp);
+            }
             mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
             mbar_expect_tx(&full[st], V_STAGE);
             const int row = u.bg * p.T_cap + c0 + blk * TILE_M;
@@ -485,33 +489,45 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     return;
   }
   if (warp == 9) {
-    // ---------------- MMA issuer: D[buf][j] += V^T x P^T per 128-token block
+    // ---------------- MMA issuer: per V_SUB-token sub-block sb (buffer sb & 1)
+    // D[buf][j] = V^T x P^T over the sub-block's 128-token blocks
     if (lane == 0) {
-      int ctr = 0, k = 0;
+      int ctr = 0, sb = 0;
       while (it.next(u)) {
         const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
         const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
-        const int buf = k & 1;
-        mbar_wait(&pfull[buf], (k >> 1) & 1);
-        if (k >= 2) mbar_wait(&dempty[buf], ((k >> 1) - 1) & 1);
-        fence_after();
-        const uint32_t pb = smem_u32(pbuf + buf * PB);
-        for (int blk = 0; blk < nblk; ++blk)
-          for (int j = 0; j < NJ; ++j, ++ctr) {
-            const int st = ctr % vs;
-            mbar_wait(&full[st], (ctr / vs) & 1);
-            fence_after();
-            const uint32_t a0 = smem_u32(ring + st * V_STAGE);
-            const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
+        for (int b0 = 0; b0 < nblk; b0 += V_SUB / TILE_M, ++sb) {
+          const int buf = sb & 1;
+          if ((p.mode & 2) == 0) mbar_wait(&pfull[buf], (sb >> 1) & 1);
+          if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
+          fence_after();
+          const uint32_t pb = smem_u32(pbuf + buf * PB);
+          const int b1 = min(nblk, b0 + V_SUB / TILE_M);
+          for (int blk = b0; blk < b1; ++blk)
+            for (int j = 0; j < NJ; ++j, ++ctr) {
+              const int st = ctr % vs;
+              mbar_wait(&full[st], (ctr / vs) & 1);
+              fence_after();
+              if (p.mode & 1) {  // diagnostics: release the stage without MMAs
+                mbar_arrive(&empty[st]);
+                continue;
+              }
+              const uint32_t a0 = smem_u32(ring + st * V_STAGE);
+              const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
 #pragma unroll
-            for (int kk = 0; kk < TILE_M / 16; ++kk)
-              umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, V_STAGE / 2, 1024),
-                           sdesc(pb + (blk * 2 + kk / 4) * 1024 + (kk % 4) * 32), IDESC_V,
-                           (blk | kk) != 0);
-            umma_commit(&empty[st]);
+              for (int kk = 0; kk < TILE_M / 16; ++kk)
+                umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, V_STAGE / 2, 1024),
+                             sdesc(pb + ((blk - b0) * 2 + kk / 4) * 1024 + (kk % 4) * 32), IDESC_V,
+                             (blk != b0) || (kk != 0));
+              umma_commit(&empty[st]);
+            }
+          if (p.mode & 1) {
+            if ((p.mode & 2) != 0) mbar_wait(&pfull[buf], (sb >> 1) & 1);
+            mbar_arrive(&dfull[buf]);
+          } else {
+            umma_commit(&dfull[buf]);
           }
-        umma_commit(&dfull[buf]);
-        ++k;
+        }
       }
     }
     __syncwarp();
@@ -530,207 +546,186 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       if (p.trace != nullptr && ta == 0 && 5 * kk_trace + 8 < TRACE_STRIDE)
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 5 * kk_trace + slot] = gtimer();
     };
-    // wait for the unit's score items, then cp.async its logits (V_HP rows of
-    // the padded token range) into lbuf[buf]; one commit group per unit
-    auto fetch = [&](const VUnit& x, int buf) {
-      if (ta == 0) {
-        for (int i = x.item0; i < x.item0 + (x.st1 - x.st0); ++i)
+    int sb = 0;
+    while (it.next(u)) {
+      if (ta == 0 && !vp.no_wait) {
+        for (int i = u.item0; i < u.item0 + (u.st1 - u.st0); ++i)
           while (ld_acquire_u32(&p.ready[i]) < 2u * (EPI_WARPS / 2)) __nanosleep(64);
       }
-      named_bar_sync(3, 128);
-      const int b = x.bg / p.G, g = x.bg - b * p.G;
-      const int c0 = x.st0 * SUPER, c1 = min(T_rows, x.st1 * SUPER);
-      const int n16 = (c1 - c0 + 3) / 4;  // 16-byte granules per head row
-      const float* src = p.logits + ((size_t)b * p.n_heads + g * s_v) * p.ld_logits + c0;
-      float* dst = lbuf + buf * V_HP * max_tok;
-      for (int i = ta; i < s_v * n16; i += 128) {
-        const int h = i / n16, q = i - h * n16;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
-                         smem_u32(dst + h * max_tok + 4 * q)),
-                     "l"(src + (size_t)h * p.ld_logits + 4 * q)
-                     : "memory");
-      }
-      asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    int k = 0;
-    VUnit nx;
-    bool have = it.next(u);
-    if (have) fetch(u, 0);
-    while (have) {
-      const bool more = it.next(nx);
-      if (more) fetch(nx, (k + 1) & 1);
-      if (more)
-        asm volatile("cp.async.wait_group 1;" ::: "memory");
-      else
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
       named_bar_sync(3, 128);
       trace(0);
       const int b = u.bg / p.G, g = u.bg - b * p.G;
       const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
       const int nt = c1 - c0;
       const int ntok = (nt + TILE_M - 1) / TILE_M * TILE_M;  // padded to whole blocks
-      const int buf = k & 1;
-      const float* lg = lbuf + buf * V_HP * max_tok;
-      // (1) per-head max over the unit (thread = token pairs)
-      float m[V_HP];
+      const float* lg = p.logits + ((size_t)b * p.n_heads + g * s_v) * p.ld_logits + c0;
+      // the sub-block's logits (thread = token pairs 2 ta + 256 i); the next
+      // sub-block's are loaded while this one is processed
+      constexpr int NP = V_SUB / 256;
+      float2 x[NP][V_HP], xn[NP][V_HP];
+      auto load = [&](int s0, float2 (&dst)[NP][V_HP]) {
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
-      for (int t = 2 * ta; t < nt; t += 256) {
+        for (int i = 0; i < NP; ++i) {
+          const int t = s0 + 2 * ta + 256 * i;
 #pragma unroll
-        for (int h = 0; h < V_HP; ++h)
-          if (h < s_v) {
-            const float2 v = *reinterpret_cast<const float2*>(lg + h * max_tok + t);
-            m[h] = fmaxf(m[h], t + 1 < nt ? fmaxf(v.x, v.y) : v.x);
+          for (int h = 0; h < V_HP; ++h) {
+            float2 v = make_float2(-INFINITY, -INFINITY);
+            if (h < s_v && t < nt) {
+              v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
+              if (t + 1 >= nt) v.y = -INFINITY;
+            }
+            dst[i][h] = v;
           }
-      }
+        }
+      };
+      load(0, xn);
+      for (int s0 = 0; s0 < ntok; s0 += V_SUB, ++sb) {
+        const int buf = sb & 1;
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h) {
-        m[h] = warp_reduce(m[h], [](float a, float c) { return fmaxf(a, c); });
-        if (lane == 0) red_m[warp][h] = m[h];
-      }
-      // P buffer `buf` is free once the MMAs of unit k - 2 are read back
-      if (k >= 2) mbar_wait(&dempty[buf], ((k >> 1) - 1) & 1);
-      named_bar_sync(3, 128);
-      trace(2);
+        for (int i = 0; i < NP; ++i)
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h)
-        m[h] = fmaxf(fmaxf(red_m[0][h], red_m[1][h]), fmaxf(red_m[2][h], red_m[3][h]));
-      // (2) P = hi + lo bf16 (rows h and h + 4 of the K-major SW128 operand:
-      // ~16 mantissa bits of p at no extra tensor work); zeros past the last
-      // token; l sums the fp32 probabilities
-      uint8_t* pb = pbuf + buf * PB;
-      float l[V_HP];
+          for (int h = 0; h < V_HP; ++h) x[i][h] = xn[i][h];
+        if (s0 + V_SUB < ntok) load(s0 + V_SUB, xn);
+        // (1) max of the sub-block
+        float m[V_HP];
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h) l[h] = 0.f;
-      for (int t = 2 * ta; t < ntok; t += 256) {
-        const int blk = t >> 6, w = t & 63;
-        const uint32_t rowb = blk * 1024 + (w & 7) * 2;
+        for (int h = 0; h < V_HP; ++h) m[h] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < NP; ++i)
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) m[h] = fmaxf(m[h], fmaxf(x[i][h].x, x[i][h].y));
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
-          if (h < s_v) {
-            const float2 v = t < nt ? *reinterpret_cast<const float2*>(lg + h * max_tok + t)
-                                    : make_float2(-INFINITY, -INFINITY);
-            const float p0 = __expf(v.x - m[h]), p1 = t + 1 < nt ? __expf(v.y - m[h]) : 0.f;
-            const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
-            const float2 hf = __bfloat1622float2(hi);
-            const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
-            l[h] += p0 + p1;
-            *reinterpret_cast<__nv_bfloat162*>(pb + rowb + h * 128 + ((((w >> 3) ^ h) & 7) << 4)) = hi;
-            *reinterpret_cast<__nv_bfloat162*>(pb + rowb + (h + 4) * 128 +
-                                               ((((w >> 3) ^ (h + 4)) & 7) << 4)) = lo;
+          m[h] = warp_reduce(m[h], [](float a, float c) { return fmaxf(a, c); });
+          if (lane == 0) red_m[warp][h] = m[h];
+        }
+        // buffer `buf` (P operand + statistics) is free once sub-block sb - 2
+        // has been read back
+        if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
+        named_bar_sync(3, 128);
+        trace(2);
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h)
+          m[h] = fmaxf(fmaxf(red_m[0][h], red_m[1][h]), fmaxf(red_m[2][h], red_m[3][h]));
+        // (2) P = hi + lo bf16 (rows h and h + 4 of the K-major SW128 operand:
+        // ~16 mantissa bits of p at no extra tensor work), zeros past the
+        // last token; l sums the fp32 probabilities
+        uint8_t* pb = pbuf + buf * PB;
+        float l[V_HP];
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h) l[h] = 0.f;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          const int tl = 2 * ta + 256 * i;
+          if (s0 + tl < ntok) {
+            const int blk = tl >> 6, w = tl & 63;
+            const uint32_t rowb = blk * 1024 + (w & 7) * 2;
+#pragma unroll
+            for (int h = 0; h < V_HP; ++h) {
+              if (h < s_v) {
+                const float p0 = __expf(x[i][h].x - m[h]), p1 = __expf(x[i][h].y - m[h]);
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
+                const float2 hf = __bfloat1622float2(hi);
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+                l[h] += p0 + p1;
+                *reinterpret_cast<__nv_bfloat162*>(pb + rowb + h * 128 + ((((w >> 3) ^ h) & 7) << 4)) = hi;
+                *reinterpret_cast<__nv_bfloat162*>(pb + rowb + (h + 4) * 128 +
+                                                   ((((w >> 3) ^ (h + 4)) & 7) << 4)) = lo;
+              }
+            }
           }
         }
-      }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 #pragma unroll
-      for (int h = 0; h < V_HP; ++h) {
-        l[h] = warp_reduce(l[h], [](float a, float c) { return a + c; });
-        if (lane == 0) red_l[warp][h] = l[h];
-      }
-      named_bar_sync(3, 128);
-      if (ta == 0) mbar_arrive(&pfull[buf]);
-#pragma unroll
-      for (int h = 0; h < V_HP; ++h)
-        if (ta == h && h < s_v) {
-          const size_t pi = ((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0;
-          vp.pm[pi] = m[h];
-          vp.pl[pi] = red_l[0][h] + red_l[1][h] + red_l[2][h] + red_l[3][h];
+        for (int h = 0; h < V_HP; ++h) {
+          l[h] = warp_reduce(l[h], [](float a, float c) { return a + c; });
+          if (lane == 0) red_l[warp][h] = l[h];
         }
+        named_bar_sync(3, 128);
+        if (ta < V_HP) {
+          float mh = m[0], lh = 0.f;
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h)
+            if (ta == h) {
+              mh = m[h];
+              lh = (red_l[0][h] + red_l[1][h]) + (red_l[2][h] + red_l[3][h]);
+            }
+          stat[(buf * 2 + 0) * V_HP + ta] = mh;
+          stat[(buf * 2 + 1) * V_HP + ta] = lh;
+        }
+        named_bar_sync(3, 128);
+        if (ta == 0) mbar_arrive(&pfull[buf]);
+      }
       trace(1);
       if (p.trace != nullptr) ++kk_trace;
-      u = nx;
-      have = more;
-      ++k;
     }
   } else {
-    // ======== group B (warps 4-7): accumulator -> partial, ticket, merge ========
+    // ======== group B (warps 4-7): sub-block accumulators -> unit partial ========
+    // online softmax across the unit's sub-blocks in registers: thread = one
+    // V column per 128-column pair j, all heads
     const int tb = tid - 128, wb = warp - 4;  // wb = TMEM lane quarter
-    int k = 0;
+    int sb = 0;
     while (it.next(u)) {
-      const int buf = k & 1;
       const int b = u.bg / p.G, g = u.bg - b * p.G;
-      mbar_wait(&dfull[buf], (k >> 1) & 1);
-      fence_after();
-      for (int j = 0; j < NJ; ++j) {
-        float v[16];
-        tmem_ld16(tmem + ((uint32_t)(wb * 32) << 16) + (uint32_t)((buf * NJ + j) * 16), v);
-        tmem_wait_ld();
+      const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
+      const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
+      float acc[4][V_HP], mr[V_HP], lr[V_HP];
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) {
+        mr[h] = -INFINITY;
+        lr[h] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][h] = 0.f;
+      }
+      for (int b0 = 0; b0 < nblk; b0 += V_SUB / TILE_M, ++sb) {
+        const int buf = sb & 1;
+        mbar_wait(&dfull[buf], (sb >> 1) & 1);
+        fence_after();
+        float sc_old[V_HP], sc_new[V_HP];
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h) {
+          const float ms = stat[(buf * 2 + 0) * V_HP + h], ls = stat[(buf * 2 + 1) * V_HP + h];
+          const float mn = fmaxf(mr[h], ms);
+          sc_old[h] = mr[h] == -INFINITY ? 0.f : __expf(mr[h] - mn);
+          sc_new[h] = ms == -INFINITY ? 0.f : __expf(ms - mn);
+          lr[h] = lr[h] * sc_old[h] + ls * sc_new[h];
+          mr[h] = mn;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (j < NJ) {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(wb * 32) << 16) + (uint32_t)((buf * NJ + j) * 16), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int h = 0; h < V_HP; ++h)
+              acc[j][h] = acc[j][h] * sc_old[h] + (v[h] + v[h + V_HP]) * sc_new[h];
+          }
+        }
+        fence_before();
+        named_bar_sync(4, 128);
+        if (tb == 0) mbar_arrive(&dempty[buf]);
+      }
+      // the unit's partial: columns of all heads, statistics
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
         const int col = j * 128 + wb * 32 + lane;
-        if (col < vp.Rv_pad) {
+        if (j < NJ && col < vp.Rv_pad) {
 #pragma unroll
           for (int h = 0; h < V_HP; ++h)
             if (h < s_v)
-              vp.pctx[(((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0) * vp.Rv_pad + col] =
-                  v[h] + v[h + V_HP];
+              vp.pctx[(((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0) * vp.Rv_pad + col] = acc[j][h];
         }
       }
-      fence_before();
-      named_bar_sync(4, 128);
-      if (tb == 0) {
-        mbar_arrive(&dempty[buf]);
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+        if (tb == h && h < s_v) {
+          const size_t pi = ((size_t)b * p.n_heads + g * s_v + h) * ns + u.st0;
+          vp.pm[pi] = mr[h];
+          vp.pl[pi] = lr[h];
+        }
+      if (tb == 0 && !vp.no_wait)
         for (int i = u.item0; i < u.item0 + (u.st1 - u.st0); ++i) p.ready[i] = 0;
-      }
-      ++k;
-      __threadfence();
-      named_bar_sync(4, 128);
-      if (tb == 0) {
-        ticket_sh = atomicAdd(&vp.tickets[u.bg], (unsigned)(u.st1 - u.st0)) + (unsigned)(u.st1 - u.st0);
-        go_sh = ticket_sh == (unsigned)n_super;
-        if (go_sh) {
-          int nu = 0;  // the group's sub-unit slots, in token order (fixed merge order)
-          for (int x = 0; x < n_super;) {
-            ulist[nu++] = x;
-            x = min(sch.win_end(u.bg * n_super + x), (u.bg + 1) * n_super) - u.bg * n_super;
-          }
-          nu_sh = nu;
-        }
-      }
-      named_bar_sync(4, 128);
-      if (!go_sh) continue;
-      __threadfence();
-      const int nu = nu_sh;
-      const int r = vp.ranks_v[g];
-      if (wb < s_v) {
-        const size_t base = ((size_t)b * p.n_heads + g * s_v + wb) * ns;
-        float M = -INFINITY;
-        for (int q = lane; q < nu; q += 32) M = fmaxf(M, __ldcg(vp.pm + base + ulist[q]));
-        M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
-        float Ls = 0.f;
-        for (int q = lane; q < nu; q += 32) {
-          const float w = __expf(__ldcg(vp.pm + base + ulist[q]) - M);
-          wsm[wb * ns + q] = w;
-          Ls += w * __ldcg(vp.pl + base + ulist[q]);
-        }
-        Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
-        if (lane == 0) inv_l[wb] = 1.f / Ls;
-      }
-      named_bar_sync(4, 128);
-      // unit-parallel over 4 warps, 128 columns per round, fixed summation order
-      for (int h = 0; h < s_v; ++h) {
-        const float* src =
-            vp.pctx + ((size_t)b * p.n_heads + g * s_v + h) * ns * (size_t)vp.Rv_pad;
-        for (int col0 = 0; col0 < r; col0 += 128) {
-          float a4[4] = {0.f, 0.f, 0.f, 0.f};
-          for (int q = wb; q < nu; q += 4) {
-            const float w = wsm[h * ns + q];
-            const float* srow = src + (size_t)ulist[q] * vp.Rv_pad;
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq) {
-              const int col = col0 + lane + 32 * qq;
-              if (col < r) a4[qq] = fmaf(w, __ldcg(srow + col), a4[qq]);
-            }
-          }
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) red[wb * 128 + lane + 32 * qq] = a4[qq];
-          named_bar_sync(4, 128);
-          if (col0 + tb < r) {
-            const float v = (red[tb] + red[128 + tb]) + (red[256 + tb] + red[384 + tb]);
-            vp.ctx_out[(size_t)b * vp.ld_ctx + vp.o_off[g * s_v + h] + col0 + tb] = v * inv_l[h];
-          }
-          named_bar_sync(4, 128);
-        }
-      }
-      if (tb == 0) vp.tickets[u.bg] = 0u;
     }
   }
   named_bar_sync(2, 288);
@@ -758,6 +753,109 @@ rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
     value_role(map_v, p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
   }
+}
+
+// Deterministic merge of the value units' partials (runs after the fused or
+// the standalone value kernel): block = (128 columns, head, sequence).  The
+// group's unit slots are found in parallel (a slot starts a unit iff it is
+// the group's first super-tile or a window start of the VSched), compacted in
+// token order, and summed with 8 independent float4 loads in flight.
+__global__ void __launch_bounds__(128)
+value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
+                   const float* __restrict__ pctx, int ns, int Rv_pad, int n_heads, int s_v, int G,
+                   int B, const int* __restrict__ t_dev, int score_pairs, int vc,
+                   const int* __restrict__ ranks_v, const int* __restrict__ o_off,
+                   float* __restrict__ ctx, int ld_ctx) {
+  extern __shared__ float msm[];
+  float* w = msm;                                    // [ns]
+  int* ulist = reinterpret_cast<int*>(msm + ns);     // [ns]
+  __shared__ int wcount[4];
+  __shared__ float inv_l_sh;
+  const int head = blockIdx.y, b = blockIdx.z, g = head / s_v;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int T_rows = *t_dev + 1;
+  const int n_super = (T_rows + SUPER - 1) / SUPER;
+  const int total = B * G * n_super;
+  const int per = (total + score_pairs - 1) / score_pairs;
+  const int bg = b * G + g;
+  if (vc <= 0) vc = per;  // standalone value kernel: one window per CTA
+  // (1) unit starts of this group, compacted in order (chunks of 128 slots)
+  int nu = 0;
+  for (int x0 = 0; x0 < n_super; x0 += 128) {
+    const int x = x0 + tid;
+    bool start = false;
+    if (x < n_super) {
+      const int a = bg * n_super + x;
+      const int off = a - (a / per) * per;
+      start = x == 0 || off % vc == 0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, start);
+    if (lane == 0) wcount[warp] = __popc(bal);
+    __syncthreads();
+    int before = nu;
+    for (int q = 0; q < warp; ++q) before += wcount[q];
+    if (start) ulist[before + __popc(bal & ((1u << lane) - 1u))] = x;
+    nu += wcount[0] + wcount[1] + wcount[2] + wcount[3];
+    __syncthreads();
+  }
+  // (2) chunk weights exp(m_u - M) and 1 / sum_u w_u l_u
+  const size_t base = ((size_t)b * n_heads + head) * ns;
+  if (warp == 0) {
+    float M = -INFINITY;
+    for (int q = lane; q < nu; q += 32) M = fmaxf(M, __ldcg(pm + base + ulist[q]));
+    M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
+    float Ls = 0.f;
+    for (int q = lane; q < nu; q += 32) {
+      const float wq = __expf(__ldcg(pm + base + ulist[q]) - M);
+      w[q] = wq;
+      Ls += wq * __ldcg(pl + base + ulist[q]);
+    }
+    Ls = warp_reduce(Ls, [](float x, float y) { return x + y; });
+    if (lane == 0) inv_l_sh = 1.f / Ls;
+  }
+  __syncthreads();
+  // (3) lane = 4 columns of this block's 128; warp w sums units w, w + 4, ...
+  // (8 float4 loads in flight), then the 4 warp sums combine in a fixed order
+  __shared__ float4 part4[4][32];
+  const int r = ranks_v[g];
+  const int col = blockIdx.x * 128 + 4 * lane;
+  const float* src = pctx + base * (size_t)Rv_pad + min(col, Rv_pad - 4);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+  for (int q = warp; q < nu; q += 4) {
+    const float wq = w[q];
+    const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ulist[q] * Rv_pad));
+    acc.x = fmaf(wq, v.x, acc.x);
+    acc.y = fmaf(wq, v.y, acc.y);
+    acc.z = fmaf(wq, v.z, acc.z);
+    acc.w = fmaf(wq, v.w, acc.w);
+  }
+  part4[warp][lane] = acc;
+  __syncthreads();
+  if (warp != 0 || col >= r) return;
+  const float4 a0 = part4[0][lane], a1 = part4[1][lane], a2 = part4[2][lane], a3 = part4[3][lane];
+  const float il = inv_l_sh;
+  const float av[4] = {((a0.x + a1.x) + (a2.x + a3.x)) * il, ((a0.y + a1.y) + (a2.y + a3.y)) * il,
+                       ((a0.z + a1.z) + (a2.z + a3.z)) * il, ((a0.w + a1.w) + (a2.w + a3.w)) * il};
+  float* dst = ctx + (size_t)b * ld_ctx + o_off[head] + col;
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (col + e < r) dst[e] = av[e];
+}
+
+// Standalone softmax + value pass on tcgen05 (after palu_rope_score_tc): every
+// CTA runs value_role over a round-robin share of the (sequence, group)
+// units; no readiness protocol.
+__global__ void __launch_bounds__(THREADS, 1)
+value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const VParams vp) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  if (p.trace != nullptr && threadIdx.x == 0) {
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 0] = gtimer();
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
+  }
+  value_role(map_v, p, vp, smem, (int)blockIdx.x, (int)gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -940,13 +1038,59 @@ static int fused_ns_cap(int T_cap) {
   return (T_cap + SUPER - 1) / SUPER;
 }
 
-size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap) {
+// Workspace carve-up shared by the fused and standalone value kernels; every
+// array starts on a 256-byte boundary (float4 partial loads in the merge).
+struct ValueWs {
+  unsigned* tickets;
+  int* ready;
+  float *pm, *pl, *pctx;
+  size_t bytes;
+};
+static ValueWs value_ws(void* base, int B, int n_heads, int G, int Rv_pad, int T_cap) {
   using palu::tc::SUPER;
-  const int nc = fused_ns_cap(T_cap);
+  auto up = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t nc = fused_ns_cap(T_cap);
   const size_t items = (size_t)B * G * ((T_cap + SUPER - 1) / SUPER);
   const size_t head = (size_t)B * n_heads * nc;
-  return 256 + sizeof(unsigned) * (size_t)B * G + sizeof(int) * items + sizeof(float) * head * 2 +
-         sizeof(float) * head * (size_t)Rv_pad + 1024;
+  uint8_t* p = reinterpret_cast<uint8_t*>(base);
+  size_t o = 256;
+  ValueWs w;
+  w.tickets = reinterpret_cast<unsigned*>(p + o);
+  o = up(o + sizeof(unsigned) * (size_t)B * G);
+  w.ready = reinterpret_cast<int*>(p + o);
+  o = up(o + sizeof(int) * items);
+  w.pm = reinterpret_cast<float*>(p + o);
+  o = up(o + sizeof(float) * head);
+  w.pl = reinterpret_cast<float*>(p + o);
+  o = up(o + sizeof(float) * head);
+  w.pctx = reinterpret_cast<float*>(p + o);
+  o = up(o + sizeof(float) * head * (size_t)Rv_pad);
+  w.bytes = o;
+  return w;
+}
+
+size_t palu_rope_attend_workspace(int B, int n_heads, int G, int Rv_pad, int T_cap) {
+  return value_ws(nullptr, B, n_heads, G, Rv_pad, T_cap).bytes;
+}
+
+static int launch_value_merge(const float* pm, const float* pl, const float* pctx, int ns, int Rv_pad,
+                              int n_heads, int s, int G, int B, const int* t_dev, int score_pairs,
+                              int vc, const int* ranks_v, const int* o_off, float* ctx, int ld_ctx,
+                              cudaStream_t st) {
+  using namespace palu::tc;
+  const size_t smem = (size_t)ns * 8;
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(value_merge_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 100 * 1024));
+    attr = true;
+  }
+  PALU_REQUIRE(smem <= 100 * 1024, "value merge: too many super-tiles (%d)", ns);
+  value_merge_kernel<<<dim3((Rv_pad + 127) / 128, n_heads, B), 128, smem, st>>>(
+      pm, pl, pctx, ns, Rv_pad, n_heads, s, G, B, t_dev, score_pairs, vc, ranks_v, o_off, ctx,
+      ld_ctx);
+  PALU_LAUNCHED();
+  return PALU_OK;
 }
 
 int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int s, int G,
@@ -993,12 +1137,10 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   const int vc = getenv("PALU_FUSED_VC") ? atoi(getenv("PALU_FUSED_VC")) : 4;  // tuning only
   const int nc_max = fused_ns_cap(T_cap);
   uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
-  unsigned* tickets = reinterpret_cast<unsigned*>(ws + 256);
-  int* ready = reinterpret_cast<int*>(tickets + (size_t)B * G);
-  const size_t items = (size_t)B * G * ((T_cap + SUPER - 1) / SUPER);
-  float* pm = reinterpret_cast<float*>(ready + items);
-  float* pl = pm + (size_t)B * n_heads * nc_max;
-  float* pctx = pl + (size_t)B * n_heads * nc_max;
+  const ValueWs W = value_ws(ws, B, n_heads, G, Rv_pad, T_cap);
+  unsigned* tickets = W.tickets;
+  int* ready = W.ready;
+  float *pm = W.pm, *pl = W.pl, *pctx = W.pctx;
   Params prm;
   prm.B = B;
   prm.n_heads = n_heads;
@@ -1029,14 +1171,12 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   VParams vp;
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
-  const size_t pbytes = (size_t)2 * (vc * SUPER / 64) * 1024 + 1024;
-  const size_t side = pbytes + sizeof(float) * ((size_t)2 * V_HP * vc * SUPER + (size_t)V_HP * nc_max +
-                                                (size_t)((nc_max + 3) & ~3) + 4 * 128) + 16 * 64 + 64;
+  const size_t side = (size_t)2 * (V_SUB / 64) * 1024 + 1024 + 4 * V_HP * 4 + 16 * 64 + 64;
   // the value role takes whatever the score role leaves: launch at the limit
   const size_t smem_launch = (size_t)dyn_limit;
   vp.v_stages = (int)(((long long)smem_launch - 1024 - (long long)side) / V_STAGE);
   PALU_REQUIRE(vp.v_stages >= 2, "palu_rope_attend_tc: value ring too small (%d)", vp.v_stages);
-  if (vp.v_stages > 8) vp.v_stages = 8;
+  if (vp.v_stages > 8) vp.v_stages = 8;  // 32 KB stages
   vp.tickets = tickets;
   vp.pm = pm;
   vp.pl = pl;
@@ -1046,6 +1186,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   vp.o_off = o_off;
   vp.ctx_out = ctx;
   vp.ld_ctx = ld_ctx;
+  vp.no_wait = 0;
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1055,7 +1196,81 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   rope_attend_tc_kernel<<<dim3(sms), THREADS, smem_launch, (cudaStream_t)stream>>>(map_h, map_uw,
                                                                                   map_v, prm, vp);
   PALU_LAUNCHED();
-  return PALU_OK;
+  return launch_value_merge(pm, pl, pctx, nc_max, Rv_pad, n_heads, s, G, B, t_dev, prm.score_pairs,
+                            vc, ranks_v, o_off, ctx, ld_ctx, (cudaStream_t)stream);
+}
+
+
+// Standalone tcgen05 softmax + value (the unfused path's second kernel).
+int palu_value_tc(const void* hv, int B, int n_heads, int s, int G, int Rv_pad, int T_cap,
+                  const float* logits, int ld_logits, const int* t_dev, const int* ranks_v,
+                  const int* o_off, float* ctx, int ld_ctx, void* workspace, void* stream) {
+  using namespace palu::tc;
+  if (G * s != n_heads || Rv_pad % KB != 0 || Rv_pad > 512 || s > V_HP) {
+    set_error("palu_value_tc: unsupported shape (Rv %d, s %d)", Rv_pad, s);
+    return PALU_EUNSUPPORTED;
+  }
+  PALU_REQUIRE(((uintptr_t)hv & 15) == 0, "palu_value_tc: unaligned H_v");
+  CUtensorMap map_v;
+  int rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int vc = 0;
+  const int nc_max = fused_ns_cap(T_cap);
+  uint8_t* ws = reinterpret_cast<uint8_t*>(workspace);
+  const ValueWs W = value_ws(ws, B, n_heads, G, Rv_pad, T_cap);
+  unsigned* tickets = W.tickets;
+  int* ready = W.ready;
+  float *pm = W.pm, *pl = W.pl, *pctx = W.pctx;
+  Params prm = {};
+  prm.B = B;
+  prm.n_heads = n_heads;
+  prm.s_k = s;
+  prm.G = G;
+  prm.T_cap = T_cap;
+  prm.ld_logits = ld_logits;
+  prm.score_pairs = sms;  // one contiguous window of items per CTA (vc = per)
+  prm.mode = getenv("PALU_VALUE_DIAG") ? atoi(getenv("PALU_VALUE_DIAG")) : 0;  // diagnostics only
+  prm.ready = ready;
+  prm.t_dev = t_dev;
+  prm.logits = const_cast<float*>(logits);
+  prm.trace = nullptr;
+  if (getenv("PALU_FUSED_TRACE")) {
+    if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
+    PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));
+    prm.trace = g_trace;
+    g_trace_ctas = sms;
+  }
+  VParams vp;
+  vp.Rv_pad = Rv_pad;
+  vp.vc = vc;
+  const int dyn_limit = SMEM_LIMIT - 2048;
+  const size_t side = (size_t)2 * (V_SUB / 64) * 1024 + 1024 + 4 * V_HP * 4 + 16 * 64 + 64;
+  vp.v_stages = (int)(((long long)dyn_limit - 1024 - (long long)side) / V_STAGE);
+  PALU_REQUIRE(vp.v_stages >= 2, "palu_value_tc: value ring too small (%d)", vp.v_stages);
+  if (vp.v_stages > 8) vp.v_stages = 8;  // 32 KB stages
+  vp.tickets = tickets;
+  vp.pm = pm;
+  vp.pl = pl;
+  vp.pctx = pctx;
+  vp.ns_cap = nc_max;
+  vp.ranks_v = ranks_v;
+  vp.o_off = o_off;
+  vp.ctx_out = ctx;
+  vp.ld_ctx = ld_ctx;
+  vp.no_wait = 1;
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(value_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 dyn_limit));
+    attr = true;
+  }
+  value_tc_kernel<<<dim3(sms), THREADS, dyn_limit, (cudaStream_t)stream>>>(map_v, prm, vp);
+  PALU_LAUNCHED();
+  return launch_value_merge(pm, pl, pctx, nc_max, Rv_pad, n_heads, s, G, B, t_dev, sms, vc, ranks_v,
+                            o_off, ctx, ld_ctx, (cudaStream_t)stream);
 }
 
 }  // extern "C"

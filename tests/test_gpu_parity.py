@@ -300,10 +300,10 @@ def test_fused_attend_matches_oracle(P, golden, which):
 
 @pytest.mark.parametrize("batch,context,rk,rv", [(3, 9000, 256, 256), (2, 20000, 128, 384),
                                                  (1, 300, 256, 256)])
-def test_fused_attend_long_batched(P, batch, context, rk, rv):
-    """Fused kernel vs the unfused tcgen05 + softmax-value path on the same
-    long, batched synthetic cache (many score items per pair, sub-units
-    straddling sequence/group boundaries, merge ordering)."""
+def test_fused_attend_long_batched(P, batch, context, rk, rv, monkeypatch):
+    """tcgen05 softmax-value kernel and the fused kernel vs the CUDA-core
+    softmax-value path on the same long, batched synthetic cache (many units
+    per CTA, sub-units straddling sequence/group boundaries, merge order)."""
     import torch
     from paper_2407_21118_b200.attention import _Session
     from paper_2407_21118_b200.harness import synthetic_engine
@@ -311,15 +311,18 @@ def test_fused_attend_long_batched(P, batch, context, rk, rv):
                                        rank_k=rk, rank_v=rv, seed=99)
     x0 = torch.randn(batch, 4096, device="cuda") * 0.5
     outs = {}
-    for sk in ("tcgen05", "fused"):
+    for name, sk, vk in (("simt_value", "tcgen05", "simt"), ("tc_value", "tcgen05", "tc"),
+                         ("fused", "fused", "tc")):
+        monkeypatch.setenv("PALU_VALUE_KERNEL", vk)
         s = _Session(fused, cache, score_kernel=sk, use_graph=False)
-        assert any(s.fused_layers) == (sk == "fused")
-        s.x.copy_(x0)
+        assert any(s.fused_layers) == (name == "fused")
+        assert any(s.value_tc_layers) == (name == "tc_value")
         for _ in range(2):  # second launch checks the self-resetting counters
             s.x.copy_(x0)
             s.t_dev.fill_(cache.t)
             s.launch_step()
         torch.cuda.synchronize()
-        outs[sk] = s.x.double().cpu().numpy()
-    e = rel_err(outs["fused"], outs["tcgen05"])
-    assert e < 2e-3, e
+        outs[name] = s.x.double().cpu().numpy()
+    for name in ("tc_value", "fused"):
+        e = rel_err(outs[name], outs["simt_value"])
+        assert e < 1e-3, (name, e)

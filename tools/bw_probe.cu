@@ -6,6 +6,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cuda_runtime.h>
+#include <cuda.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -114,6 +115,52 @@ __global__ void __launch_bounds__(288, 1) tma_stream(const uint8_t* src, size_t 
   if (acc == 12345.f) sink[0] = acc;
 }
 
+// 2-D tensor TMA streaming: rows of 256 bf16 (512 B), stage = 2 boxes {64 cols, box_rows}
+__global__ void __launch_bounds__(288, 1) tma2d_stream(const __grid_constant__ CUtensorMap map, int rows_per_cta,
+                                                       int stages, int box_rows, float* sink) {
+  extern __shared__ __align__(1024) uint8_t sm2[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm2) + 1023) & ~uintptr_t(1023));
+  const int chunk = 2 * box_rows * 128;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)stages * chunk);
+  uint64_t* empty = full + stages;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mb_init(&full[s], 1);
+      mb_init(&empty[s], 8);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int n = rows_per_cta / box_rows * 2;  // (row block, column pair) steps over 4 slabs -> 2 pairs
+  if (warp == 8) {
+    if (lane == 0)
+      for (int i = 0; i < n; ++i) {
+        const int s = i % stages;
+        mb_wait(&empty[s], ((i / stages) & 1) ^ 1);
+        mb_expect(&full[s], chunk);
+        const int row = blockIdx.x * rows_per_cta + (i / 2) * box_rows, col = (i & 1) * 128;
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                     ::"r"(su32(sm + (size_t)s * chunk)), "l"(&map), "r"(su32(&full[s])), "r"(col), "r"(row) : "memory");
+        asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];"
+                     ::"r"(su32(sm + (size_t)s * chunk + chunk / 2)), "l"(&map), "r"(su32(&full[s])), "r"(col + 64), "r"(row) : "memory");
+      }
+    return;
+  }
+  float acc = 0.f;
+  for (int i = 0; i < n; ++i) {
+    const int s = i % stages;
+    mb_wait(&full[s], (i / stages) & 1);
+    __syncwarp();
+    if (lane == 0) mb_arrive(&empty[s]);
+  }
+  if (acc == 12345.f) sink[0] = acc;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
 // plain loads: each thread keeps U 16-B loads in flight
 template <int U>
 __global__ void __launch_bounds__(256, 1) ldg_stream(const uint4* src, size_t per_cta16, float* sink) {
@@ -142,11 +189,45 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  int ctas_list[] = {1, 22, 120};
+  int ctas_list[] = {22, 148};
   cudaFuncSetAttribute(tma_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-  for (int mode : {1, 4})
+  {
+    void* fp = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+    cudaFuncSetAttribute(tma2d_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    const cuuint64_t rows_total = total / 512;
+    for (int box_rows : {128, 256})
+      for (int stages : {3, 5, 6}) {
+        const int chunk = 2 * box_rows * 128;
+        if ((size_t)chunk * stages > 200 * 1024) continue;
+        CUtensorMap map;
+        const cuuint64_t dims[2] = {256, rows_total};
+        const cuuint64_t strides[1] = {512};
+        const cuuint32_t box[2] = {64, (cuuint32_t)box_rows}, es[2] = {1, 1};
+        ((EncodeFn)fp)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        for (int ctas : {22, 148}) {
+          const int rows_per_cta = (int)(rows_total / 148) / 256 * 256;
+          const size_t smem = (size_t)chunk * stages + 16 * stages + 2048;
+          tma2d_stream<<<ctas, 288, smem>>>(map, rows_per_cta, stages, box_rows, sink);
+          cudaEventRecord(a);
+          tma2d_stream<<<ctas, 288, smem>>>(map, rows_per_cta, stages, box_rows, sink);
+          cudaEventRecord(b);
+          cudaEventSynchronize(b);
+          float ms;
+          cudaEventElapsedTime(&ms, a, b);
+          const double bytes = (double)rows_per_cta * 512;
+          printf("tma2d box_rows %3d stages %d ctas %3d: %7.1f GB/s per CTA, %7.1f total\n", box_rows, stages,
+                 ctas, bytes / (ms * 1e6), bytes * ctas / (ms * 1e6));
+        }
+      }
+  }
+  for (int mode : {1})
     for (int chunk : {32768, 65536})
       for (int stages : {3, 5}) {
+        if ((size_t)chunk * stages > 200 * 1024) continue;
         if ((size_t)chunk * stages > 200 * 1024) continue;
         for (int ctas : ctas_list) {
           const size_t per = (size_t)(32 << 20) / chunk * chunk;  // 32 MiB per CTA

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--rank-k", type=int, default=256)
     ap.add_argument("--rank-v", type=int, default=256)
     ap.add_argument("--batch", type=int, default=1)
+    ap.add_argument("--score-kernel", default="fused", help="fused | tcgen05 (standalone value kernel)")
     a = ap.parse_args()
     import torch
 
@@ -35,7 +36,7 @@ def main():
     _lib.load()
     w, f, c = synthetic_engine(layers=1, batch=a.batch, context=a.context, extra=64,
                                rank_k=a.rank_k, rank_v=a.rank_v)
-    s = _session(f, c, score_kernel="fused")
+    s = _session(f, c, score_kernel=a.score_kernel)
     s.x.normal_(0, 0.5)
     for _ in range(3):
         s.launch_step()
@@ -64,6 +65,8 @@ def main():
         ev = [us(x) for x in tr[i, 4:4 + cnt]]
         print(f"score CTA {i} (sm {tr[i, 2]}): {cnt} items, done at", [round(x, 1) for x in ev[:8]],
               "...", [round(x, 1) for x in ev[-3:]])
+    merges = [(us(tr[i, 500]), us(tr[i, 501])) for i in value if tr[i, 500] > 0]
+    print("merges (start, end) us:", [(round(a_, 1), round(b_, 1)) for a_, b_ in merges])
     for i in value[:6] + value[-2:]:
         k = int((tr[i, 4::5][:100] > 0).sum())
         rd = [us(tr[i, 4 + 5 * j]) for j in range(k)]
@@ -73,6 +76,8 @@ def main():
                        for j in range(k)]) / 1e3
         print(f"  group A phases (max, P, gap to next) median us: {np.median(ph, axis=0).round(2)}")
         stream = sum(dn[j] - max(rd[j], dn[j - 1] if j else us(tr[i, 0])) for j in range(k))
+        if tr[i, 500] > 0:
+            print(f"  merge {us(tr[i, 500]):.1f} -> {us(tr[i, 501]):.1f} us")
         print(f"value CTA {i} (sm {tr[i, 2]}): {k} chunks, start {us(tr[i, 0]):.1f} end "
               f"{us(tr[i, 1]):.1f}; busy {stream:.1f} us; first ready {rd[0]:.1f}, "
               f"per-chunk (ready->done):", [(round(r, 1), round(d, 1)) for r, d in zip(rd[:6], dn[:6])])
