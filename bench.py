@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--context", type=int, default=65536)
     ap.add_argument("--batch", type=int, default=1, help="sequences per GPU")
     ap.add_argument("--layers", type=int, default=LAYERS)
-    ap.add_argument("--bits", type=int, default=16)
+    ap.add_argument("--bits", default="16", help="latent bits: 16 | 2/3/4/8 | k_bits,v_bits (e.g. 16,4)")
     ap.add_argument("--rank-k", type=int, default=RANK, help="kept key rank per group (256 = uniform 50%%)")
     ap.add_argument("--rank-v", type=int, default=RANK, help="kept value rank per group (paper preset: 128/384)")
     ap.add_argument("--dtype", default="bfloat16")
@@ -47,7 +47,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true", help="skip the uncompressed comparators")
-    return ap.parse_args()
+    a = ap.parse_args()
+    b = [int(x) for x in str(a.bits).split(",")]
+    a.bits = b[0] if len(b) == 1 else (b[0], b[1])
+    return a
 
 
 METRIC = "RoPE-attn decode us/step & HBM GB/s vs roofline, Llama-2-7B layer, 4K-64K ctx"

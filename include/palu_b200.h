@@ -99,6 +99,8 @@ int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* 
  * bk: [G][bk_rows][s_k*d_h] in `dtype` (rows >= rank zero, bk_rows >= R_pad).
  * layout 0: uw fp32 [B][n][R_pad][d_h]  (cols j < h: u_j, j >= h: w_{j-h})
  * layout 1: uw bf16 [B][G][s_k*d_h][R_pad] (K-major rows, tcgen05 B operand)
+ * layouts 2/3: as 1 with the rank order permuted for int4 / int2 keys on the
+ *   tcgen05 path (groups of 8 / 16: rank k at position k < G/2 ? 2k : 2k-G+1)
  */
 int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, int head_dim,
                       int s_k, const void* bk, int bk_rows, int R_pad, const double* theta,
@@ -117,19 +119,22 @@ int palu_rope_score(int dtype, int bits, const void* hk, const float* scales, co
                     int ld_logits, void* stream);
 
 /*
- * tcgen05 (sm_100a) RoPE score kernel, bf16 raw latents.  Same math as
- * palu_rope_score with uw in layout 1.  The rank is split into
- * palu_rope_score_tc_splits(s_k, R_pad) = KS slices (so the resident UW
- * operand fits in shared memory); slice ks writes partial logits to plane
- * ks (logits + ks * plane_stride) and palu_softmax_value adds the planes.
- * Requires d_h 128, s_k in {2, 4}, R_pad a multiple of 64 (KS != 0);
- * returns PALU_EUNSUPPORTED otherwise.
+ * tcgen05 (sm_100a) RoPE score kernel (attention.py:433-444): same math as
+ * palu_rope_score with uw in layout 1 (bf16 [B][G][s_k*128][R_pad]); logits
+ * [B][n][ld_logits].  Requires d_h 128, s_k in {2, 4}, R_pad a multiple of 64
+ * and <= 256 (palu_rope_score_tc_splits != 0); PALU_EUNSUPPORTED otherwise.
+ * bits 16: hk is bf16 [B][G][T_cap][R_pad].  bits 2/3/4/8: hk holds the
+ * packed codes [B][G][T_cap][R_pad*bits/8] (quant.py:156-169 order) with fp32
+ * scales / zero points [B][G][T_cap]; converter warps unpack the codes into
+ * the bf16 MMA operand as code - z (exact for |z| <= 128, else one bf16
+ * rounding) and the epilogue multiplies by the scale (quant.py:106-107).
+ * uw must use palu_query_absorb layout 2 (int4) / 3 (int2) / 1 (others).
  */
 int palu_rope_score_tc_splits(int s_k, int R_pad);
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
-                       size_t plane_stride, void* stream);
+                       void* stream);
 
 /*
  * Fused RoPE score + softmax + value path (attention.py:433-446, 350-362 up

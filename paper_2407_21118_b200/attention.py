@@ -455,7 +455,7 @@ class _Session:
         c = cache
         for li, L in enumerate(fused.layers):
             K = cache._stores[li][0]
-            ok = (fused.dtype == "bfloat16" and K.bits == FP_BITS and self.dh == 128
+            ok = (fused.dtype == "bfloat16" and K.bits in (FP_BITS, 2, 3, 4, 8) and self.dh == 128
                   and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
             if score_kernel in ("tcgen05", "fused") and not ok:
                 raise ValidationError(f"layer {li}: shape not supported by the tcgen05 score kernel")
@@ -471,7 +471,7 @@ class _Session:
         self.fused_layers = []
         for li, L in enumerate(fused.layers):
             K, V = c._stores[li]
-            ok = (self.tc_layers[li] and V.bits == FP_BITS and L.s_v == L.s_k
+            ok = (self.tc_layers[li] and K.bits == FP_BITS and V.bits == FP_BITS and L.s_v == L.s_k
                   and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512 and V.r_pad % 64 == 0
                   and score_kernel == "fused")
             self.fused_layers.append(ok)
@@ -534,12 +534,14 @@ class _Session:
                       _ptr(x), d, 0, st)
             return
         if self.tc_layers[li]:
+            # UW K order matches the converter's code order for int4 / int2 keys
+            layout = {4: 2, 2: 3}.get(K.bits, 1)
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
-                      _ptr(self.uw_bf), 1, st)
+                      _ptr(self.uw_bf), layout, st)
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
-                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, self.plane, st)
+                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
             if self.value_tc_layers[li]:
                 _lib.call("palu_value_tc", _ptr(V.rows), B, n, L.s_v, V.G, V.r_pad, V.cap,
                           _ptr(self.logits), self.ld_logits, _ptr(self.t_dev), _ptr(L.ranks_v_dev),

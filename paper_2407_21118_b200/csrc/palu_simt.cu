@@ -306,14 +306,23 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
       out[(size_t)kk * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
     }
   } else {
-    // bf16 [B][G][s_k*dh][R_pad]: row n = p*dh + c, c < half -> u_c, else w_{c-half}
+    // bf16 [B][G][s_k*dh][R_pad]: row n = p*dh + c, c < half -> u_c, else w_{c-half}.
+    // layouts 2/3: rank k stored at the K position the tcgen05 converter gives
+    // code k of an int4 / int2 key row (groups of 8 / 16: k < G/2 -> 2k,
+    // else 2k - G + 1), so that the dot product is unchanged
     bf16* out = reinterpret_cast<bf16*>(uw) +
-                (((size_t)b * (n_heads / s_k) + g) * width + (size_t)p * dh) * R_pad + k0;
+                (((size_t)b * (n_heads / s_k) + g) * width + (size_t)p * dh) * R_pad;
+    const int grp = layout == 2 ? 8 : (layout == 3 ? 16 : 0);
     for (int idx = threadIdx.x; idx < half * nk; idx += blockDim.x) {
       const int j = idx / nk, kk = idx - j * nk;
       const float b1 = bs[kk * dh + j], b2 = bs[kk * dh + j + half];
-      out[(size_t)j * R_pad + kk] = __float2bfloat16_rn(scale * (qr[j] * b1 + qr[j + half] * b2));
-      out[(size_t)(j + half) * R_pad + kk] =
+      int pos = k0 + kk;
+      if (grp) {
+        const int i = pos % grp;
+        pos = pos - i + (i < grp / 2 ? 2 * i : 2 * i - grp + 1);
+      }
+      out[(size_t)j * R_pad + pos] = __float2bfloat16_rn(scale * (qr[j] * b1 + qr[j + half] * b2));
+      out[(size_t)(j + half) * R_pad + pos] =
           __float2bfloat16_rn(scale * (qr[j + half] * b1 - qr[j] * b2));
     }
   }
@@ -1183,7 +1192,7 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
   PALU_REQUIRE(head_dim % 2 == 0, "rotary embedding requires an even head_dim");
   PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k,
                n_heads);
-  PALU_REQUIRE(layout == 0 || layout == 1, "palu_query_absorb: layout must be 0 or 1");
+  PALU_REQUIRE(layout >= 0 && layout <= 3, "palu_query_absorb: layout must be 0..3");
   dim3 grid(n_heads, (R_pad + 31) / 32, B);
   const size_t smem = (size_t)33 * head_dim * sizeof(float);
   if (dtype == PALU_DTYPE_BF16)

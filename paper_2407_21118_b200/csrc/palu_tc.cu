@@ -44,6 +44,12 @@ struct Params {
   const int* t_dev;
   float* logits;
   unsigned long long* trace;  // diagnostics only (PALU_FUSED_TRACE): [CTA][TRACE_STRIDE]
+  // quantised keys (bits 2/3/4/8): packed LE codes [B][G][T_cap][code_row_bytes]
+  // (quant.py:156-169 order) and per-token fp32 scale / zero point
+  int bits, code_row_bytes;
+  const uint8_t* codes;
+  const float* scales;
+  const float* zps;
 };
 
 constexpr int TRACE_STRIDE = 512;
@@ -56,6 +62,158 @@ __device__ __forceinline__ unsigned smid_u32() {
   unsigned r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
   return r;
+}
+
+constexpr int CONV_WARPS = 2;    // quantised keys: code -> bf16 converter warps per SM
+constexpr int CODE_BIAS = 128;   // bits <= 4: bf16(128 + c) has bit pattern 0x4300 | c
+
+// Unpack this SM's 128-token tile of packed key codes into the SW128 K-major
+// bf16 H stages (the layout TMA would produce), one k-block per stage, and
+// signal the leader's full barrier.  Lane cl owns rows cl and cl + 64; the
+// next k-block's packed bytes are loaded while the current one is written.
+// The operand holds c - z (quant.py:106-107 without the scale): for bits <= 4
+// bf16(128 + c) is built with the exponent trick and (128 + z) subtracted in
+// bf16x2 (exact when |z| <= 128), else c - z goes through fp32 and one bf16
+// rounding; the epilogue multiplies by s.  quant.py:156-169 bit order (code
+// k at bits [k b, (k + 1) b)).
+template <int BITS>
+__device__ __forceinline__ void convert_tile(const Params& p, uint8_t* s_h, uint64_t* full,
+                                             uint64_t* empty, int bg, int tile, int T_rows,
+                                             int kblocks, int cl, int& kc) {
+  constexpr int NW = BITS;  // 8-byte words per row per 64-code k-block
+  const int lane = threadIdx.x & 31;
+  const uint8_t* rowp[2];
+  bool ok[2];
+  float zr[2];
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int t = tile * TILE_M + cl + 64 * rr;
+    ok[rr] = t < T_rows;
+    const size_t tok = (size_t)bg * p.T_cap + (ok[rr] ? t : 0);
+    rowp[rr] = p.codes + tok * p.code_row_bytes;
+    zr[rr] = ok[rr] ? __ldg(p.zps + tok) : 0.f;
+  }
+  if constexpr (BITS == 2 || BITS == 4) {
+    // fast path: rank order inside each group of 32/BITS codes is permuted
+    // (UW is written with the same permutation by palu_query_absorb layouts
+    // 2/3) so that one 32-bit word yields bf16 pairs (c_k, c_{k+G/2}) with a
+    // shift and a LOP3: 0x43004300 | ((w >> BITS k) & mask)
+    constexpr uint32_t MASK = BITS == 4 ? 0x000F000Fu : 0x00030003u;
+    constexpr int NV = 2 * BITS / 4;  // uint4 loads per row per k-block (32 B int4, 16 B int2)
+    uint4 nx[2][2], cu[2][2];
+    auto load4 = [&](int kb) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int q = 0; q < NV; ++q)
+          nx[rr][q] = ok[rr] ? __ldg(reinterpret_cast<const uint4*>(rowp[rr] + kb * 8 * BITS) + q)
+                             : make_uint4(0u, 0u, 0u, 0u);
+    };
+    load4(0);
+    for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) cu[rr][q] = nx[rr][q];
+      if (kb + 1 < kblocks) load4(kb + 1);
+      const int stage = kc % p.stages;
+      mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
+      uint8_t* sb = s_h + stage * H_STAGE_BYTES;
+#pragma unroll
+      for (int rr = 0; rr < 2 && (p.mode & 16) == 0; ++rr) {
+        const int row = cl + 64 * rr;
+        const uint32_t words[8] = {cu[rr][0].x, cu[rr][0].y, cu[rr][0].z, cu[rr][0].w,
+                                   cu[rr][1].x, cu[rr][1].y, cu[rr][1].z, cu[rr][1].w};
+        // c - z: one bf16x2 subtract of (128 + z) from (128 + c), exact when
+        // |z| <= 128; otherwise through fp32 (one bf16 rounding of c - z)
+        const bool zsmall = fabsf(zr[rr]) <= 128.f;
+        const __nv_bfloat162 zb = __float2bfloat162_rn((float)CODE_BIAS + zr[rr]);
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          // int4: word ch -> pairs k = 0..3; int2: word ch / 2 -> pairs 4 (ch & 1) + 0..3
+          const uint32_t w = BITS == 4 ? words[ch] : words[ch >> 1];
+          const int k0 = BITS == 4 ? 0 : 4 * (ch & 1);
+          uint32_t wv[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t cc = (w >> (BITS * (k0 + e))) & MASK;
+            __nv_bfloat162 v;
+            if (zsmall) {
+              const uint32_t biased = 0x43004300u | cc;
+              v = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&biased), zb);
+            } else {
+              v = __floats2bfloat162_rn((float)(cc & 0xFFFFu) - zr[rr], (float)(cc >> 16) - zr[rr]);
+            }
+            wv[e] = *reinterpret_cast<const uint32_t*>(&v);
+          }
+          const uint32_t dst = smem_u32(sb + row * 128 + ((ch ^ (row & 7)) << 4));
+          asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(wv[0]), "r"(wv[1]),
+                       "r"(wv[2]), "r"(wv[3])
+                       : "memory");
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                         smem_u32(&full[stage]) & PEER_MASK)
+                     : "memory");
+    }
+    return;
+  }
+  unsigned long long nxt[2][NW], cur[2][NW];
+  auto load = [&](int kb) {
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int q = 0; q < NW; ++q)
+        nxt[rr][q] = ok[rr] ? __ldg(reinterpret_cast<const unsigned long long*>(rowp[rr] + kb * 8 * BITS) + q)
+                            : 0ull;
+  };
+  load(0);
+  for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+      for (int q = 0; q < NW; ++q) cur[rr][q] = nxt[rr][q];
+    if (kb + 1 < kblocks) load(kb + 1);
+    const int stage = kc % p.stages;
+    mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
+    uint8_t* sb = s_h + stage * H_STAGE_BYTES;
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int row = cl + 64 * rr;
+#pragma unroll
+      for (int ch = 0; ch < 8; ++ch) {  // 8 codes -> one 16-byte swizzled chunk
+        uint32_t wv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          uint32_t c2[2];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int bit = (ch * 8 + 2 * e + h) * BITS;  // within the k-block
+            const int wd = bit >> 6, sh = bit & 63;
+            unsigned long long v = cur[rr][wd] >> sh;
+            if (sh + BITS > 64 && wd + 1 < NW) v |= cur[rr][wd + 1] << (64 - sh);
+            c2[h] = (uint32_t)v & ((1u << BITS) - 1u);
+          }
+          const __nv_bfloat162 b2 =
+              __floats2bfloat162_rn((float)c2[0] - zr[rr], (float)c2[1] - zr[rr]);
+          wv[e] = *reinterpret_cast<const uint32_t*>(&b2);
+        }
+        const uint32_t dst = smem_u32(sb + row * 128 + ((ch ^ (row & 7)) << 4));
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(wv[0]), "r"(wv[1]),
+                     "r"(wv[2]), "r"(wv[3])
+                     : "memory");
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                       smem_u32(&full[stage]) & PEER_MASK)
+                   : "memory");
+  }
 }
 
 // Work item = (sequence b, key group g, 256-token super-tile) for a CTA pair
@@ -100,7 +258,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     prefetch_map(&map_h);
     prefetch_map(&map_uw);
     for (int s = 0; s < p.stages; ++s) {
-      mbar_init(&full[s], 1);
+      // raw bf16: the leader's expect_tx; quantised: both SMs' converter warps
+      mbar_init(&full[s], p.bits == 16 ? 1 : 2 * CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -156,8 +315,13 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           const int ip = i + p.pf_dist;
           const int bgp = ip / n_super, stp = ip - bgp * n_super;
           const int rowp = bgp * p.T_cap + (2 * stp + (int)rank) * TILE_M;
-          for (int kb = 0; kb < kblocks; ++kb) tma_prefetch_l2(&map_h, kb * KB, rowp);
+          if (p.bits == 16) {
+            for (int kb = 0; kb < kblocks; ++kb) tma_prefetch_l2(&map_h, kb * KB, rowp);
+          } else {
+            tma_prefetch_l2(&map_h, 0, rowp);  // packed code rows (one box per tile)
+          }
         }
+        if (p.bits != 16) continue;  // the converter warps fill the H stages
         for (int kb = 0; kb < kblocks; ++kb, ++kc) {
           const int stage = kc % p.stages;
           mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
@@ -205,6 +369,22 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         kc += kblocks;
       }
     }
+  } else if (warp >= 2 + EPI_WARPS) {
+    // ---------------- quantised keys: converter warps (both SMs) ----------------
+    if (p.bits != 16) {
+      const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // rows cl, cl + 64 of the SM's tile
+      int kc = 0;
+      for (int i = i0; i < i1; ++i) {
+        const int bg = i / n_super, st = i - bg * n_super;
+        const int tile = 2 * st + (int)rank;
+        switch (p.bits) {
+          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+        }
+      }
+    }
   } else {
     // ---------------- epilogue (both SMs): cos/sin-weighted row reduction ----------------
     const int q = warp & 3;          // TMEM lane quarter
@@ -228,6 +408,12 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       const int b = bg / p.G, g = bg - b * p.G;
       const int tile = 2 * st + (int)rank;
       const int bs = it % BASE_RING;
+      // quantised keys: the converter wrote c - z, so logit = s_t x (epilogue sum)
+      float sq = 1.f;
+      if (p.bits != 16) {
+        const int tq = tile * TILE_M + delta;
+        if (tq < T_rows) sq = __ldg(p.scales + (size_t)bg * p.T_cap + tq);
+      }
       mbar_wait(&bfull[bs], (it / BASE_RING) & 1);
       // cos/sin((t0 + delta) th_j) = base (x) offset, for this thread's 32 frequencies
       float2 c2[16], s2[16];
@@ -287,8 +473,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             // D columns 0..127 = head 2h (leader's UW rows), 128..255 = head 2h + 1
             const int head0 = g * p.s_k + 2 * h;
             float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
-            lg[0] = v0;
-            lg[p.ld_logits] = v1;
+            lg[0] = v0 * sq;
+            lg[p.ld_logits] = v1 * sq;
           }
           if (p.trace != nullptr && warp == 2 && lane == 0 && h == halves - 1 && it < TRACE_STRIDE - 8)
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + it] = gtimer();
@@ -458,6 +644,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   const uint32_t tmem = *tslot;
   VIter it(sch, vcta, n_vctas);
   VUnit u;
+  if (warp >= 10) return;  // the score role's converter warps have no value work
 
   if (warp == 8) {
     // ---------------- TMA producer: H_v does not depend on the score role,
@@ -892,6 +1079,24 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+// packed key codes: uint8 rows, one box = the whole row x 128 rows (L2 prefetch only)
+static int make_map_u8(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t rows) {
+  EncodeTiledFn fn = encode_fn();
+  PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  const cuuint64_t dims[2] = {row_bytes, rows};
+  const cuuint64_t strides[1] = {row_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)row_bytes, 128};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box,
+                  estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled (codes) failed (%d)", (int)r);
+    return PALU_ECUDA;
+  }
+  return PALU_OK;
+}
+
 static int make_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows,
                        uint32_t box_cols, uint32_t box_rows) {
   EncodeTiledFn fn = encode_fn();
@@ -940,22 +1145,24 @@ int palu_rope_score_tc_splits(int s_k, int R_pad) {
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
-                       size_t plane_stride, void* stream) {
+                       void* stream) {
   using namespace palu::tc;
-  (void)scales;
-  (void)zps;
-  (void)plane_stride;
-  if (bits != 16) {
-    set_error("palu_rope_score_tc: bits %d not on the tensor-core path yet", bits);
+  if (bits != 16 && bits != 2 && bits != 3 && bits != 4 && bits != 8) {
+    set_error("palu_rope_score_tc: bits %d unsupported", bits);
     return PALU_EUNSUPPORTED;
   }
   if (!palu_rope_score_tc_splits(s_k, R_pad) || G * s_k != n_heads) {
     set_error("palu_rope_score_tc: unsupported shape (R_pad %d, s_k %d)", R_pad, s_k);
     return PALU_EUNSUPPORTED;
   }
+  const int row_bytes = bits == 16 ? R_pad * 2 : R_pad * bits / 8;
   PALU_REQUIRE(((uintptr_t)hk & 15) == 0 && ((uintptr_t)uw & 15) == 0, "tc: unaligned operands");
+  PALU_REQUIRE(bits == 16 || (row_bytes % 16 == 0 && row_bytes <= 256 && scales && zps),
+               "palu_rope_score_tc: quantised rows need 16-byte multiples <= 256 B, scales and "
+               "zero points");
   CUtensorMap map_h, map_uw;
-  int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  int rc = bits == 16 ? make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M)
+                      : make_map_u8(&map_h, hk, row_bytes, (uint64_t)B * G * T_cap);
   if (rc) return rc;
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, TILE_M);
   if (rc) return rc;
@@ -993,6 +1200,12 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.t_dev = t_dev;
   prm.logits = logits;
   prm.trace = nullptr;
+  prm.bits = bits;
+  prm.code_row_bytes = row_bytes;
+  prm.codes = reinterpret_cast<const uint8_t*>(hk);
+  prm.scales = scales;
+  prm.zps = zps;
+  if (bits != 16 && getenv("PALU_TC_PROFILE_MODE")) prm.mode = atoi(getenv("PALU_TC_PROFILE_MODE"));
   rope_score_tc_kernel<<<dim3(sms & ~1), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
   PALU_LAUNCHED();
   return PALU_OK;
@@ -1159,6 +1372,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   prm.t_dev = t_dev;
   prm.logits = logits;
   prm.trace = nullptr;
+  prm.bits = 16;
   if (getenv("PALU_FUSED_TRACE")) {
     if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
     PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));

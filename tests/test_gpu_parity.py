@@ -326,3 +326,28 @@ def test_fused_attend_long_batched(P, batch, context, rk, rv, monkeypatch):
     for name in ("tc_value", "fused"):
         e = rel_err(outs[name], outs["simt_value"])
         assert e < 1e-3, (name, e)
+
+
+@pytest.mark.parametrize("bits", [2, 3, 4, 8, (4, 16), (16, 4)])
+def test_tc_quantized_keys_match_simt(P, bits):
+    """Quantised (packed-code) keys on the tcgen05 score kernel (converter
+    warps + epilogue dequant) against the CUDA-core quantised path on the same
+    cache: logits and the step output."""
+    import torch
+    from paper_2407_21118_b200.attention import _Session
+    from paper_2407_21118_b200.harness import synthetic_engine
+    _, fused, cache = synthetic_engine(layers=1, batch=2, context=3000, extra=8, bits=bits,
+                                       seed=7)
+    x0 = torch.randn(2, 4096, device="cuda") * 0.5
+    out, lg = {}, {}
+    for sk in ("simt", "tcgen05"):
+        s = _Session(fused, cache, score_kernel=sk, use_graph=False)
+        assert s.tc_layers[0] == (sk == "tcgen05")
+        s.x.copy_(x0)
+        s.t_dev.fill_(cache.t)
+        s.launch_step()
+        torch.cuda.synchronize()
+        out[sk] = s.x.double().cpu().numpy()
+        lg[sk] = s.logits[0, :, :, :cache.t + 1].double().cpu().numpy()
+    assert rel_err(lg["tcgen05"], lg["simt"]) < 5e-3
+    assert rel_err(out["tcgen05"], out["simt"]) < 5e-3
