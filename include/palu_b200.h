@@ -160,7 +160,10 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
 
 /*
  * Softmax + value on tcgen05 (attention.py:445-446, _value_output :350-362 up
- * to wo_fused) for bf16 latents after palu_rope_score_tc: every SM streams
+ * to wo_fused) after palu_rope_score_tc.  bits 16: bf16 latents; bits
+ * 2/3/4/8: packed codes (Rv_pad % 128 == 0) with fp32 scales / zero points,
+ * unpacked as c - z by converter warps, the scale folded into P (quant.py:
+ * 106-107).  Every SM streams
  * its share of H_v units ([B][G][T_cap][Rv_pad], Rv_pad % 64 == 0, <= 512,
  * s <= 4) as swizzled 2-D TMA boxes and reduces D[128 cols x 16] += H_v^T x
  * P^T with P = hi + lo bf16 probabilities; per-unit partials are merged in a
@@ -168,9 +171,10 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
  * palu_softmax_value.  workspace: palu_rope_attend_workspace() bytes,
  * zero-initialised once (the counters reset themselves).
  */
-int palu_value_tc(const void* hv, int B, int n_heads, int s, int G, int Rv_pad, int T_cap,
-                  const float* logits, int ld_logits, const int* t_dev, const int* ranks_v,
-                  const int* o_off, float* ctx, int ld_ctx, void* workspace, void* stream);
+int palu_value_tc(int bits, const void* hv, const float* scales, const float* zps, int B,
+                  int n_heads, int s, int G, int Rv_pad, int T_cap, const float* logits,
+                  int ld_logits, const int* t_dev, const int* ranks_v, const int* o_off, float* ctx,
+                  int ld_ctx, void* workspace, void* stream);
 
 /* Diagnostics for the fused kernel (not on the product path): with
  * PALU_FUSED_TRACE set, palu_rope_attend_tc records a per-CTA timeline

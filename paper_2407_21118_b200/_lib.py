@@ -41,7 +41,8 @@ SIGNATURES = {
     "palu_rope_attend_workspace": (sz, [i32, i32, i32, i32, i32]),
     "palu_rope_attend_tc": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, p, p, p,
                                   i32, p, i32, p]),
-    "palu_value_tc": (i32, [p, i32, i32, i32, i32, i32, i32, p, i32, p, p, p, p, i32, p, p]),
+    "palu_value_tc": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, i32, p, p, p, p, i32, p,
+                            p]),
     "palu_fused_trace": (i32, [p, sz]),
     "palu_fused_max_clusters": (i32, [i32]),
     "palu_rope_table": (i32, [p, i32, i32, p, p]),

@@ -481,9 +481,14 @@ class _Session:
         for li, L in enumerate(fused.layers):
             K, V = c._stores[li]
             self.value_tc_layers.append(
-                self.tc_layers[li] and not self.fused_layers[li] and V.bits == FP_BITS
+                self.tc_layers[li] and not self.fused_layers[li]
                 and V.r_pad % 64 == 0 and V.r_pad <= 512 and L.s_v <= 4
-                and os.environ.get("PALU_VALUE_KERNEL", "tc") == "tc")
+                # quantised values: the CUDA-core softmax-value kernel is faster than
+                # the converter-fed tcgen05 one on B200; opt in with
+                # PALU_VALUE_KERNEL=tc_quant
+                and ((V.bits == FP_BITS and os.environ.get("PALU_VALUE_KERNEL", "tc") != "simt")
+                     or (V.bits in (2, 3, 4, 8) and V.r_pad % 128 == 0
+                         and os.environ.get("PALU_VALUE_KERNEL") == "tc_quant")))
         self.ws_fused = None
         if any(self.fused_layers) or any(self.value_tc_layers):
             nbytes = max(_lib.call("palu_rope_attend_workspace", self.B, self.n, V.G, V.r_pad, self.cap)
@@ -543,9 +548,10 @@ class _Session:
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
             if self.value_tc_layers[li]:
-                _lib.call("palu_value_tc", _ptr(V.rows), B, n, L.s_v, V.G, V.r_pad, V.cap,
-                          _ptr(self.logits), self.ld_logits, _ptr(self.t_dev), _ptr(L.ranks_v_dev),
-                          _ptr(L.o_off_dev), _ptr(self.ctx), self.ko, _ptr(self.ws_fused), st)
+                _lib.call("palu_value_tc", V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B, n,
+                          L.s_v, V.G, V.r_pad, V.cap, _ptr(self.logits), self.ld_logits,
+                          _ptr(self.t_dev), _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), _ptr(self.ctx),
+                          self.ko, _ptr(self.ws_fused), st)
                 _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
                           _ptr(x), d, 0, st)
                 return

@@ -537,6 +537,12 @@ struct VParams {
   float* ctx_out;
   int ld_ctx;
   int no_wait;  // standalone value kernel: the logits are complete at launch
+  // quantised values (bits 2/3/4/8; 16 = raw bf16 through TMA): packed codes
+  // [B][G][T_cap][code_row_bytes] and per-token fp32 scale / zero point
+  int bits, code_row_bytes;
+  const uint8_t* codes;
+  const float* scales;
+  const float* zps;
 };
 
 constexpr int V_STAGE = 32768;  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
@@ -592,6 +598,125 @@ struct VIter {
   }
 };
 
+// Quantised values: token rows [t0, t0 + 128) (zeros past t1), columns
+// [128 j, 128 j + 128) -> two 64-column MN-major SW128 slabs of c - z.  Lane
+// cl owns rows cl and cl + 64.  int4 / int2 use the 32-bit word trick (pairs
+// (c_k, c_{k + G/2}) per group of 8 / 16 columns, undone on readback).
+struct VStage {  // one converter stage: (unit, 128-token block, column pair)
+  int bg, t0, t1, j;
+};
+template <int BITS>
+struct VCodes {
+  uint4 w[2][BITS];
+  float z[2];
+};
+template <int BITS>
+__device__ __forceinline__ void load_v_codes(const VParams& vp, int T_cap, const VStage& g, int cl,
+                                             VCodes<BITS>& c) {
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int t = g.t0 + cl + 64 * rr;
+    const bool ok = g.bg >= 0 && t < g.t1;
+    const size_t tok = (size_t)(ok ? g.bg : 0) * T_cap + (ok ? t : 0);
+    const uint4* rp = reinterpret_cast<const uint4*>(vp.codes + tok * vp.code_row_bytes +
+                                                     (size_t)g.j * 128 * BITS / 8);
+    c.z[rr] = ok ? __ldg(vp.zps + tok) : 0.f;
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) c.w[rr][q] = ok ? __ldg(rp + q) : make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+template <int BITS>
+__device__ __forceinline__ void convert_v_codes(const VCodes<BITS>& c, int cl, uint8_t* sb) {
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int row = cl + 64 * rr;
+    const float z = c.z[rr];
+    const bool zsmall = fabsf(z) <= 128.f;
+    const __nv_bfloat162 zb = __float2bfloat162_rn((float)CODE_BIAS + z);
+    uint32_t wd[4 * BITS];
+#pragma unroll
+    for (int q = 0; q < BITS; ++q) {
+      wd[4 * q] = c.w[rr][q].x;
+      wd[4 * q + 1] = c.w[rr][q].y;
+      wd[4 * q + 2] = c.w[rr][q].z;
+      wd[4 * q + 3] = c.w[rr][q].w;
+    }
+#pragma unroll
+    for (int ch = 0; ch < 16; ++ch) {  // 16 chunks of 8 columns; slab = ch / 8
+      uint32_t wv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 v;
+        if (BITS == 4 || BITS == 2) {
+          constexpr uint32_t MASK = BITS == 4 ? 0x000F000Fu : 0x00030003u;
+          const uint32_t w = BITS == 4 ? wd[ch] : wd[ch >> 1];
+          const int k0 = BITS == 4 ? 0 : 4 * (ch & 1);
+          const uint32_t cc = (w >> (BITS * (k0 + e))) & MASK;
+          if (zsmall) {
+            const uint32_t biased = 0x43004300u | cc;
+            v = __hsub2(*reinterpret_cast<const __nv_bfloat162*>(&biased), zb);
+          } else {
+            v = __floats2bfloat162_rn((float)(cc & 0xFFFFu) - z, (float)(cc >> 16) - z);
+          }
+        } else {
+          uint32_t c2[2];
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int bit = (ch * 8 + 2 * e + hh) * BITS;
+            const int w0 = bit >> 5, sh = bit & 31;
+            uint32_t x = wd[w0] >> sh;
+            if (sh + BITS > 32 && w0 + 1 < 4 * BITS) x |= wd[w0 + 1] << (32 - sh);
+            c2[hh] = x & ((1u << BITS) - 1u);
+          }
+          v = __floats2bfloat162_rn((float)c2[0] - z, (float)c2[1] - z);
+        }
+        wv[e] = *reinterpret_cast<const uint32_t*>(&v);
+      }
+      const uint32_t dst =
+          smem_u32(sb + (ch >> 3) * (V_STAGE / 2) + row * 128 + (((ch & 7) ^ (row & 7)) << 4));
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(dst), "r"(wv[0]), "r"(wv[1]),
+                   "r"(wv[2]), "r"(wv[3])
+                   : "memory");
+    }
+  }
+}
+
+// Converter warp loop: codes of stage n + 2 are in flight while stage n is
+// written (two register buffers, loop unrolled by two).
+template <int BITS, class Next>
+__device__ __forceinline__ void value_converter(const VParams& vp, int T_cap, Next&& next_stage,
+                                                uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                                int vs, int cl, int lane) {
+  VStage g0, g1, gn;
+  VCodes<BITS> b0, b1;
+  next_stage(g0);
+  next_stage(g1);
+  load_v_codes<BITS>(vp, T_cap, g0, cl, b0);
+  load_v_codes<BITS>(vp, T_cap, g1, cl, b1);
+  int ctr = 0;
+  auto emit = [&](const VCodes<BITS>& b) {
+    const int st = ctr % vs;
+    mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
+    convert_v_codes<BITS>(b, cl, ring + st * V_STAGE);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&full[st]);
+    ++ctr;
+  };
+  while (g0.bg >= 0) {
+    emit(b0);
+    next_stage(gn);
+    g0 = gn;
+    load_v_codes<BITS>(vp, T_cap, g0, cl, b0);
+    if (g1.bg < 0) break;
+    emit(b1);
+    next_stage(gn);
+    g1 = gn;
+    load_v_codes<BITS>(vp, T_cap, g1, cl, b1);
+    if (g0.bg < 0) break;
+  }
+}
+
 __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VParams& vp,
                            uint8_t* smem, int vcta, int n_vctas) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -621,7 +746,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
 
   if (tid == 0) {
     for (int st = 0; st < vs; ++st) {
-      mbar_init(&full[st], 1);
+      mbar_init(&full[st], vp.bits == 16 ? 1 : CONV_WARPS);  // TMA expect_tx | converter warps
       mbar_init(&empty[st], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -644,12 +769,42 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   const uint32_t tmem = *tslot;
   VIter it(sch, vcta, n_vctas);
   VUnit u;
-  if (warp >= 10) return;  // the score role's converter warps have no value work
+  if (warp >= 10) {
+    // ---------------- quantised values: converter warps write c - z of each
+    // stage's 128 tokens x 128 columns into the MN-major SW128 operand (the
+    // layout the TMA boxes would give); columns permuted as for the keys
+    if (vp.bits == 16) return;
+    const int cl = (warp - 10) * 32 + lane;  // token rows cl, cl + 64 of each block
+    // stage cursor over (unit, block, column pair) in the producer's order
+    int blk = 0, jj = 0, nblk = 0, c0 = 0, c1 = 0, bgc = -1;
+    bool more = true;
+    auto next_stage = [&](VStage& g) {
+      if (!more) { g = VStage{-1, 0, 0, 0}; return; }
+      if (bgc < 0 || (jj == 0 && blk == nblk)) {
+        if (!it.next(u)) { more = false; g = VStage{-1, 0, 0, 0}; return; }
+        bgc = u.bg;
+        c0 = u.st0 * SUPER;
+        c1 = min(T_rows, u.st1 * SUPER);
+        nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
+        blk = 0;
+        jj = 0;
+      }
+      g = VStage{bgc, c0 + blk * TILE_M, c1, jj};
+      if (++jj == NJ) { jj = 0; ++blk; }
+    };
+    switch (vp.bits) {
+      case 2: value_converter<2>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
+      case 3: value_converter<3>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
+      case 4: value_converter<4>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
+      default: value_converter<8>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
+    }
+    return;
+  }
 
   if (warp == 8) {
     // ---------------- TMA producer: H_v does not depend on the score role,
     // so it streams every sub-unit back to back, bounded by the ring
-    if (lane == 0) {
+    if (lane == 0 && vp.bits == 16) {
       prefetch_map(&map_v);
       int ctr = 0;
       while (it.next(u)) {
@@ -773,6 +928,18 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
 #pragma unroll
           for (int h = 0; h < V_HP; ++h) x[i][h] = xn[i][h];
         if (s0 + V_SUB < ntok) load(s0 + V_SUB, xn);
+        // quantised values: P carries p s_t (the operand holds c - z)
+        float2 sv[NP];
+#pragma unroll
+        for (int i = 0; i < NP; ++i) {
+          sv[i] = make_float2(1.f, 1.f);
+          const int t = s0 + 2 * ta + 256 * i;
+          if (vp.bits != 16 && t < nt) {
+            const float* sp = vp.scales + (size_t)u.bg * p.T_cap + c0 + t;
+            sv[i].x = __ldg(sp);
+            if (t + 1 < nt) sv[i].y = __ldg(sp + 1);
+          }
+        }
         // (1) max of the sub-block
         float m[V_HP];
 #pragma unroll
@@ -811,10 +978,11 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
             for (int h = 0; h < V_HP; ++h) {
               if (h < s_v) {
                 const float p0 = __expf(x[i][h].x - m[h]), p1 = __expf(x[i][h].y - m[h]);
-                const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
-                const float2 hf = __bfloat1622float2(hi);
-                const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
                 l[h] += p0 + p1;
+                const float q0 = p0 * sv[i].x, q1 = p1 * sv[i].y;
+                const __nv_bfloat162 hi = __floats2bfloat162_rn(q0, q1);
+                const float2 hf = __bfloat1622float2(hi);
+                const __nv_bfloat162 lo = __floats2bfloat162_rn(q0 - hf.x, q1 - hf.y);
                 *reinterpret_cast<__nv_bfloat162*>(pb + rowb + h * 128 + ((((w >> 3) ^ h) & 7) << 4)) = hi;
                 *reinterpret_cast<__nv_bfloat162*>(pb + rowb + (h + 4) * 128 +
                                                    ((((w >> 3) ^ (h + 4)) & 7) << 4)) = lo;
@@ -895,8 +1063,17 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       }
       // the unit's partial: columns of all heads, statistics
 #pragma unroll
+      // TMEM lane m of pair j = column j*128 + m, except int4 / int2 values whose
+      // converter stores rank k of each 8 / 16 group at position k < G/2 ? 2k : 2k-G+1
+      const int m = wb * 32 + lane;
+      const int grp = vp.bits == 4 ? 8 : (vp.bits == 2 ? 16 : 0);
+      int mc = m;
+      if (grp) {
+        const int pp = m % grp;
+        mc = m - pp + ((pp & 1) ? grp / 2 + pp / 2 : pp / 2);
+      }
       for (int j = 0; j < 4; ++j) {
-        const int col = j * 128 + wb * 32 + lane;
+        const int col = j * 128 + mc;
         if (j < NJ && col < vp.Rv_pad) {
 #pragma unroll
           for (int h = 0; h < V_HP; ++h)
@@ -1401,6 +1578,10 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   vp.ctx_out = ctx;
   vp.ld_ctx = ld_ctx;
   vp.no_wait = 0;
+  vp.bits = 16;
+  vp.code_row_bytes = Rv_pad * 2;
+  vp.codes = nullptr;
+  vp.scales = vp.zps = nullptr;
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(rope_attend_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1416,18 +1597,23 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
 
 
 // Standalone tcgen05 softmax + value (the unfused path's second kernel).
-int palu_value_tc(const void* hv, int B, int n_heads, int s, int G, int Rv_pad, int T_cap,
-                  const float* logits, int ld_logits, const int* t_dev, const int* ranks_v,
-                  const int* o_off, float* ctx, int ld_ctx, void* workspace, void* stream) {
+int palu_value_tc(int bits, const void* hv, const float* scales, const float* zps, int B,
+                  int n_heads, int s, int G, int Rv_pad, int T_cap, const float* logits,
+                  int ld_logits, const int* t_dev, const int* ranks_v, const int* o_off, float* ctx,
+                  int ld_ctx, void* workspace, void* stream) {
   using namespace palu::tc;
-  if (G * s != n_heads || Rv_pad % KB != 0 || Rv_pad > 512 || s > V_HP) {
-    set_error("palu_value_tc: unsupported shape (Rv %d, s %d)", Rv_pad, s);
+  if (G * s != n_heads || Rv_pad % KB != 0 || Rv_pad > 512 || s > V_HP ||
+      (bits != 16 && (Rv_pad % 128 != 0 || (bits != 2 && bits != 3 && bits != 4 && bits != 8)))) {
+    set_error("palu_value_tc: unsupported shape (bits %d, Rv %d, s %d)", bits, Rv_pad, s);
     return PALU_EUNSUPPORTED;
   }
   PALU_REQUIRE(((uintptr_t)hv & 15) == 0, "palu_value_tc: unaligned H_v");
-  CUtensorMap map_v;
-  int rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
-  if (rc) return rc;
+  PALU_REQUIRE(bits == 16 || (scales && zps), "palu_value_tc: quantised values need scales/zps");
+  CUtensorMap map_v = {};
+  if (bits == 16) {
+    int rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+    if (rc) return rc;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1475,6 +1661,11 @@ int palu_value_tc(const void* hv, int B, int n_heads, int s, int G, int Rv_pad, 
   vp.ctx_out = ctx;
   vp.ld_ctx = ld_ctx;
   vp.no_wait = 1;
+  vp.bits = bits;
+  vp.code_row_bytes = bits == 16 ? Rv_pad * 2 : Rv_pad * bits / 8;
+  vp.codes = reinterpret_cast<const uint8_t*>(hv);
+  vp.scales = scales;
+  vp.zps = zps;
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(value_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
