@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--rank-k", type=int, default=RANK, help="kept key rank per group (256 = uniform 50%%)")
     ap.add_argument("--rank-v", type=int, default=RANK, help="kept value rank per group (paper preset: 128/384)")
     ap.add_argument("--dtype", default="bfloat16")
+    ap.add_argument("--rope", default="on", choices=["on", "off"],
+                    help="off: palu_decode_step_norope path (attention.py:365-389)")
     ap.add_argument("--score-kernel", default="auto")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-e2e", action="store_true")
@@ -311,7 +313,8 @@ def main():
     weights, fused, cache = synthetic_engine(layers=args.layers, batch=args.batch,
                                              context=args.context, extra=extra, bits=args.bits,
                                              dtype=args.dtype, seed=1234 + rank,
-                                             rank_k=args.rank_k, rank_v=args.rank_v)
+                                             rank_k=args.rank_k, rank_v=args.rank_v,
+                                             rope=args.rope == "on")
     sess = _session(fused, cache, score_kernel=args.score_kernel)
     sess.x.copy_(torch.randn(args.batch, D, device="cuda") * 0.5)
     torch.cuda.synchronize()
@@ -347,16 +350,17 @@ def main():
     # --- e2e through the public API with host buffers --------------------
     e2e = None
     if not args.no_e2e:
+        step_fn = P.palu_decode_step_rope if args.rope == "on" else P.palu_decode_step_norope
         xh = np.random.default_rng(rank).standard_normal((args.batch, D)) * 0.5
         x_in = xh[0] if args.batch == 1 else xh
         for _ in range(2):
-            P.palu_decode_step_rope(weights, fused, cache, x_in)
+            step_fn(weights, fused, cache, x_in)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(K):
-            P.palu_decode_step_rope(weights, fused, cache, x_in)
+            step_fn(weights, fused, cache, x_in)
         torch.cuda.synchronize()
         e2e_ms = (time.perf_counter() - t0) * 1e3 / K
         if world > 1:
@@ -371,7 +375,8 @@ def main():
     hbm, tf_burst, tf_sus, src = _peaks()
     T1 = args.context + W + K + 1  # rows scored in the profiled step (approx.)
     n_groups = NH // GS
-    for score_name in ("palu_rope_attend_tc", "palu_rope_score_tc", "palu_rope_score"):
+    for score_name in ("palu_rope_attend_tc", "palu_rope_score_tc", "palu_rope_score",
+                       "palu_latent_score_tc", "palu_latent_score"):
         if score_name in prof:
             break
     score_ms = statistics.mean(prof[score_name])
@@ -382,8 +387,15 @@ def main():
     sv_name = next((k for k in ("palu_value_tc", "palu_softmax_value") if k in prof), None)
     sv_ms = statistics.mean(prof[sv_name]) if sv_name else 0.0
     latent_total = T1 * n_groups * (args.rank_k + args.rank_v) * 2 * args.batch
-    roofline = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
-                "frac": achieved_tf / tf_sus, "traffic": None, "peak_source": f"{src} sustained bf16",
+    if args.rope == "off":  # no reconstruction: the score kernel streams H_k (HBM-bound)
+        achieved_gbs = lat_bytes / (score_ms * 1e-3) / 1e9
+        roofline_head = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved_gbs / hbm, "traffic": None, "peak_source": f"{src} HBM copy"}
+    else:
+        roofline_head = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
+                         "frac": achieved_tf / tf_sus, "traffic": None,
+                         "peak_source": f"{src} sustained bf16"}
+    roofline = {**roofline_head,
                 "kernel": score_name, "kernel_ms": score_ms,
                 "share_of_step": sum(prof[score_name]) / total_kernel_ms,
                 "score_hbm_gbs": (latent_total if sv_ms == 0.0 else lat_bytes) / (score_ms * 1e-3) / 1e9,
@@ -409,7 +421,8 @@ def main():
             "warmup": W, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16" if args.dtype == "bfloat16" else "f32",
             "data": "synthetic (random-init weights, N(0,1/9) latent cache rows)",
-            "config": {"workload": f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-rope",
+            "config": {"workload": (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
+                                    + ("rope" if args.rope == "on" else "norope")),
                        "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
                        "batch_per_gpu": args.batch, "global_batch": args.batch * world,
                        "layers": args.layers, "bits": args.bits, "parallelism": f"replicas{world}",

@@ -102,7 +102,9 @@ def _head_offsets(ranks, s: int, n_heads: int) -> tuple:
 class LayerFused:
     """attention.py:179-186 plus the device tensors the kernels consume.
 
-    w1   [d + sum r_k + sum r_v, d]  rows: W_q columns, then A_k^T, A_v^T
+    w1   [qdim + sum r_k + sum r_v, d]  rows: W_q columns (rope on, qdim = d) or
+                                       wq_fused columns (rope off, qdim = sum_i r_k(i)),
+                                       then A_k^T, A_v^T
     bk   [G_k, Rk_pad, s_k * d_h]    key up-projections, zero rows past rank
     woT  [d, Ko_pad]                 wo_fused^T (B_v folded into W_o, Eq. 5)
     """
@@ -126,6 +128,8 @@ class LayerFused:
     ranks_v_dev: object = None
     latoff_v_dev: object = None
     o_off_dev: object = None
+    qdim: int = 0           # rows of w1 before the latents (d, or sum_i r_k(i) rope off)
+    q_off_dev: object = None  # rope off: per-head offsets of q_lat inside y
 
 
 @dataclass
@@ -191,7 +195,11 @@ def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=N
         rv_pad = _round_up(max(value_ranks), 128)
         ko = wo_fused.shape[0]
         ko_pad = _round_up(ko, 8)
-        w1 = np.concatenate([wq.T] + [a.T for a in ak] + [a.T for a in av], axis=0)
+        # rope off: the key reconstruction is absorbed into W_q (attention.py:219-220),
+        # so the first rows of w1 produce q_lat directly
+        wq_f = None if config.rope else np.concatenate(q_blocks, axis=1)
+        first = wq.T if config.rope else wq_f.T
+        w1 = np.concatenate([first] + [a.T for a in ak] + [a.T for a in av], axis=0)
         bk_pad = np.zeros((len(bk), rk_pad, s_k * dh))
         for g, b in enumerate(bk):
             bk_pad[g, :b.shape[0]] = b
@@ -201,7 +209,7 @@ def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=N
         lat_k = np.concatenate([[0], np.cumsum(key_ranks)[:-1]]).astype(int)
         lat_v = np.concatenate([[0], np.cumsum(value_ranks)[:-1]]).astype(int)
         layers.append(LayerFused(
-            wq_fused=None if config.rope else np.concatenate(q_blocks, axis=1),
+            wq_fused=wq_f,
             wo_fused=wo_fused,
             q_offsets=_head_offsets(key_ranks, s_k, n),
             o_offsets=_head_offsets(value_ranks, s_v, n),
@@ -213,6 +221,8 @@ def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=N
             ranks_k_dev=i32(key_ranks), latoff_k_dev=i32(lat_k),
             ranks_v_dev=i32(value_ranks), latoff_v_dev=i32(lat_v),
             o_off_dev=i32(_head_offsets(value_ranks, s_v, n)),
+            qdim=d if config.rope else int(_head_offsets(key_ranks, s_k, n)[-1]),
+            q_off_dev=i32(_head_offsets(key_ranks, s_k, n)),
         ))
     theta = theta_table(dh, config.rope_base) if config.rope else np.zeros(max(dh // 2, 1))
     return FusedWeights(layers=tuple(layers), config=config, dtype=dtype,
@@ -400,6 +410,9 @@ class LatentKVCache:
 
 
 def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
+    if fused.config is not None and fused.config.rope != cache.config.rope:
+        raise ValidationError("fused weights were built for rope="
+                              f"{fused.config.rope}, the cache config has rope={cache.config.rope}")
     """attention.py:334-340."""
     if len(fused.layers) != len(cache._stores):
         raise ValidationError("cache and fused weights disagree on layer count")
@@ -425,7 +438,8 @@ class _Session:
         self.B, self.d, self.n, self.dh = cache.batch, cfg.d_model, cfg.n_heads, cfg.head_dim
         dev = cache.device
         self.cap = cache.capacity
-        self.n1 = max(self.d + sum(L.key_ranks) + sum(L.value_ranks) for L in fused.layers)
+        self.rope = cfg.rope
+        self.n1 = max(int(L.w1.shape[0]) for L in fused.layers)
         self.ko = max(L.ko_pad for L in fused.layers)
         rk = max(L.rk_pad for L in fused.layers)
         rv = max(L.rv_pad for L in fused.layers)
@@ -455,9 +469,9 @@ class _Session:
         c = cache
         for li, L in enumerate(fused.layers):
             K = cache._stores[li][0]
-            ok = (fused.dtype == "bfloat16" and K.bits in (FP_BITS, 2, 3, 4, 8) and self.dh == 128
-                  and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
-            if score_kernel in ("tcgen05", "fused") and not ok:
+            ok = (cfg.rope and fused.dtype == "bfloat16" and K.bits in (FP_BITS, 2, 3, 4, 8)
+                  and self.dh == 128 and L.s_k % 2 == 0 and K.r_pad % 64 == 0 and K.r_pad <= 256)
+            if score_kernel in ("tcgen05", "fused") and not ok and cfg.rope:
                 raise ValidationError(f"layer {li}: shape not supported by the tcgen05 score kernel")
             ks = _lib.call("palu_rope_score_tc_splits", L.s_k, K.r_pad) if ok else 0
             ok = ok and 1 <= ks <= 2
@@ -475,13 +489,21 @@ class _Session:
                   and len(L.value_ranks) == len(L.key_ranks) and V.r_pad <= 512 and V.r_pad % 64 == 0
                   and score_kernel == "fused")
             self.fused_layers.append(ok)
+        # rope off: tcgen05 latent-score kernel for bf16 raw keys
+        self.ls_tc_layers = [
+            (not cfg.rope and fused.dtype == "bfloat16" and c._stores[li][0].bits == FP_BITS
+             and L.s_k <= 16 and c._stores[li][0].r_pad % 64 == 0 and c._stores[li][0].r_pad <= 256
+             and score_kernel != "simt")
+            for li, L in enumerate(fused.layers)]
+        if score_kernel == "tcgen05" and not cfg.rope and not all(self.ls_tc_layers):
+            raise ValidationError("shape not supported by the tcgen05 latent-score kernel")
         # tcgen05 softmax + value after the tcgen05 score kernel: bf16 raw V,
         # 64-column-aligned rows, up to 4 heads per value group
         self.value_tc_layers = []
         for li, L in enumerate(fused.layers):
             K, V = c._stores[li]
             self.value_tc_layers.append(
-                self.tc_layers[li] and not self.fused_layers[li]
+                (self.tc_layers[li] or self.ls_tc_layers[li]) and not self.fused_layers[li]
                 and V.r_pad % 64 == 0 and V.r_pad <= 512 and L.s_v <= 4
                 # quantised values: the CUDA-core softmax-value kernel is faster than
                 # the converter-fed tcgen05 one on B200; opt in with
@@ -517,16 +539,30 @@ class _Session:
         B, d, n, dh = self.B, self.d, self.n, self.dh
         code = f.dtype_code
         x, y = self.x, self.y
-        n1 = d + sum(L.key_ranks) + sum(L.value_ranks)
+        n1 = int(L.w1.shape[0])
         sk_sum = sum(L.key_ranks)
+        qd = L.qdim if L.qdim else d
         _lib.call("palu_gemv", code, _ptr(L.w1), n1, d, _ptr(x), B, d, _ptr(y), self.n1, 0, st)
         yp = y.data_ptr()
-        _lib.call("palu_latent_append", code, K.bits, yp + 4 * d, B, self.n1, K.G,
+        _lib.call("palu_latent_append", code, K.bits, yp + 4 * qd, B, self.n1, K.G,
                   _ptr(L.ranks_k_dev), _ptr(L.latoff_k_dev), _ptr(K.rows), _ptr(K.scales),
                   _ptr(K.zps), _ptr(K.scales64), _ptr(K.zps64), K.r_pad, K.cap, _ptr(self.t_dev), st)
-        _lib.call("palu_latent_append", code, V.bits, yp + 4 * (d + sk_sum), B, self.n1, V.G,
+        _lib.call("palu_latent_append", code, V.bits, yp + 4 * (qd + sk_sum), B, self.n1, V.G,
                   _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev), _ptr(V.rows), _ptr(V.scales),
                   _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64), V.r_pad, V.cap, _ptr(self.t_dev), st)
+        if not self.rope:
+            # attention.py:380-388: latent-cache GEMV against q_lat (no reconstruction)
+            if self.ls_tc_layers[li]:
+                _lib.call("palu_latent_score_tc", _ptr(K.rows), B, n, L.s_k, K.G, K.r_pad, K.cap,
+                          yp, self.n1, _ptr(L.q_off_dev), _ptr(L.ranks_k_dev), self.scale,
+                          _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+            else:
+                _lib.call("palu_latent_score", code, K.bits, _ptr(K.rows), _ptr(K.scales),
+                          _ptr(K.zps), B, n, L.s_k, K.G, K.r_pad, K.cap, yp, self.n1,
+                          _ptr(L.q_off_dev), _ptr(L.ranks_k_dev), self.scale, _ptr(self.t_dev),
+                          _ptr(self.logits), self.ld_logits, st)
+            self._value(li, st)
+            return
         if self.fused_layers[li]:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
@@ -547,14 +583,6 @@ class _Session:
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
-            if self.value_tc_layers[li]:
-                _lib.call("palu_value_tc", V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B, n,
-                          L.s_v, V.G, V.r_pad, V.cap, _ptr(self.logits), self.ld_logits,
-                          _ptr(self.t_dev), _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), _ptr(self.ctx),
-                          self.ko, _ptr(self.ws_fused), st)
-                _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
-                          _ptr(x), d, 0, st)
-                return
         else:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
@@ -562,13 +590,27 @@ class _Session:
             _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps),
                       B, n, dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
-        _lib.call("palu_softmax_value", code, V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B,
-                  n, L.s_v, V.G, V.r_pad, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), V.cap,
-                  _ptr(self.logits), self.ld_logits, self.planes[li], self.plane, _ptr(self.t_dev),
-                  self.n_chunks,
-                  _ptr(self.ws), _ptr(self.ctx), self.ko, st)
-        _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko, _ptr(x),
-                  d, 0, st)
+        self._value(li, st)
+
+    def _value(self, li: int, st: int):
+        """Softmax + value path + wo_fused GEMV of layer li (attention.py:445-446, 350-362)."""
+        f, c = self.fused, self.cache
+        L = f.layers[li]
+        K, V = c._stores[li]
+        B, d, n = self.B, self.d, self.n
+        code = f.dtype_code
+        if self.value_tc_layers[li]:
+            _lib.call("palu_value_tc", V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), B, n,
+                      L.s_v, V.G, V.r_pad, V.cap, _ptr(self.logits), self.ld_logits,
+                      _ptr(self.t_dev), _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), _ptr(self.ctx),
+                      self.ko, _ptr(self.ws_fused), st)
+        else:
+            _lib.call("palu_softmax_value", code, V.bits, _ptr(V.rows), _ptr(V.scales), _ptr(V.zps),
+                      B, n, L.s_v, V.G, V.r_pad, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), V.cap,
+                      _ptr(self.logits), self.ld_logits, self.planes[li], self.plane,
+                      _ptr(self.t_dev), self.n_chunks, _ptr(self.ws), _ptr(self.ctx), self.ko, st)
+        _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
+                  _ptr(self.x), d, 0, st)
 
     def launch_step(self):
         """All layers + t += 1 on the current stream (graph-capturable)."""
@@ -676,12 +718,31 @@ def palu_decode_step_rope(weights, fused: FusedWeights, cache: LatentKVCache, x_
     return out[0].copy() if np.asarray(x_t).ndim == 1 else out.copy()
 
 
-def palu_decode_step_norope(weights, fused, cache, x_t) -> np.ndarray:
-    """attention.py:365-389 (rope off).  Not on the accelerated path yet."""
-    if cache.config.rope:
+def palu_decode_step_norope(weights, fused: FusedWeights, cache: LatentKVCache, x_t) -> np.ndarray:
+    """attention.py:365-389 -- one decode step with both fusions active (rope off).
+
+    q_lat_i = x @ wq_fused[:, q_off[i]:] comes out of the first rows of the
+    layer GEMV; the score is a GEMV of the latent key cache against it (tcgen05
+    streaming kernel for bf16 latents, CUDA cores otherwise); softmax, value
+    path and wo_fused as in the rope-on step.  Validation before any mutation.
+    """
+    cfg = cache.config
+    if cfg.rope:
         raise ValidationError("palu_decode_step_norope requires a rope-off config")
-    raise ValidationError("the rope-off fused path is not implemented on the B200 build "
-                          "(SURVEY 8(f)-1, next round)")
+    _check_cache_fused(cache, fused)
+    validate_weights(weights, cfg)
+    x = _validate_x(x_t, cache)
+    torch = _torch()
+    cache.reserve(cache.t + 1)
+    s = _session(fused, cache)
+    s.x_host.copy_(torch.from_numpy(x.reshape(cache.batch, -1).astype(np.float32)))
+    s.x.copy_(s.x_host, non_blocking=True)
+    s.step_device()
+    s.out_host.copy_(s.x, non_blocking=True)
+    torch.cuda.current_stream().synchronize()
+    cache.t += 1
+    out = s.out_host.numpy().astype(np.float64)
+    return out[0].copy() if np.asarray(x_t).ndim == 1 else out.copy()
 
 
 def palu_decode_step_quantized(weights, fused, cache, x_t, tile_len=None) -> np.ndarray:

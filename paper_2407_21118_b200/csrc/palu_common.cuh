@@ -31,6 +31,35 @@ void set_error(const char* fmt, ...);
 
 #define PALU_LAUNCHED() PALU_CK(cudaGetLastError())
 
+// ---- programmatic dependent launch (PDL) -----------------------------------
+// Every kernel of the decode step is launched with programmatic stream
+// serialisation, triggers its dependents at entry and waits for its
+// predecessor (griddepcontrol.wait) before touching any global data: the next
+// kernel's launch and CTA ramp then overlap this kernel's tail.  Every kernel
+// waits, so completion stays transitive along the stream.  PALU_PDL=0 turns
+// the attribute off (griddepcontrol.* are no-ops then).
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 typedef __nv_bfloat16 bf16;
 
 __device__ __forceinline__ float to_f(float v) { return v; }

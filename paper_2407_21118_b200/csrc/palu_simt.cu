@@ -7,10 +7,19 @@
 #include <string.h>
 
 #include "palu_common.cuh"
+#include <stdlib.h>
 
 namespace palu {
 
 static thread_local char g_err[1024] = "";
+
+bool pdl_enabled() {
+  static const int on = [] {
+    const char* e = getenv("PALU_PDL");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on != 0;
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -27,12 +36,13 @@ static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s)
 // lane, x staged in shared memory in K chunks, up to MAXB batch rows per pass.
 // ---------------------------------------------------------------------------
 constexpr int GEMV_WARPS = 8;
-constexpr int GEMV_UNROLL = 8;  // 16-byte weight loads in flight per lane
+constexpr int GEMV_UNROLL_DEF = 8;  // 16-byte weight loads in flight per lane
 
-template <typename T, int MAXB>
+template <typename T, int MAXB, int GEMV_UNROLL>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
 gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, int B, int ldx,
             float* __restrict__ y, int ldy, int accumulate) {
+  pdl_enter();
   using V = Vec16<T>;
   constexpr int VEC = V::N;
   constexpr int STEP = 32 * VEC;
@@ -85,7 +95,13 @@ template <typename T, int MAXB>
 static int launch_gemv(const T* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
                        int acc, cudaStream_t st) {
   dim3 grid((N + GEMV_WARPS - 1) / GEMV_WARPS);
-  gemv_kernel<T, MAXB><<<grid, GEMV_WARPS * 32, 0, st>>>(W, N, K, x, B, ldx, y, ldy, acc);
+  static const int unroll = getenv("PALU_GEMV_UNROLL") ? atoi(getenv("PALU_GEMV_UNROLL")) : GEMV_UNROLL_DEF;
+  if (unroll >= 16)
+    PALU_CK(launch_k(gemv_kernel<T, MAXB, 16>, grid, dim3(GEMV_WARPS * 32), 0, st, W, N, K, x, B,
+                     ldx, y, ldy, acc));
+  else
+    PALU_CK(launch_k(gemv_kernel<T, MAXB, 8>, grid, dim3(GEMV_WARPS * 32), 0, st, W, N, K, x, B,
+                     ldx, y, ldy, acc));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -116,6 +132,7 @@ __global__ void append_raw_kernel(const float* __restrict__ lat, int ld_lat, int
                                   const int* __restrict__ ranks, const int* __restrict__ lat_off,
                                   T* __restrict__ rows, int R_pad, int T_cap,
                                   const int* __restrict__ t_dev) {
+  pdl_enter();
   const int g = blockIdx.x, b = blockIdx.y;
   const int t = *t_dev;
   if (t >= T_cap) return;
@@ -188,6 +205,7 @@ __global__ void append_quant_kernel(const float* __restrict__ lat, int ld_lat, i
                                     float* __restrict__ zps, double* __restrict__ scales64,
                                     int64_t* __restrict__ zps64, int R_pad, int T_cap,
                                     const int* __restrict__ t_dev) {
+  pdl_enter();
   extern __shared__ double qsm[];  // [R_pad] values, 64 reduction slots, then codes
   double* xrow = qsm;
   double* red = qsm + R_pad;
@@ -245,6 +263,7 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
                                     const double* __restrict__ theta, float scale,
                                     const int* __restrict__ t_dev, void* __restrict__ uw,
                                     int layout) {
+  pdl_enter();
   // grid (n_heads, ceil(R_pad / 32), B): one head, 32 rank rows per CTA
   extern __shared__ float qa_sm[];  // qr[dh] then bs[32][dh]
   float* qr = qa_sm;
@@ -357,6 +376,7 @@ rope_score_tiled_kernel(const void* __restrict__ hk, const float* __restrict__ s
                         const float* __restrict__ zps, int n_heads, int s_k, int G, int R_pad,
                         int T_cap, const float* __restrict__ uw, const double* __restrict__ theta,
                         const int* __restrict__ t_dev, float* __restrict__ logits, int ld_logits) {
+  pdl_enter();
   constexpr int DH = 128, HALF = 64, HS = SC_TT + 4;
   extern __shared__ __align__(16) float sc_sm[];
   float (*Hs)[HS] = reinterpret_cast<float (*)[HS]>(sc_sm);                  // [SC_KC][HS]
@@ -441,6 +461,7 @@ __global__ void rope_score_generic_kernel(const void* __restrict__ hk, const flo
                                           const double* __restrict__ theta,
                                           const int* __restrict__ t_dev, float* __restrict__ logits,
                                           int ld_logits) {
+  pdl_enter();
   const int b = blockIdx.z, head = blockIdx.y;
   const int g = head / s_k;
   const int T_rows = *t_dev + 1;
@@ -548,6 +569,44 @@ __device__ void sv_merge_group(const SvPartial& part, size_t head_base, int hp, 
   asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
 }
 
+// ---------------------------------------------------------------------------
+// Rope-off score (attention.py:380-388, both fusions active): the key-side
+// reconstruction is absorbed into wq_fused offline, so per head i of key group
+// g the logits are a latent-cache GEMV
+//   logit[t] = (H_k[g][t] . q_lat_i) / sqrt(d_h),   q_lat_i = x @ wq_fused[:, q_off[i]:]
+// CUDA-core version for every dtype / bit width: one warp per (token, group),
+// lanes over the rank, the group's s heads reduced together.
+template <typename T, int BITS>
+__global__ void __launch_bounds__(256)
+latent_score_kernel(const void* __restrict__ hk, const float* __restrict__ scales,
+                    const float* __restrict__ zps, int n_heads, int s_k, int G, int R_pad,
+                    int T_cap, const float* __restrict__ y, int ld_y, const int* __restrict__ q_off,
+                    const int* __restrict__ ranks, float scale, const int* __restrict__ t_dev,
+                    float* __restrict__ logits, int ld_logits) {
+  pdl_enter();
+  const int g = blockIdx.y, b = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T_rows = *t_dev + 1;
+  const int r = ranks[g];
+  const size_t tok_base = ((size_t)b * G + g) * T_cap;
+  for (int t = blockIdx.x * 8 + warp; t < T_rows; t += gridDim.x * 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int k = lane; k < r; k += 32) {
+      const float h = load_latent<T, BITS>(hk, scales, zps, tok_base + t, R_pad, k);
+#pragma unroll
+      for (int p = 0; p < 8; ++p)
+        if (p < s_k) acc[p] = fmaf(h, y[(size_t)b * ld_y + q_off[g * s_k + p] + k], acc[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      if (p < s_k) {
+        const float v = warp_reduce(acc[p], [](float a, float c) { return a + c; });
+        if (lane == 0) logits[((size_t)b * n_heads + g * s_k + p) * ld_logits + t] = v * scale;
+      }
+    }
+  }
+}
+
 template <typename T, int BITS>
 struct SvSeg {
   static constexpr bool RAW = BITS == 16;
@@ -624,6 +683,7 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
                              int Lr, SvPartial part, const int* __restrict__ ranks_v,
                              const int* __restrict__ o_off, float* __restrict__ ctx_out,
                              int ld_ctx) {
+  pdl_enter();
   using Seg = SvSeg<T, BITS>;
   constexpr int COLV = Seg::COLV;
   extern __shared__ __align__(128) uint8_t sv_raw[];
@@ -892,7 +952,7 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
   if (tid == 0) part.cnt[(size_t)b * G + g] = 0u;  // ready for the next launch
 }
 
-__global__ void advance_kernel(int* t_dev) { *t_dev += 1; }
+__global__ void advance_kernel(int* t_dev) { pdl_enter(); *t_dev += 1; }
 
 // ---------------------------------------------------------------------------
 // Uncompressed baseline K0 (reference_decode, attention.py:133-168)
@@ -1031,15 +1091,15 @@ static void launch_score(const void* hk, const float* scales, const float* zps, 
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       attr_set = true;
     }
-    rope_score_tiled_kernel<T, BITS><<<grid, 256, smem, st>>>(hk, scales, zps, n_heads, s_k, G, R_pad,
+    (void)(launch_k(rope_score_tiled_kernel<T, BITS>, dim3(grid), dim3(256), smem, st, hk, scales, zps, n_heads, s_k, G, R_pad,
                                                            T_cap, uw, theta, t_dev, logits,
-                                                           ld_logits);
+                                                           ld_logits));
   } else {
     const int blocks = (T_cap + 127) / 128;
     dim3 grid(blocks < 64 ? blocks : 64, n_heads, B);
-    rope_score_generic_kernel<T, BITS><<<grid, 128, 0, st>>>(hk, scales, zps, n_heads, head_dim,
+    (void)(launch_k(rope_score_generic_kernel<T, BITS>, dim3(grid), dim3(128), 0, st, hk, scales, zps, n_heads, head_dim,
                                                              s_k, G, R_pad, T_cap, uw, theta,
-                                                             t_dev, logits, ld_logits);
+                                                             t_dev, logits, ld_logits));
   }
 }
 
@@ -1066,9 +1126,9 @@ static int launch_sv_n(const void* hv, const float* scales, const float* zps, in
   dim3 grid(NC, G, B);
   PALU_REQUIRE(sizeof(float) * ((size_t)SV_HP * NC + SV_HP + (size_t)8 * SV_HP * R_pad) <= ring,
                "palu_softmax_value: too many chunks for the merge buffer");
-  softmax_value_partial_kernel<T, BITS, NSEG><<<grid, SV_BLOCK, smem, st>>>(
+  PALU_CK(launch_k(softmax_value_partial_kernel<T, BITS, NSEG>, dim3(grid), dim3(SV_BLOCK), smem, st, 
       hv, scales, zps, n_heads, s_v, G, R_pad, T_cap, logits, ld_logits, n_planes, plane, t_dev, NC,
-      Lr, part, ranks_v, o_off, ctx, ld_ctx);
+      Lr, part, ranks_v, o_off, ctx, ld_ctx));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1141,11 +1201,11 @@ int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat,
   dim3 grid(G, B);
   if (bits == 16) {
     if (dtype == PALU_DTYPE_BF16)
-      append_raw_kernel<bf16><<<grid, 128, 0, S(stream)>>>(lat, ld_lat, G, ranks, lat_off,
-                                                            (bf16*)rows, R_pad, T_cap, t_dev);
+      PALU_CK(launch_k(append_raw_kernel<bf16>, dim3(grid), dim3(128), 0, S(stream), lat, ld_lat, G, ranks, lat_off,
+                                                            (bf16*)rows, R_pad, T_cap, t_dev));
     else
-      append_raw_kernel<float><<<grid, 128, 0, S(stream)>>>(lat, ld_lat, G, ranks, lat_off,
-                                                             (float*)rows, R_pad, T_cap, t_dev);
+      PALU_CK(launch_k(append_raw_kernel<float>, dim3(grid), dim3(128), 0, S(stream), lat, ld_lat, G, ranks, lat_off,
+                                                             (float*)rows, R_pad, T_cap, t_dev));
     PALU_LAUNCHED();
     return PALU_OK;
   }
@@ -1153,9 +1213,9 @@ int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat,
                "bits must be one of (2, 3, 4, 8), got %d", bits);
   PALU_REQUIRE(R_pad % 32 == 0, "quantised rows need R_pad %% 32 == 0 (got %d)", R_pad);
   const size_t smem = (size_t)(R_pad + 64) * sizeof(double) + R_pad;
-  append_quant_kernel<<<grid, 128, smem, S(stream)>>>(lat, ld_lat, G, bits, ranks, lat_off,
+  PALU_CK(launch_k(append_quant_kernel, dim3(grid), dim3(128), smem, S(stream), lat, ld_lat, G, bits, ranks, lat_off,
                                                       (uint8_t*)rows, scales, zps, scales64, zps64,
-                                                      R_pad, T_cap, t_dev);
+                                                      R_pad, T_cap, t_dev));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1196,15 +1256,39 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
   dim3 grid(n_heads, (R_pad + 31) / 32, B);
   const size_t smem = (size_t)33 * head_dim * sizeof(float);
   if (dtype == PALU_DTYPE_BF16)
-    query_absorb_kernel<bf16><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
+    PALU_CK(launch_k(query_absorb_kernel<bf16>, dim3(grid), dim3(256), smem, S(stream), q, ld_q, n_heads, head_dim, s_k,
                                                               (const bf16*)bk, bk_rows, R_pad, theta,
                                                               scale,
-                                                              t_dev, uw, layout);
+                                                              t_dev, uw, layout));
   else
-    query_absorb_kernel<float><<<grid, 256, smem, S(stream)>>>(q, ld_q, n_heads, head_dim, s_k,
+    PALU_CK(launch_k(query_absorb_kernel<float>, dim3(grid), dim3(256), smem, S(stream), q, ld_q, n_heads, head_dim, s_k,
                                                                (const float*)bk, bk_rows, R_pad,
-                                                               theta, scale, t_dev, uw, layout);
+                                                               theta, scale, t_dev, uw, layout));
   PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_latent_score(int dtype, int bits, const void* hk, const float* scales, const float* zps,
+                      int B, int n_heads, int s_k, int G, int R_pad, int T_cap, const float* y,
+                      int ld_y, const int* q_off, const int* ranks, float scale, const int* t_dev,
+                      float* logits, int ld_logits, void* stream) {
+  PALU_REQUIRE(G * s_k == n_heads, "palu_latent_score: G*s_k != n_heads");
+  PALU_REQUIRE(s_k <= 8, "palu_latent_score: at most 8 heads per key group (got %d)", s_k);
+  PALU_REQUIRE(ld_logits >= T_cap, "palu_latent_score: ld_logits < T_cap");
+  dim3 grid((T_cap + 7) / 8 < 512 ? (T_cap + 7) / 8 : 512, G, B);
+  cudaStream_t st = S(stream);
+#define LS(T_, BITS_)                                                                          \
+  PALU_CK(launch_k(latent_score_kernel<T_, BITS_>, grid, dim3(256), 0, st, hk, scales, zps, n_heads, \
+                   s_k, G, R_pad, T_cap, y, ld_y, q_off, ranks, scale, t_dev, logits, ld_logits))
+  if (bits == 16) {
+    if (dtype == PALU_DTYPE_BF16) LS(bf16, 16);
+    else LS(float, 16);
+  } else if (bits == 2) LS(float, 2);
+  else if (bits == 3) LS(float, 3);
+  else if (bits == 4) LS(float, 4);
+  else if (bits == 8) LS(float, 8);
+  else PALU_REQUIRE(false, "bits must be one of (2, 3, 4, 8, 16), got %d", bits);
+#undef LS
   return PALU_OK;
 }
 
@@ -1264,7 +1348,7 @@ int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales,
 }
 
 int palu_advance(int* t_dev, void* stream) {
-  advance_kernel<<<1, 1, 0, S(stream)>>>(t_dev);
+  PALU_CK(launch_k(advance_kernel, dim3(1), dim3(1), 0, S(stream), t_dev));
   PALU_LAUNCHED();
   return PALU_OK;
 }

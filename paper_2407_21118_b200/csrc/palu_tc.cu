@@ -504,6 +504,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -547,6 +548,8 @@ struct VParams {
 
 constexpr int V_STAGE = 32768;  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
 constexpr int V_HP = 4;         // heads per group handled by the value role
+constexpr uint32_t IDESC_LS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);  // K-major A and B, M 128, N 16
 constexpr int V_TMEM_COLS = 128;
 constexpr int V_PF = 0;     // L2 prefetch distance of the value stream (128-token blocks)
 constexpr int V_SUB = 512;  // tokens per P sub-block (double-buffered)
@@ -1104,6 +1107,7 @@ rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                       const __grid_constant__ CUtensorMap map_uw,
                       const __grid_constant__ CUtensorMap map_v, const Params p,
                       const VParams vp) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1130,6 +1134,7 @@ value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
                    int B, const int* __restrict__ t_dev, int score_pairs, int vc,
                    const int* __restrict__ ranks_v, const int* __restrict__ o_off,
                    float* __restrict__ ctx, int ld_ctx) {
+  pdl_enter();
   extern __shared__ float msm[];
   float* w = msm;                                    // [ns]
   int* ulist = reinterpret_cast<int*>(msm + ns);     // [ns]
@@ -1212,6 +1217,7 @@ value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
 // units; no readiness protocol.
 __global__ void __launch_bounds__(THREADS, 1)
 value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const VParams vp) {
+  pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1220,6 +1226,172 @@ value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
   }
   value_role(map_v, p, vp, smem, (int)blockIdx.x, (int)gridDim.x);
+}
+
+// ===========================================================================
+// Rope-off score on tcgen05 (attention.py:380-388): per (sequence, key group)
+//   D[128 tokens x 16] = H_k[tokens x R] (K-major SW128, TMA) x Q^T,
+//   Q[16 x R] = rows h < s: scale * q_lat(head g s + h) (bf16, built in smem)
+// one CTA per SM over a contiguous range of (group, 128-token tile) items; the
+// latent cache streams at HBM rate, the MMA is tiny.  Warps: 0 TMA producer,
+// 1 MMA issuer (+ TMEM owner), 2..5 epilogue / Q builders (warp w reads TMEM
+// lane quarter w % 4).
+// ===========================================================================
+struct LSParams {
+  int B, n_heads, s, G, R_pad, T_cap, ld_logits, ld_y, stages;
+  float scale;
+  const float* y;       // [B][ld_y] fp32, q_lat of head i at q_off[i]
+  const int* q_off;
+  const int* ranks;
+  const int* t_dev;
+  float* logits;
+};
+constexpr int LS_THREADS = 192;
+
+__global__ void __launch_bounds__(LS_THREADS, 1)
+latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams p) {
+  pdl_enter();
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const int kblocks = p.R_pad / KB;
+  const int QB = kblocks * 2048;                      // Q bytes: per k-block 16 rows x 128 B
+  uint8_t* s_h = smem;                                // stages x 16 KB
+  uint8_t* s_q = s_h + p.stages * H_STAGE_BYTES;      // [2] x QB (+1 KB alias slack)
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_q + 2 * QB + 1024);
+  uint64_t* empty = full + p.stages;
+  uint64_t* dfull = empty + p.stages;  // [2] accumulator slot complete
+  uint64_t* dempty = dfull + 2;        // [2] accumulator slot read (4 warps)
+  uint64_t* qfull = dempty + 2;        // [2] Q buffer written
+  uint64_t* qempty = qfull + 2;        // [2] Q buffer's MMAs complete
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(qempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int T_rows = *p.t_dev + 1;
+  const int ntile = (T_rows + TILE_M - 1) / TILE_M;
+  const int total = p.B * p.G * ntile;
+  const int per = (total + gridDim.x - 1) / gridDim.x;
+  const int i0 = min(total, (int)blockIdx.x * per), i1 = min(total, i0 + per);
+  if (threadIdx.x == 0) {
+    prefetch_map(&map_h);
+    for (int st = 0; st < p.stages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&dfull[a], 1);
+      mbar_init(&dempty[a], 4);
+      mbar_init(&qfull[a], 1);
+      mbar_init(&qempty[a], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+        smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  if (warp == 0) {
+    if (lane == 0) {
+      int kc = 0;
+      for (int i = i0; i < i1; ++i) {
+        const int bg = i / ntile, tile = i - bg * ntile;
+        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+          const int st = kc % p.stages;
+          mbar_wait(&empty[st], ((kc / p.stages) & 1) ^ 1);
+          mbar_expect_tx(&full[st], H_STAGE_BYTES);
+          tma_load_2d(&map_h, &full[st], s_h + st * H_STAGE_BYTES, kb * KB,
+                      bg * p.T_cap + tile * TILE_M);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int kc = 0, seg = -1, cur = -1;
+      for (int i = i0; i < i1; ++i) {
+        const int bg = i / ntile;
+        if (bg != cur) {
+          if (seg >= 0) umma_commit(&qempty[seg & 1]);
+          ++seg;
+          cur = bg;
+          mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
+          fence_after();
+        }
+        const int k = i - i0, slot = k & 1;
+        if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
+        fence_after();
+        const uint32_t q0 = smem_u32(s_q + (seg & 1) * QB);
+        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+          const int st = kc % p.stages;
+          mbar_wait(&full[st], (kc / p.stages) & 1);
+          fence_after();
+          const uint32_t a0 = smem_u32(s_h + st * H_STAGE_BYTES);
+#pragma unroll
+          for (int kk = 0; kk < KB / 16; ++kk)
+            umma_bf16_id(tmem + slot * 16, sdesc(a0 + kk * 32), sdesc(q0 + kb * 2048 + kk * 32),
+                         IDESC_LS, (kb | kk) != 0);
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&dfull[slot]);
+      }
+    }
+  } else {
+    // ---------------- epilogue / Q builders (warps 2..5) ----------------
+    const int q4 = warp & 3;  // TMEM lane quarter
+    const int te = threadIdx.x - 64;  // 0..127
+    int seg = -1, cur = -1;
+    for (int i = i0; i < i1; ++i) {
+      const int bg = i / ntile, tile = i - bg * ntile;
+      const int b = bg / p.G, g = bg - b * p.G;
+      if (bg != cur) {
+        ++seg;
+        cur = bg;
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&qempty[buf], ((seg >> 1) - 1) & 1);
+        // Q rows h < s: scale * q_lat (zeros past the group rank); rows >= s are
+        // never read back (their D columns are ignored)
+        uint8_t* qb = s_q + buf * QB;
+        const int r = p.ranks[g];
+        for (int idx = te; idx < p.s * p.R_pad / 2; idx += 128) {
+          const int h = idx / (p.R_pad / 2), k = 2 * (idx - h * (p.R_pad / 2));
+          const float* qv = p.y + (size_t)b * p.ld_y + p.q_off[g * p.s + h];
+          const float v0 = k < r ? qv[k] * p.scale : 0.f, v1 = k + 1 < r ? qv[k + 1] * p.scale : 0.f;
+          const int kb = k / KB, w = k % KB;
+          const uint32_t off = kb * 2048 + (h >> 3) * 1024 + (h & 7) * 128 +
+                               ((((w >> 3) ^ (h & 7)) & 7) << 4) + (w & 7) * 2;
+          *reinterpret_cast<__nv_bfloat162*>(qb + off) = __floats2bfloat162_rn(v0, v1);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar_sync(1, 128);
+        if (te == 0) mbar_arrive(&qfull[buf]);
+      }
+      const int k = i - i0, slot = k & 1;
+      mbar_wait(&dfull[slot], (k >> 1) & 1);
+      fence_after();
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + slot * 16, v);
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty[slot]);
+      const int t = tile * TILE_M + q4 * 32 + lane;
+      if (t < T_rows) {
+#pragma unroll
+        for (int h = 0; h < 16; ++h)
+          if (h < p.s) p.logits[((size_t)b * p.n_heads + g * p.s + h) * p.ld_logits + t] = v[h];
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1383,7 +1555,8 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.scales = scales;
   prm.zps = zps;
   if (bits != 16 && getenv("PALU_TC_PROFILE_MODE")) prm.mode = atoi(getenv("PALU_TC_PROFILE_MODE"));
-  rope_score_tc_kernel<<<dim3(sms & ~1), THREADS, smem, (cudaStream_t)stream>>>(map_h, map_uw, prm);
+  PALU_CK(launch_k(rope_score_tc_kernel, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream, map_h,
+                   map_uw, prm));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1476,9 +1649,9 @@ static int launch_value_merge(const float* pm, const float* pl, const float* pct
     attr = true;
   }
   PALU_REQUIRE(smem <= 100 * 1024, "value merge: too many super-tiles (%d)", ns);
-  value_merge_kernel<<<dim3((Rv_pad + 127) / 128, n_heads, B), 128, smem, st>>>(
-      pm, pl, pctx, ns, Rv_pad, n_heads, s, G, B, t_dev, score_pairs, vc, ranks_v, o_off, ctx,
-      ld_ctx);
+  PALU_CK(launch_k(value_merge_kernel, dim3((Rv_pad + 127) / 128, n_heads, B), dim3(128), smem, st,
+                   pm, pl, pctx, ns, Rv_pad, n_heads, s, G, B, t_dev, score_pairs, vc, ranks_v, o_off,
+                   ctx, ld_ctx));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -1588,8 +1761,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
                                  dyn_limit));
     attr = true;
   }
-  rope_attend_tc_kernel<<<dim3(sms), THREADS, smem_launch, (cudaStream_t)stream>>>(map_h, map_uw,
-                                                                                  map_v, prm, vp);
+  PALU_CK(launch_k(rope_attend_tc_kernel, dim3(sms), dim3(THREADS), smem_launch, (cudaStream_t)stream,
+                   map_h, map_uw, map_v, prm, vp));
   PALU_LAUNCHED();
   return launch_value_merge(pm, pl, pctx, nc_max, Rv_pad, n_heads, s, G, B, t_dev, prm.score_pairs,
                             vc, ranks_v, o_off, ctx, ld_ctx, (cudaStream_t)stream);
@@ -1672,10 +1845,59 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
                                  dyn_limit));
     attr = true;
   }
-  value_tc_kernel<<<dim3(sms), THREADS, dyn_limit, (cudaStream_t)stream>>>(map_v, prm, vp);
+  PALU_CK(launch_k(value_tc_kernel, dim3(sms), dim3(THREADS), (size_t)dyn_limit, (cudaStream_t)stream,
+                   map_v, prm, vp));
   PALU_LAUNCHED();
   return launch_value_merge(pm, pl, pctx, nc_max, Rv_pad, n_heads, s, G, B, t_dev, sms, vc, ranks_v,
                             o_off, ctx, ld_ctx, (cudaStream_t)stream);
+}
+
+
+// Rope-off score on tcgen05 (bf16 latents, s <= 16, R_pad % 64 == 0, <= 256).
+int palu_latent_score_tc(const void* hk, int B, int n_heads, int s, int G, int R_pad, int T_cap,
+                         const float* y, int ld_y, const int* q_off, const int* ranks, float scale,
+                         const int* t_dev, float* logits, int ld_logits, void* stream) {
+  using namespace palu::tc;
+  if (G * s != n_heads || s > 16 || R_pad % KB != 0 || R_pad > 256) {
+    set_error("palu_latent_score_tc: unsupported shape (R_pad %d, s %d)", R_pad, s);
+    return PALU_EUNSUPPORTED;
+  }
+  PALU_REQUIRE(((uintptr_t)hk & 15) == 0, "palu_latent_score_tc: unaligned latents");
+  CUtensorMap map_h;
+  int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+  if (rc) return rc;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  LSParams prm;
+  prm.B = B;
+  prm.n_heads = n_heads;
+  prm.s = s;
+  prm.G = G;
+  prm.R_pad = R_pad;
+  prm.T_cap = T_cap;
+  prm.ld_logits = ld_logits;
+  prm.ld_y = ld_y;
+  prm.scale = scale;
+  prm.y = y;
+  prm.q_off = q_off;
+  prm.ranks = ranks;
+  prm.t_dev = t_dev;
+  prm.logits = logits;
+  const int QB = R_pad / KB * 2048;
+  const int fixed = 1024 + 2 * QB + 1024 + 256;
+  prm.stages = (SMEM_LIMIT - 2048 - fixed) / H_STAGE_BYTES;
+  if (prm.stages > 10) prm.stages = 10;
+  const size_t smem = (size_t)fixed + (size_t)prm.stages * H_STAGE_BYTES;
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(latent_score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    attr = true;
+  }
+  PALU_CK(launch_k(latent_score_tc_kernel, dim3(sms), dim3(LS_THREADS), smem, (cudaStream_t)stream,
+                   map_h, prm));
+  return PALU_OK;
 }
 
 }  // extern "C"

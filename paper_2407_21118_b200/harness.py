@@ -172,7 +172,7 @@ def _shape_only(rows: int, cols: int):
 
 def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=256, layers=32,
                      batch=1, context=65536, extra=64, bits=16, dtype="bfloat16", seed=0,
-                     rope_base=10000.0):
+                     rope_base=10000.0, rope=True):
     """Return (weights, fused, cache) for a Llama-2-7B-shaped Palu model.
 
     Random-init weights of that architecture (uniform, scaled as SURVEY
@@ -201,8 +201,9 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
     fl, wl, dl = [], [], []
     gran = Granularity.group_head(s) if 1 < s < n_heads else (
         Granularity.multi_head() if s == 1 else Granularity.joint_head(n_heads))
+    qdim = d if rope else n_heads * rank_k  # rope off: w1 starts with wq_fused^T
     for li in range(layers):
-        n1 = d + G * (rank_k + rank_v)
+        n1 = qdim + G * (rank_k + rank_v)
         w1 = U(n1, d, scale=1.0 / math.sqrt(d)).to(tdt)
         bk = torch.zeros(G, rk_pad, s * head_dim, device=dev, dtype=tdt)
         bk[:, :rank_k] = U(G, rank_k, s * head_dim, scale=1.0 / math.sqrt(rank_k)).to(tdt)
@@ -215,7 +216,8 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
                              s_k=s, s_v=s, rk_pad=rk_pad, rv_pad=rv_pad, ko_pad=ko_pad, w1=w1, bk=bk,
                              woT=woT, ranks_k_dev=i32(rk), latoff_k_dev=i32(lat_k),
                              ranks_v_dev=i32(rv), latoff_v_dev=i32(lat_v),
-                             o_off_dev=i32(_head_offsets(rv, s, n_heads))))
+                             o_off_dev=i32(_head_offsets(rv, s, n_heads)), qdim=qdim,
+                             q_off_dev=i32(_head_offsets(rk, s, n_heads))))
         sh = _shape_only(d, d)
         wl.append(LayerWeights(sh, sh, sh, sh))
         kg = tuple(GroupFactors(_shape_only(d, rank_k), _shape_only(rank_k, s * head_dim), rank_k)
@@ -224,7 +226,7 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
                    for _ in range(G))
         dl.append(LayerKV(DecomposedLayer(gran, kg, d, head_dim, n_heads),
                           DecomposedLayer(gran, vg, d, head_dim, n_heads)))
-    config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=True, rope_base=rope_base)
+    config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=rope, rope_base=rope_base)
     theta = theta_table(head_dim, rope_base)
     fused = FusedWeights(layers=tuple(fl), config=config, dtype=dtype,
                          theta_dev=torch.from_numpy(theta).to(dev), theta=theta)

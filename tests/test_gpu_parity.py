@@ -98,14 +98,14 @@ def test_random_matrix_gpu_bit_exact(P, golden):
 
 @pytest.mark.parametrize("dtype", ["float32"])
 def test_small_golden_streams(P, golden, dtype):
-    """Every rope-on reference stream (d=16, 1-2 layers, all bit widths,
-    mixed granularities, Hadamard-fused factors) decoded token by token."""
+    """Every reference stream (d=16, 1-2 layers, all bit widths, mixed
+    granularities, Hadamard-fused factors, rope on and off) decoded token by
+    token: rope on through palu_decode_step_rope, rope off through
+    palu_decode_step_norope (wq_fused, latent-score kernel)."""
     g = golden("small_decode.npz")
     for ci, name in enumerate(g["names"]):
         case = small_case(g, ci)
-        if not case["rope"]:
-            continue
-        w, dec, cfg = _to_types(P, case["layers"], case["n"], case["dh"], True, case["base"])
+        w, dec, cfg = _to_types(P, case["layers"], case["n"], case["dh"], case["rope"], case["base"])
         bits = case["bits"] if case["bits"][0] != case["bits"][1] else case["bits"][0]
         got, cache = P.palu_decode(w, dec, cfg, case["tokens"], bits=bits, tile_len=case["tile"],
                                    dtype=dtype)
@@ -357,3 +357,29 @@ def test_tc_quantized_keys_match_simt(P, bits, vk, monkeypatch):
         lg[sk] = s.logits[0, :, :, :cache.t + 1].double().cpu().numpy()
     assert rel_err(lg["tcgen05"], lg["simt"]) < 5e-3
     assert rel_err(out["tcgen05"], out["simt"]) < 5e-3
+
+
+
+@pytest.mark.parametrize("s,bits", [(4, 16), (2, 16), (4, 4), (1, 16)])
+def test_norope_tc_matches_simt(P, s, bits):
+    """Rope-off step: the tcgen05 latent-score kernel (bf16 raw keys) and the
+    CUDA-core one on the same cache; quantised keys use the CUDA-core score."""
+    import torch
+    from paper_2407_21118_b200.attention import _Session
+    from paper_2407_21118_b200.harness import synthetic_engine
+    r = min(256, 64 * s)  # rank <= group width
+    _, fused, cache = synthetic_engine(layers=1, batch=2, context=5000, extra=8, s=s, bits=bits,
+                                       seed=5, rope=False, rank_k=r, rank_v=r)
+    x0 = torch.randn(2, 4096, device="cuda") * 0.5
+    out, lg = {}, {}
+    for sk in ("simt", "auto"):
+        ses = _Session(fused, cache, score_kernel=sk, use_graph=False)
+        assert ses.ls_tc_layers[0] == (sk == "auto" and bits == 16)
+        ses.x.copy_(x0)
+        ses.t_dev.fill_(cache.t)
+        ses.launch_step()
+        torch.cuda.synchronize()
+        out[sk] = ses.x.double().cpu().numpy()
+        lg[sk] = ses.logits[0, :, :, :cache.t + 1].double().cpu().numpy()
+    assert rel_err(lg["auto"], lg["simt"]) < 5e-3
+    assert rel_err(out["auto"], out["simt"]) < 5e-3
