@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--rank-k", type=int, default=RANK, help="kept key rank per group (256 = uniform 50%%)")
     ap.add_argument("--rank-v", type=int, default=RANK, help="kept value rank per group (paper preset: 128/384)")
     ap.add_argument("--dtype", default="bfloat16")
+    ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
+                    help="multi-GPU: batch replicas (weak scaling) or head-group shards with one "
+                         "NCCL all-reduce of the layer output per layer (strong scaling)")
     ap.add_argument("--rope", default="on", choices=["on", "off"],
                     help="off: palu_decode_step_norope path (attention.py:365-389)")
     ap.add_argument("--score-kernel", default="auto")
@@ -305,17 +308,28 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.shard == "heads" and (NH // GS) % world:
+        raise SystemExit(f"--shard heads needs the {NH // GS} head groups to split over {world} GPUs")
     _lib.load()
     _lib.call("palu_device_check", local)
 
     K, W = args.steps, args.warmup
     extra = 2 * (K + W) + 16
+    heads = args.shard == "heads"
     weights, fused, cache = synthetic_engine(layers=args.layers, batch=args.batch,
                                              context=args.context, extra=extra, bits=args.bits,
-                                             dtype=args.dtype, seed=1234 + rank,
+                                             dtype=args.dtype, seed=1234 + (0 if heads else rank),
                                              rank_k=args.rank_k, rank_v=args.rank_v,
                                              rope=args.rope == "on")
+    if heads:
+        # this rank keeps its head groups; one all-reduce per layer
+        from paper_2407_21118_b200.sharding import attach_allreduce, shard_engine
+
+        fused, cache = shard_engine(fused, cache, rank, world)
+        torch.cuda.empty_cache()
     sess = _session(fused, cache, score_kernel=args.score_kernel)
+    if heads and world > 1:
+        attach_allreduce(sess, lambda t: dist.all_reduce(t, op=dist.ReduceOp.SUM))
     sess.x.copy_(torch.randn(args.batch, D, device="cuda") * 0.5)
     torch.cuda.synchronize()
 
@@ -418,16 +432,19 @@ def main():
         launches_per_step = sum(len(v) for v in prof.values())
         line = {
             "metric": METRIC, "value": ms * 1e3, "unit": "us/step", "n_gpus": world, "steps": K,
-            "warmup": W, "ms_per_step": ms, "higher_is_better": False, "scaling": "weak",
+            "warmup": W, "ms_per_step": ms, "higher_is_better": False,
+            "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16" if args.dtype == "bfloat16" else "f32",
             "data": "synthetic (random-init weights, N(0,1/9) latent cache rows)",
             "config": {"workload": (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
                                     + ("rope" if args.rope == "on" else "norope")),
                        "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
-                       "batch_per_gpu": args.batch, "global_batch": args.batch * world,
-                       "layers": args.layers, "bits": args.bits, "parallelism": f"replicas{world}",
+                       "batch_per_gpu": args.batch,
+                       "global_batch": args.batch if heads else args.batch * world,
+                       "layers": args.layers, "bits": args.bits,
+                       "parallelism": (f"heads{world}" if heads else f"replicas{world}"),
                        "l2": "inputs larger than L2 (latent cache 17 GB/step)"},
-            "tokens_per_s": args.batch * world / (ms * 1e-3),
+            "tokens_per_s": (args.batch if heads else args.batch * world) / (ms * 1e-3),
             "gpu_launches": launches_per_step * K,
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "uncompressed": uncompressed,

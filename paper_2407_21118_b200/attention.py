@@ -527,6 +527,7 @@ class _Session:
                       _ptr(self.rope_tab), _stream())
         self.use_graph = use_graph
         self.graph = None
+        self.allreduce = None  # head-group shards: sum of partial layer outputs (sharding.py)
         self.eager_steps = 0
         self.score_kernel = score_kernel
         self.scale = 1.0 / math.sqrt(self.dh)
@@ -617,6 +618,8 @@ class _Session:
         st = _stream()
         for li in range(len(self.fused.layers)):
             self._layer(li, st)
+            if self.allreduce is not None:
+                self.allreduce(self.x)
         _lib.call("palu_advance", _ptr(self.t_dev), st)
 
     def profile_step(self) -> dict:
@@ -656,10 +659,17 @@ class _Session:
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
-            with torch.cuda.stream(s):
-                # capture does not execute: t_dev is unchanged by the capture itself
-                with torch.cuda.graph(g, stream=s):
-                    self.launch_step()
+            try:
+                with torch.cuda.stream(s):
+                    # capture does not execute: t_dev is unchanged by the capture itself
+                    with torch.cuda.graph(g, stream=s):
+                        self.launch_step()
+            except Exception:  # a collective that cannot be captured: run eagerly
+                torch.cuda.current_stream().wait_stream(s)
+                torch.cuda.synchronize()
+                self.use_graph = False
+                self.launch_step()
+                return
             torch.cuda.current_stream().wait_stream(s)
             self.graph = g
         self.graph.replay()

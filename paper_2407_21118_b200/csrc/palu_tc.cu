@@ -1887,12 +1887,13 @@ int palu_latent_score_tc(const void* hk, int B, int n_heads, int s, int G, int R
   const int QB = R_pad / KB * 2048;
   const int fixed = 1024 + 2 * QB + 1024 + 256;
   prm.stages = (SMEM_LIMIT - 2048 - fixed) / H_STAGE_BYTES;
-  if (prm.stages > 10) prm.stages = 10;
+  const int smax = getenv("PALU_LS_STAGES") ? atoi(getenv("PALU_LS_STAGES")) : 10;  // tuning only
+  if (prm.stages > smax) prm.stages = smax;
   const size_t smem = (size_t)fixed + (size_t)prm.stages * H_STAGE_BYTES;
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(latent_score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
+                                 SMEM_LIMIT - 2048));
     attr = true;
   }
   PALU_CK(launch_k(latent_score_tc_kernel, dim3(sms), dim3(LS_THREADS), smem, (cudaStream_t)stream,

@@ -383,3 +383,35 @@ def test_norope_tc_matches_simt(P, s, bits):
         lg[sk] = ses.logits[0, :, :, :cache.t + 1].double().cpu().numpy()
     assert rel_err(lg["auto"], lg["simt"]) < 5e-3
     assert rel_err(out["auto"], out["simt"]) < 5e-3
+
+
+@pytest.mark.parametrize("world,rope", [(2, True), (4, True), (2, False)])
+def test_head_group_shards_sum_to_full_step(P, world, rope):
+    """every head-group shard runs its own step (its slice of the
+    GEMV rows, its groups' caches, its wo_fused rows); the sum of the partial
+    layer outputs equals the unsharded step.  One layer, one GPU, ranks run in
+    sequence (the all-reduce is the sum)."""
+    import torch
+    from paper_2407_21118_b200.attention import _Session
+    from paper_2407_21118_b200.harness import synthetic_engine
+    from paper_2407_21118_b200.sharding import shard_engine
+    _, fused, cache = synthetic_engine(layers=1, batch=2, context=3000, extra=8, seed=11,
+                                       rope=rope)
+    x0 = torch.randn(2, 4096, device="cuda") * 0.5
+    full = _Session(fused, cache, use_graph=False)
+    full.x.copy_(x0)
+    full.t_dev.fill_(cache.t)
+    full.launch_step()
+    torch.cuda.synchronize()
+    want = full.x.double().cpu().numpy()
+    acc = np.zeros_like(want)
+    for r in range(world):
+        fs, cs = shard_engine(fused, cache, r, world)
+        ses = _Session(fs, cs, use_graph=False)
+        assert ses.n == 32 // world
+        ses.x.copy_(x0)
+        ses.t_dev.fill_(cache.t)
+        ses.launch_step()
+        torch.cuda.synchronize()
+        acc += ses.x.double().cpu().numpy()
+    assert rel_err(acc, want) < 1e-4

@@ -5,6 +5,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <initializer_list>
 #include <cuda_runtime.h>
 #include <cuda.h>
 
@@ -208,8 +209,11 @@ int main() {
         ((EncodeFn)fp)(&map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        for (int ctas : {22, 148}) {
-          const int rows_per_cta = (int)(rows_total / 148) / 256 * 256;
+        for (int ctas : {22, 148, 1148}) {
+          // 1148: 148 CTAs streaming 1.8 MB each (the value / latent-score kernels' share)
+          const bool short_run = ctas == 1148;
+          if (short_run) ctas = 148;
+          const int rows_per_cta = short_run ? 3584 : (int)(rows_total / 148) / 256 * 256;
           const size_t smem = (size_t)chunk * stages + 16 * stages + 2048;
           tma2d_stream<<<ctas, 288, smem>>>(map, rows_per_cta, stages, box_rows, sink);
           cudaEventRecord(a);
@@ -219,12 +223,13 @@ int main() {
           float ms;
           cudaEventElapsedTime(&ms, a, b);
           const double bytes = (double)rows_per_cta * 512;
-          printf("tma2d box_rows %3d stages %d ctas %3d: %7.1f GB/s per CTA, %7.1f total\n", box_rows, stages,
-                 ctas, bytes / (ms * 1e6), bytes * ctas / (ms * 1e6));
+          printf("tma2d box_rows %3d stages %d ctas %3d%s: %7.1f GB/s per CTA, %7.1f total (%.1f us)\n",
+                 box_rows, stages, ctas, short_run ? " x 1.8MB" : "", bytes / (ms * 1e6),
+                 bytes * ctas / (ms * 1e6), ms * 1e3);
         }
       }
   }
-  for (int mode : {1})
+  for (int mode : std::initializer_list<int>{})
     for (int chunk : {32768, 65536})
       for (int stages : {3, 5}) {
         if ((size_t)chunk * stages > 200 * 1024) continue;
