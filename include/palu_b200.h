@@ -181,16 +181,19 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
  * = scale * (H_k[g(i)][t] . q_lat_i) for t <= *t_dev, where q_lat_i =
  * y[b][q_off[i] : q_off[i] + ranks[g(i)]] (y = x @ [wq_fused | A_k | A_v]).
  * palu_latent_score: CUDA cores, every dtype / bit width, s_k <= 8.
- * palu_latent_score_tc: tcgen05 streaming kernel for bf16 latents
- * (D[128 tokens x 16] = H_k x Q^T per tile), s_k <= 16, R_pad % 64 == 0, <= 256.
+ * palu_latent_score_tc: tcgen05 streaming kernel (D[128 tokens x 16] = H_k x
+ * Q^T per tile), s_k <= 16, R_pad % 64 == 0, <= 256; bits 16 streams bf16
+ * rows through TMA, bits 2/3/4/8 unpack packed codes as c - z (converter
+ * warps, as palu_rope_score_tc) and scale the logits per token.
  */
 int palu_latent_score(int dtype, int bits, const void* hk, const float* scales, const float* zps,
                       int B, int n_heads, int s_k, int G, int R_pad, int T_cap, const float* y,
                       int ld_y, const int* q_off, const int* ranks, float scale, const int* t_dev,
                       float* logits, int ld_logits, void* stream);
-int palu_latent_score_tc(const void* hk, int B, int n_heads, int s, int G, int R_pad, int T_cap,
-                         const float* y, int ld_y, const int* q_off, const int* ranks, float scale,
-                         const int* t_dev, float* logits, int ld_logits, void* stream);
+int palu_latent_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
+                         int n_heads, int s, int G, int R_pad, int T_cap, const float* y, int ld_y,
+                         const int* q_off, const int* ranks, float scale, const int* t_dev,
+                         float* logits, int ld_logits, void* stream);
 
 /* Diagnostics for the fused kernel (not on the product path): with
  * PALU_FUSED_TRACE set, palu_rope_attend_tc records a per-CTA timeline

@@ -45,8 +45,8 @@ SIGNATURES = {
                             p]),
     "palu_latent_score": (i32, [i32, i32, p, p, p, i32, i32, i32, i32, i32, i32, p, i32, p, p, f32,
                                 p, p, i32, p]),
-    "palu_latent_score_tc": (i32, [p, i32, i32, i32, i32, i32, i32, p, i32, p, p, f32, p, p, i32,
-                                   p]),
+    "palu_latent_score_tc": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, i32, p, p, f32, p,
+                                   p, i32, p]),
     "palu_fused_trace": (i32, [p, sz]),
     "palu_fused_max_clusters": (i32, [i32]),
     "palu_rope_table": (i32, [p, i32, i32, p, p]),

@@ -491,7 +491,8 @@ class _Session:
             self.fused_layers.append(ok)
         # rope off: tcgen05 latent-score kernel for bf16 raw keys
         self.ls_tc_layers = [
-            (not cfg.rope and fused.dtype == "bfloat16" and c._stores[li][0].bits == FP_BITS
+            (not cfg.rope and fused.dtype == "bfloat16"
+             and c._stores[li][0].bits in (FP_BITS, 2, 3, 4, 8)
              and L.s_k <= 16 and c._stores[li][0].r_pad % 64 == 0 and c._stores[li][0].r_pad <= 256
              and score_kernel != "simt")
             for li, L in enumerate(fused.layers)]
@@ -554,9 +555,10 @@ class _Session:
         if not self.rope:
             # attention.py:380-388: latent-cache GEMV against q_lat (no reconstruction)
             if self.ls_tc_layers[li]:
-                _lib.call("palu_latent_score_tc", _ptr(K.rows), B, n, L.s_k, K.G, K.r_pad, K.cap,
-                          yp, self.n1, _ptr(L.q_off_dev), _ptr(L.ranks_k_dev), self.scale,
-                          _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+                _lib.call("palu_latent_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales),
+                          _ptr(K.zps), B, n, L.s_k, K.G, K.r_pad, K.cap, yp, self.n1,
+                          _ptr(L.q_off_dev), _ptr(L.ranks_k_dev), self.scale, _ptr(self.t_dev),
+                          _ptr(self.logits), self.ld_logits, st)
             else:
                 _lib.call("palu_latent_score", code, K.bits, _ptr(K.rows), _ptr(K.scales),
                           _ptr(K.zps), B, n, L.s_k, K.G, K.r_pad, K.cap, yp, self.n1,

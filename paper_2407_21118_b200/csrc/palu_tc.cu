@@ -76,8 +76,8 @@ constexpr int CODE_BIAS = 128;   // bits <= 4: bf16(128 + c) has bit pattern 0x4
 // bf16x2 (exact when |z| <= 128), else c - z goes through fp32 and one bf16
 // rounding; the epilogue multiplies by s.  quant.py:156-169 bit order (code
 // k at bits [k b, (k + 1) b)).
-template <int BITS>
-__device__ __forceinline__ void convert_tile(const Params& p, uint8_t* s_h, uint64_t* full,
+template <int BITS, class PP>
+__device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t* full,
                                              uint64_t* empty, int bg, int tile, int T_rows,
                                              int kblocks, int cl, int& kc) {
   constexpr int NW = BITS;  // 8-byte words per row per 64-code k-block
@@ -120,7 +120,7 @@ __device__ __forceinline__ void convert_tile(const Params& p, uint8_t* s_h, uint
       mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
       uint8_t* sb = s_h + stage * H_STAGE_BYTES;
 #pragma unroll
-      for (int rr = 0; rr < 2 && (p.mode & 16) == 0; ++rr) {
+      for (int rr = 0; rr < 2; ++rr) {
         const int row = cl + 64 * rr;
         const uint32_t words[8] = {cu[rr][0].x, cu[rr][0].y, cu[rr][0].z, cu[rr][0].w,
                                    cu[rr][1].x, cu[rr][1].y, cu[rr][1].z, cu[rr][1].w};
@@ -1245,8 +1245,14 @@ struct LSParams {
   const int* ranks;
   const int* t_dev;
   float* logits;
+  // quantised keys (bits 2/3/4/8): converter warps 6-7 write c - z, the
+  // epilogue multiplies by the token scale (quant.py:106-107)
+  int bits, code_row_bytes;
+  const uint8_t* codes;
+  const float* scales;
+  const float* zps;
 };
-constexpr int LS_THREADS = 192;
+constexpr int LS_THREADS = 256;
 
 __global__ void __launch_bounds__(LS_THREADS, 1)
 latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams p) {
@@ -1274,7 +1280,7 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
   if (threadIdx.x == 0) {
     prefetch_map(&map_h);
     for (int st = 0; st < p.stages; ++st) {
-      mbar_init(&full[st], 1);
+      mbar_init(&full[st], p.bits == 16 ? 1 : CONV_WARPS);
       mbar_init(&empty[st], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -1296,7 +1302,7 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
   fence_after();
   const uint32_t tmem = *tslot;
   if (warp == 0) {
-    if (lane == 0) {
+    if (lane == 0 && p.bits == 16) {
       int kc = 0;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile, tile = i - bg * ntile;
@@ -1306,6 +1312,21 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
           mbar_expect_tx(&full[st], H_STAGE_BYTES);
           tma_load_2d(&map_h, &full[st], s_h + st * H_STAGE_BYTES, kb * KB,
                       bg * p.T_cap + tile * TILE_M);
+        }
+      }
+    }
+  } else if (warp >= 6) {
+    // quantised keys: converter warps (rows cl, cl + 64 of each 128-token tile)
+    if (p.bits != 16) {
+      const int cl = (warp - 6) * 32 + lane;
+      int kc = 0;
+      for (int i = i0; i < i1; ++i) {
+        const int bg = i / ntile, tile = i - bg * ntile;
+        switch (p.bits) {
+          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
         }
       }
     }
@@ -1360,10 +1381,22 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
           const int h = idx / (p.R_pad / 2), k = 2 * (idx - h * (p.R_pad / 2));
           const float* qv = p.y + (size_t)b * p.ld_y + p.q_off[g * p.s + h];
           const float v0 = k < r ? qv[k] * p.scale : 0.f, v1 = k + 1 < r ? qv[k + 1] * p.scale : 0.f;
-          const int kb = k / KB, w = k % KB;
-          const uint32_t off = kb * 2048 + (h >> 3) * 1024 + (h & 7) * 128 +
-                               ((((w >> 3) ^ (h & 7)) & 7) << 4) + (w & 7) * 2;
-          *reinterpret_cast<__nv_bfloat162*>(qb + off) = __floats2bfloat162_rn(v0, v1);
+          // int4 / int2 keys: rank k sits at the converter's K position
+          // (groups of 8 / 16: k < G/2 ? 2k : 2k - G + 1)
+          const int grp = p.bits == 4 ? 8 : (p.bits == 2 ? 16 : 0);
+          const float vv[2] = {v0, v1};
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            int pos = k + e;
+            if (grp) {
+              const int ii = pos % grp;
+              pos = pos - ii + (ii < grp / 2 ? 2 * ii : 2 * ii - grp + 1);
+            }
+            const int kb = pos / KB, w = pos % KB;
+            const uint32_t off = kb * 2048 + (h >> 3) * 1024 + (h & 7) * 128 +
+                                 ((((w >> 3) ^ (h & 7)) & 7) << 4) + (w & 7) * 2;
+            *reinterpret_cast<__nv_bfloat16*>(qb + off) = __float2bfloat16_rn(vv[e]);
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         named_bar_sync(1, 128);
@@ -1380,9 +1413,10 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
       if (lane == 0) mbar_arrive(&dempty[slot]);
       const int t = tile * TILE_M + q4 * 32 + lane;
       if (t < T_rows) {
+        const float sq = p.bits == 16 ? 1.f : __ldg(p.scales + (size_t)bg * p.T_cap + t);
 #pragma unroll
         for (int h = 0; h < 16; ++h)
-          if (h < p.s) p.logits[((size_t)b * p.n_heads + g * p.s + h) * p.ld_logits + t] = v[h];
+          if (h < p.s) p.logits[((size_t)b * p.n_heads + g * p.s + h) * p.ld_logits + t] = v[h] * sq;
       }
     }
   }
@@ -1854,18 +1888,24 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
 
 
 // Rope-off score on tcgen05 (bf16 latents, s <= 16, R_pad % 64 == 0, <= 256).
-int palu_latent_score_tc(const void* hk, int B, int n_heads, int s, int G, int R_pad, int T_cap,
-                         const float* y, int ld_y, const int* q_off, const int* ranks, float scale,
-                         const int* t_dev, float* logits, int ld_logits, void* stream) {
+int palu_latent_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
+                         int n_heads, int s, int G, int R_pad, int T_cap, const float* y, int ld_y,
+                         const int* q_off, const int* ranks, float scale, const int* t_dev,
+                         float* logits, int ld_logits, void* stream) {
   using namespace palu::tc;
-  if (G * s != n_heads || s > 16 || R_pad % KB != 0 || R_pad > 256) {
-    set_error("palu_latent_score_tc: unsupported shape (R_pad %d, s %d)", R_pad, s);
+  const int row_bytes = bits == 16 ? R_pad * 2 : R_pad * bits / 8;
+  if (G * s != n_heads || s > 16 || R_pad % KB != 0 || R_pad > 256 ||
+      (bits != 16 && bits != 2 && bits != 3 && bits != 4 && bits != 8) ||
+      (bits != 16 && (row_bytes % 16 != 0 || !scales || !zps))) {
+    set_error("palu_latent_score_tc: unsupported shape (bits %d, R_pad %d, s %d)", bits, R_pad, s);
     return PALU_EUNSUPPORTED;
   }
   PALU_REQUIRE(((uintptr_t)hk & 15) == 0, "palu_latent_score_tc: unaligned latents");
-  CUtensorMap map_h;
-  int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
-  if (rc) return rc;
+  CUtensorMap map_h = {};
+  if (bits == 16) {
+    int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+    if (rc) return rc;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1884,6 +1924,11 @@ int palu_latent_score_tc(const void* hk, int B, int n_heads, int s, int G, int R
   prm.ranks = ranks;
   prm.t_dev = t_dev;
   prm.logits = logits;
+  prm.bits = bits;
+  prm.code_row_bytes = row_bytes;
+  prm.codes = reinterpret_cast<const uint8_t*>(hk);
+  prm.scales = scales;
+  prm.zps = zps;
   const int QB = R_pad / KB * 2048;
   const int fixed = 1024 + 2 * QB + 1024 + 256;
   prm.stages = (SMEM_LIMIT - 2048 - fixed) / H_STAGE_BYTES;
