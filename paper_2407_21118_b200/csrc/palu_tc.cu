@@ -349,6 +349,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           const int slot = unit & 1;
           if ((p.mode & 4) == 0) mbar_wait(&tempty[slot], ((unit >> 1) & 1) ^ 1);
           fence_after();
+          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 4 * unit] = gtimer();
           const uint32_t d_tmem = tmem_base + slot * N_CTA;
           for (int kb = 0; kb < kblocks; ++kb) {
             const int cnt = kc + kb;
@@ -365,6 +367,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             if (h == halves - 1) umma2_commit_both(&empty[stage]);
           }
           umma2_commit_both(&tfull[slot]);
+          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = gtimer();
         }
         kc += kblocks;
       }
@@ -434,6 +438,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         const int slot = unit & 1;
         mbar_wait(&tfull[slot], (unit >> 1) & 1);
         fence_after();
+        const bool tr = p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 &&
+                        4 * unit + 7 < TRACE_STRIDE;
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + 4 * unit] = gtimer();
         float v[2] = {0.f, 0.f};
         if ((p.mode & 1) == 0)
 #pragma unroll
@@ -454,6 +461,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           }
           v[hp] = acc2.x + acc2.y;
         }
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + 4 * unit] = gtimer();
         float* r = red + slot * 2 * TILE_M;
         if (jh == 1) {
           r[delta] = v[0];
@@ -476,7 +484,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             lg[0] = v0 * sq;
             lg[p.ld_logits] = v1 * sq;
           }
-          if (p.trace != nullptr && warp == 2 && lane == 0 && h == halves - 1 && it < TRACE_STRIDE - 8)
+          if (p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == halves - 1 &&
+              it < TRACE_STRIDE - 8)
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + it] = gtimer();
           if (p.ready != nullptr && h == halves - 1) {
             // publish this warp's logits of the item to the value role
@@ -1525,6 +1534,9 @@ int palu_rope_score_tc_splits(int s_k, int R_pad) {
   return ((s_k == 2 || s_k == 4) && R_pad % KB == 0 && R_pad <= 256) ? 1 : 0;
 }
 
+static unsigned long long* g_trace = nullptr;  // diagnostics (PALU_FUSED_TRACE)
+static int g_trace_ctas = 0;
+
 int palu_rope_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
@@ -1589,6 +1601,12 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.scales = scales;
   prm.zps = zps;
   if (bits != 16 && getenv("PALU_TC_PROFILE_MODE")) prm.mode = atoi(getenv("PALU_TC_PROFILE_MODE"));
+  if (getenv("PALU_SCORE_TRACE")) {  // diagnostics: per-head-pair timeline (tools/score_trace.py)
+    if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
+    PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));
+    prm.trace = g_trace;
+    g_trace_ctas = sms & ~1;
+  }
   PALU_CK(launch_k(rope_score_tc_kernel, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream, map_h,
                    map_uw, prm));
   PALU_LAUNCHED();
@@ -1596,8 +1614,6 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
 }
 
 // ---- fused score + softmax + value ------------------------------------------
-static unsigned long long* g_trace = nullptr;  // diagnostics (PALU_FUSED_TRACE)
-static int g_trace_ctas = 0;
 
 // Copies the last traced fused launch's timeline ([CTA][TRACE_STRIDE] u64:
 // start, end, smid, role/count, events...) to host; returns the CTA count.

@@ -1,0 +1,165 @@
+// tcgen05 throughput probe (diagnostics, not product): back-to-back
+// kind::f16 MMAs on resident smem operands, one CTA (or CTA pair) per SM,
+// all SMs busy; reports ns per MMA and TFLOP/s for several shapes.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2407_21118_b200/csrc \
+//        -I include -o tools/mma_probe tools/mma_probe.cu
+#include <cstdio>
+#include <cstdint>
+
+#include "palu_sm100.cuh"
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+using namespace palu::tc;
+
+template <int M, int N, int CG>
+__global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int extra,
+                                                    const __grid_constant__ CUtensorMap map) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 96 * 1024);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
+  const int warp = threadIdx.x >> 5;
+  uint32_t rank = 0;
+  if (CG == 2) rank = cluster_rank();
+  if (threadIdx.x == 0) {
+    *reinterpret_cast<int*>(slot + 4) = 0;
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    mbar_init(&bar[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    if (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (CG == 2) cluster_sync();
+  fence_after();
+  const uint32_t tmem = *slot;
+  constexpr uint32_t ID = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
+                          ((uint32_t)(M >> 4) << 24);
+  if (threadIdx.x == 0 && (CG == 1 || rank == 0)) {
+    const uint32_t a0 = smem_u32(sm), b = smem_u32(sm + 32 * 1024);
+    for (int i = 0; i < iters; ++i) {
+      if (extra & 4) {  // a commit per 4 MMAs (the score kernel's per-k-block stage release)
+        if (CG == 1) umma_commit(&bar[2]); else umma2_commit_both(&bar[2]);
+      }
+      if ((extra & 8) && (i & 3) == 0) {  // different A stage per k-block (16 KB apart)
+      }
+      const uint32_t a = (extra & 8) ? a0 + (uint32_t)((i & 1) * 16384) : a0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (CG == 1)
+          umma_bf16_id(tmem, sdesc(a + kk * 32), sdesc(b + kk * 32), ID, 1);
+        else
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(sdesc(a + kk * 32)), "l"(sdesc(b + kk * 32)), "r"(ID), "r"(1)
+              : "memory");
+      }
+    }
+    if (CG == 1)
+      umma_commit(&bar[0]);
+    else
+      umma2_commit_both(&bar[0]);
+  }
+  volatile int* stop = reinterpret_cast<volatile int*>(slot + 4);
+  if (threadIdx.x == 0) { mbar_wait(&bar[0], 0); *stop = 1; }
+  if (warp == 1 && (extra & 1) && lane_id() == 0) {
+    // continuous 16 KB TMA tile loads into a 64 KB ring (no consumer)
+    uint64_t* tb = bar + 1;
+    for (int i = 0; *stop == 0 && i < 1000000; ++i) {
+      mbar_expect_tx(tb, 16384);
+      tma_load_2d(&map, tb, sm + 64 * 1024 - 16384 * 0 + 0 * (i & 3), 0, (blockIdx.x * 64 + (i % 64)) * 128 % 65536);
+      mbar_wait(tb, i & 1);
+    }
+  }
+  if ((warp == 2 || warp == 3) && (extra & 2)) {
+    float v[16];
+    for (int i = 0; *stop == 0 && i < 1000000; ++i) {
+      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (i & 7) * 16, v);
+      tmem_wait_ld();
+      if (v[0] == 12345.f) sink[1] = v[1];
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (CG == 2) cluster_sync();
+  if (warp == 0) {
+    fence_after();
+    if (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  if (iters < 0) sink[0] = 1.f;
+}
+
+typedef CUresult (*EncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static CUtensorMap g_map;
+static int g_extra = 0;
+
+template <int M, int N, int CG>
+void run(const char* name) {
+  auto k = mma_probe<M, N, CG>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(148);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = 100 * 1024;
+  cudaLaunchAttribute attr;
+  attr.id = cudaLaunchAttributeClusterDimension;
+  attr.val.clusterDim.x = CG;
+  attr.val.clusterDim.y = 1;
+  attr.val.clusterDim.z = 1;
+  cfg.attrs = &attr;
+  cfg.numAttrs = 1;
+  float* sink;
+  cudaMalloc(&sink, 64);
+  const int iters = 4000;
+  cudaLaunchKernelEx(&cfg, k, iters, sink, g_extra, g_map);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  cudaLaunchKernelEx(&cfg, k, iters, sink, g_extra, g_map);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms;
+  cudaEventElapsedTime(&ms, a, b);
+  const double mmas = (double)iters * 4;  // per issuing CTA
+  const int issuers = 148 / CG;
+  const double flops = 2.0 * M * N * 16 * mmas * issuers;
+  printf("extra %d %-24s %7.2f ns/MMA  %7.1f TFLOP/s  (%s)\n", g_extra, name, ms * 1e6 / mmas, flops / (ms * 1e-3) / 1e12,
+         cudaGetErrorString(cudaGetLastError()));
+}
+
+int main() {
+  void* buf;
+  cudaMalloc(&buf, (size_t)256 << 20);
+  void* fp = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
+  const cuuint64_t dims[2] = {64, 1u << 20};
+  const cuuint64_t strides[1] = {128};
+  const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
+  ((EncodeFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  for (int e : {0, 4, 8, 12}) {
+    g_extra = e;
+    run<256, 256, 2>("cta2 M256 N256 K16");
+    run<128, 256, 1>("cta1 M128 N256 K16");
+  }
+  return 0;
+}

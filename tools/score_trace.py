@@ -1,0 +1,76 @@
+"""Diagnostics: per-head-pair timeline of the tcgen05 score kernel.
+
+    PALU_SCORE_TRACE=1 python tools/score_trace.py [--rank-k 256]
+
+For leader CTAs: MMA start (after the TMEM slot is free), MMA issue end
+(commit), epilogue wake (tfull) and slot release, per head-pair unit.
+"""
+import argparse
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("PALU_SCORE_TRACE", "1")
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--context", type=int, default=65536)
+    ap.add_argument("--rank-k", type=int, default=256)
+    ap.add_argument("--rank-v", type=int, default=256)
+    a = ap.parse_args()
+    import torch
+
+    from paper_2407_21118_b200 import _lib
+    from paper_2407_21118_b200.attention import _session
+    from paper_2407_21118_b200.harness import synthetic_engine
+
+    _lib.load()
+    w, f, c = synthetic_engine(layers=1, batch=1, context=a.context, extra=64, rank_k=a.rank_k,
+                               rank_v=a.rank_v)
+    s = _session(f, c, score_kernel="tcgen05")
+    s.x.normal_(0, 0.5)
+    for _ in range(3):
+        s.launch_step()
+    torch.cuda.synchronize()
+    prof = s.profile_step()  # the value kernel must not trace: PALU_FUSED_TRACE unset
+    print({k: [round(x * 1e3, 1) for x in v] for k, v in prof.items()}, "us")
+    buf = np.zeros((1024, 512), dtype=np.uint64)
+    n = _lib.call("palu_fused_trace", buf.ctypes.data_as(C.c_void_p), 1024)
+    tr = buf[:n].astype(np.int64)
+    t0 = tr[:, 0][tr[:, 0] > 0].min() if (tr[:, 0] > 0).any() else tr[tr > 0].min()
+    rows = []
+    for cta in range(0, n, 2):  # leaders
+        u = 0
+        while 4 + 4 * u + 3 < 512 and tr[cta, 4 + 4 * u] > 0:
+            ms, me, ew, er = tr[cta, 4 + 4 * u:8 + 4 * u]
+            rows.append((cta, u, ms, me, ew, er))
+            u += 1
+    r = np.array(rows, dtype=np.int64)
+    if not len(r):
+        print("no trace")
+        return
+    mma_issue = (r[:, 3] - r[:, 2]) / 1e3
+    epi_lat = (r[:, 4] - r[:, 3]) / 1e3     # commit -> epilogue wake (MMA execution + signal)
+    epi_dur = (r[:, 5] - r[:, 4]) / 1e3     # epilogue work on the slot
+    gaps = []
+    for cta in np.unique(r[:, 0]):
+        rr = r[r[:, 0] == cta]
+        gaps += list((rr[1:, 2] - rr[:-1, 3]) / 1e3)  # MMA idle between units (waiting slot/data)
+    pct = lambda x: np.percentile(x, [10, 50, 90]).round(3)
+    print(f"units {len(r)}: MMA issue span us p10/50/90 {pct(mma_issue)}")
+    print(f"  commit->epilogue wake {pct(epi_lat)}; epilogue on slot {pct(epi_dur)}")
+    print(f"  MMA idle between units {pct(np.array(gaps))}")
+    cta = r[0, 0]
+    rr = r[r[:, 0] == cta][:8]
+    for x in rr:
+        print("  unit", x[1], "mma", round((x[2] - t0) / 1e3, 2), "->", round((x[3] - t0) / 1e3, 2),
+              "epi", round((x[4] - t0) / 1e3, 2), "->", round((x[5] - t0) / 1e3, 2))
+
+
+if __name__ == "__main__":
+    main()
