@@ -367,7 +367,9 @@ class LatentKVCache:
         self.batch = batch
         self.t = 0
         self.device = device or torch.device("cuda", torch.cuda.current_device())
-        cap = max(int(capacity or 256), 8)
+        # whole 128-token tiles: every per-tile copy of the kernels (TMA boxes,
+        # zero-point blocks) stays inside its own sequence/group rows
+        cap = _round_up(max(int(capacity or 256), 8), 128)
         self.capacity = cap
         self._stores = []
         for kv in self.decomposed:

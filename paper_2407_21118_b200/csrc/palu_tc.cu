@@ -553,9 +553,11 @@ struct VParams {
   const uint8_t* codes;
   const float* scales;
   const float* zps;
+  int raw_slots;  // standalone kernel, packed V: TMA ring of packed code tiles (+ zero points)
 };
 
-constexpr int V_STAGE = 32768;  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
+constexpr int V_STAGE = 32768;
+constexpr int V_RAW_BYTES = 65536;  // packed-code ring (tiles of 128 tokens x 128 codes)  // 128 tokens x 128 columns; 2 TMA boxes of 16 KB
 constexpr int V_HP = 4;         // heads per group handled by the value role
 constexpr uint32_t IDESC_LS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) |
                               ((uint32_t)(128 >> 4) << 24);  // K-major A and B, M 128, N 16
@@ -617,17 +619,17 @@ struct VIter {
 struct VStage {  // one converter stage: (unit, 128-token block, column pair)
   int bg, t0, t1, j;
 };
-template <int BITS>
+template <int BITS, int RPL>  // RPL: token rows per converter lane (128 / converter lanes)
 struct VCodes {
-  uint4 w[2][BITS];
-  float z[2];
+  uint4 w[RPL][BITS];
+  float z[RPL];
 };
-template <int BITS>
+template <int BITS, int RPL>
 __device__ __forceinline__ void load_v_codes(const VParams& vp, int T_cap, const VStage& g, int cl,
-                                             VCodes<BITS>& c) {
+                                             VCodes<BITS, RPL>& c) {
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int t = g.t0 + cl + 64 * rr;
+  for (int rr = 0; rr < RPL; ++rr) {
+    const int t = g.t0 + cl + (128 / RPL) * rr;
     const bool ok = g.bg >= 0 && t < g.t1;
     const size_t tok = (size_t)(ok ? g.bg : 0) * T_cap + (ok ? t : 0);
     const uint4* rp = reinterpret_cast<const uint4*>(vp.codes + tok * vp.code_row_bytes +
@@ -637,11 +639,12 @@ __device__ __forceinline__ void load_v_codes(const VParams& vp, int T_cap, const
     for (int q = 0; q < BITS; ++q) c.w[rr][q] = ok ? __ldg(rp + q) : make_uint4(0u, 0u, 0u, 0u);
   }
 }
-template <int BITS>
-__device__ __forceinline__ void convert_v_codes(const VCodes<BITS>& c, int cl, uint8_t* sb) {
+template <int BITS, int RPL>
+__device__ __forceinline__ void convert_v_codes(const VCodes<BITS, RPL>& c, int cl, uint8_t* sb,
+                                                int slab = -1) {
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int row = cl + 64 * rr;
+  for (int rr = 0; rr < RPL; ++rr) {
+    const int row = cl + (128 / RPL) * rr;
     const float z = c.z[rr];
     const bool zsmall = fabsf(z) <= 128.f;
     const __nv_bfloat162 zb = __float2bfloat162_rn((float)CODE_BIAS + z);
@@ -655,6 +658,7 @@ __device__ __forceinline__ void convert_v_codes(const VCodes<BITS>& c, int cl, u
     }
 #pragma unroll
     for (int ch = 0; ch < 16; ++ch) {  // 16 chunks of 8 columns; slab = ch / 8
+      if (slab >= 0 && (ch >> 3) != slab) continue;
       uint32_t wv[4];
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -693,23 +697,100 @@ __device__ __forceinline__ void convert_v_codes(const VCodes<BITS>& c, int cl, u
   }
 }
 
+// Stage cursor over (unit, 128-token block, column pair) in the value
+// pipeline's order; the TMA producer and the converter warps each walk a copy.
+struct VStageIter {
+  VIter it;
+  int T_rows, NJ;
+  int blk = 0, jj = 0, nblk = 0, c0 = 0, c1 = 0, bgc = -1;
+  bool more = true;
+  __device__ VStageIter(const VIter& i, int tr, int nj) : it(i), T_rows(tr), NJ(nj) {}
+  __device__ __forceinline__ bool next(VStage& g) {
+    if (!more) return false;
+    if (bgc < 0 || (jj == 0 && blk == nblk)) {
+      VUnit u;
+      if (!it.next(u)) {
+        more = false;
+        return false;
+      }
+      bgc = u.bg;
+      c0 = u.st0 * SUPER;
+      c1 = min(T_rows, u.st1 * SUPER);
+      nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
+      blk = 0;
+      jj = 0;
+    }
+    g = VStage{bgc, c0 + blk * TILE_M, c1, jj};
+    if (++jj == NJ) {
+      jj = 0;
+      ++blk;
+    }
+    return true;
+  }
+};
+
+// Packed V through the TMA ring (standalone value kernel): converter lane cl
+// owns token row cl of each block; the packed bytes and zero point come from
+// shared memory, so the loads run up to V_RAW_BYTES ahead of the conversion.
+template <int BITS>
+__device__ __forceinline__ void value_converter_ring(VStageIter sit, uint8_t* raw, int nslots,
+                                                     uint64_t* rfull, uint64_t* rempty,
+                                                     uint8_t* ring, uint64_t* full, uint64_t* empty,
+                                                     int vs, int cl, int lane,
+                                                     unsigned long long* trace) {
+  constexpr int RB = TILE_M * 16 * BITS;  // packed bytes of one stage's tile
+  // 8 converter warps: lane pair (2 row, 2 row + 1) of converter lane cl owns the
+  // two 64-column slabs of token row cl / 2; 4 warps: one lane per row, both slabs
+  const int nconv_lanes = (int)(blockDim.x >> 5) * 32 - 320;
+  const int split = nconv_lanes / TILE_M;  // 1 or 2
+  const int row = cl / split, slab = split == 2 ? (cl & 1) : -1;
+  VStage g;
+  int k = 0;
+  const bool tr = trace != nullptr && cl == 0;
+  while (sit.next(g)) {
+    const int rs = k % nslots, st = k % vs;
+    if (tr && 3 * k + 302 < TRACE_STRIDE) trace[300 + 3 * k] = gtimer();
+    mbar_wait(&rfull[rs], (k / nslots) & 1);
+    if (tr && 3 * k + 302 < TRACE_STRIDE) trace[301 + 3 * k] = gtimer();
+    const uint8_t* slot = raw + rs * (RB + TILE_M * 4);
+    VCodes<BITS, 1> c;
+    const uint32_t a = smem_u32(slot + row * 16 * BITS);
+#pragma unroll
+    for (int q = 0; q < BITS; ++q)
+      c.w[0][q] = (slab < 0 || (q >= slab * BITS / 2 && q < (slab + 1) * BITS / 2 + (BITS & 1)))
+                      ? lds128(a + 16 * q)
+                      : make_uint4(0u, 0u, 0u, 0u);
+    c.z[0] = reinterpret_cast<const float*>(slot + RB)[row];
+    mbar_wait(&empty[st], ((k / vs) & 1) ^ 1);
+    if (tr && 3 * k + 302 < TRACE_STRIDE) trace[302 + 3 * k] = gtimer();
+    convert_v_codes<BITS, 1>(c, row, ring + st * V_STAGE, slab);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&full[st]);
+      mbar_arrive(&rempty[rs]);
+    }
+    ++k;
+  }
+}
+
 // Converter warp loop: codes of stage n + 2 are in flight while stage n is
 // written (two register buffers, loop unrolled by two).
-template <int BITS, class Next>
+template <int BITS, int RPL, class Next>
 __device__ __forceinline__ void value_converter(const VParams& vp, int T_cap, Next&& next_stage,
                                                 uint8_t* ring, uint64_t* full, uint64_t* empty,
                                                 int vs, int cl, int lane) {
   VStage g0, g1, gn;
-  VCodes<BITS> b0, b1;
+  VCodes<BITS, RPL> b0, b1;
   next_stage(g0);
   next_stage(g1);
-  load_v_codes<BITS>(vp, T_cap, g0, cl, b0);
-  load_v_codes<BITS>(vp, T_cap, g1, cl, b1);
+  load_v_codes<BITS, RPL>(vp, T_cap, g0, cl, b0);
+  load_v_codes<BITS, RPL>(vp, T_cap, g1, cl, b1);
   int ctr = 0;
-  auto emit = [&](const VCodes<BITS>& b) {
+  auto emit = [&](const VCodes<BITS, RPL>& b) {
     const int st = ctr % vs;
     mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
-    convert_v_codes<BITS>(b, cl, ring + st * V_STAGE);
+    convert_v_codes<BITS, RPL>(b, cl, ring + st * V_STAGE);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[st]);
@@ -719,12 +800,12 @@ __device__ __forceinline__ void value_converter(const VParams& vp, int T_cap, Ne
     emit(b0);
     next_stage(gn);
     g0 = gn;
-    load_v_codes<BITS>(vp, T_cap, g0, cl, b0);
+    load_v_codes<BITS, RPL>(vp, T_cap, g0, cl, b0);
     if (g1.bg < 0) break;
     emit(b1);
     next_stage(gn);
     g1 = gn;
-    load_v_codes<BITS>(vp, T_cap, g1, cl, b1);
+    load_v_codes<BITS, RPL>(vp, T_cap, g1, cl, b1);
     if (g0.bg < 0) break;
   }
 }
@@ -754,17 +835,28 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   uint64_t* dfull = pfull + 2;    // [2] sub-block accumulator complete (P consumed)
   uint64_t* dempty = dfull + 2;   // [2] sub-block accumulator read back
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  // packed V, standalone kernel: TMA ring of code tiles (+ 128 zero points each)
+  const int nslots = vp.raw_slots;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(tslot + 4);  // [nslots]
+  uint64_t* rempty = rfull + nslots;                         // [nslots]
+  uint8_t* raw = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(rempty + nslots) + 127) & ~uintptr_t(127));
   __shared__ float red_m[4][V_HP], red_l[4][V_HP];
 
   if (tid == 0) {
     for (int st = 0; st < vs; ++st) {
-      mbar_init(&full[st], vp.bits == 16 ? 1 : CONV_WARPS);  // TMA expect_tx | converter warps
+      // TMA expect_tx | one arrive per converter warp
+      mbar_init(&full[st], vp.bits == 16 ? 1 : (int)(blockDim.x >> 5) - 10);
       mbar_init(&empty[st], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&pfull[a], 1);
       mbar_init(&dfull[a], 1);
       mbar_init(&dempty[a], 1);
+    }
+    for (int a = 0; a < nslots; ++a) {
+      mbar_init(&rfull[a], 1);
+      mbar_init(&rempty[a], (int)(blockDim.x >> 5) - 10);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -786,7 +878,8 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     // stage's 128 tokens x 128 columns into the MN-major SW128 operand (the
     // layout the TMA boxes would give); columns permuted as for the keys
     if (vp.bits == 16) return;
-    const int cl = (warp - 10) * 32 + lane;  // token rows cl, cl + 64 of each block
+    const int nconv = (int)(blockDim.x >> 5) - 10;  // 2 (fused kernel) or 8 (packed-V value kernel)
+    const int cl = (warp - 10) * 32 + lane;  // token rows cl (+ 64) of each block
     // stage cursor over (unit, block, column pair) in the producer's order
     int blk = 0, jj = 0, nblk = 0, c0 = 0, c1 = 0, bgc = -1;
     bool more = true;
@@ -804,15 +897,60 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       g = VStage{bgc, c0 + blk * TILE_M, c1, jj};
       if (++jj == NJ) { jj = 0; ++blk; }
     };
-    switch (vp.bits) {
-      case 2: value_converter<2>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
-      case 3: value_converter<3>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
-      case 4: value_converter<4>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
-      default: value_converter<8>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane); break;
+#define VCONV(B_, R_) value_converter<B_, R_>(vp, p.T_cap, next_stage, ring, full, empty, vs, cl, lane)
+#define VRING(B_) value_converter_ring<B_>(VStageIter(it, T_rows, NJ), raw, nslots, rfull, rempty, ring, \
+                                           full, empty, vs, cl, lane,                                  \
+                                           p.trace ? p.trace + (size_t)blockIdx.x * TRACE_STRIDE : nullptr)
+    if (nslots > 0 && (nconv == 4 || nconv == 8)) {
+      switch (vp.bits) {
+        case 2: VRING(2); break;
+        case 3: VRING(3); break;
+        case 4: VRING(4); break;
+        default: VRING(8); break;
+      }
+    } else if (nconv >= 4) {
+      switch (vp.bits) {
+        case 2: VCONV(2, 1); break;
+        case 3: VCONV(3, 1); break;
+        case 4: VCONV(4, 1); break;
+        default: VCONV(8, 1); break;
+      }
+    } else {
+      switch (vp.bits) {
+        case 2: VCONV(2, 2); break;
+        case 3: VCONV(3, 2); break;
+        case 4: VCONV(4, 2); break;
+        default: VCONV(8, 2); break;
+      }
     }
+#undef VCONV
+#undef VRING
     return;
   }
 
+  if (warp == 8 && vp.bits != 16 && nslots > 0) {
+    // ---------------- TMA producer, packed V: code tiles {16 bits bytes, 128
+    // rows} and the tile's 128 zero points into the raw ring
+    if (lane == 0) {
+      prefetch_map(&map_v);
+      const int RB = TILE_M * 16 * vp.bits;
+      VStageIter sit(it, T_rows, NJ);
+      VStage g;
+      int k = 0;
+      while (sit.next(g)) {
+        const int rs = k % nslots;
+        mbar_wait(&rempty[rs], ((k / nslots) & 1) ^ 1);
+        mbar_expect_tx(&rfull[rs], RB + TILE_M * 4);
+        uint8_t* slot = raw + rs * (RB + TILE_M * 4);
+        tma_load_2d(&map_v, &rfull[rs], slot, g.j * 16 * vp.bits, g.bg * p.T_cap + g.t0);
+        // T_cap is a multiple of 128 (LatentKVCache): the tile's zero points are
+        // 512 aligned bytes inside this sequence/group's row range
+        bulk_load(slot + RB, vp.zps + (size_t)g.bg * p.T_cap + g.t0, TILE_M * 4, &rfull[rs]);
+        ++k;
+      }
+    }
+    return;
+  }
   if (warp == 8) {
     // ---------------- TMA producer: H_v does not depend on the score role,
     // so it streams every sub-unit back to back, bounded by the ring
@@ -1224,7 +1362,12 @@ value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
 // Standalone softmax + value pass on tcgen05 (after palu_rope_score_tc): every
 // CTA runs value_role over a round-robin share of the (sequence, group)
 // units; no readiness protocol.
-__global__ void __launch_bounds__(THREADS, 1)
+// bf16 V: value role warps 0-9; packed V: + converter warps 10.. (one token row per lane)
+constexpr int VALUE_THREADS_BF16 = 320;
+constexpr int VALUE_THREADS_PACKED = 448;  // 4 converter warps (8 spill at 576 threads)
+
+template <int NT>
+__global__ void __launch_bounds__(NT, 1)
 value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const VParams vp) {
   pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1802,6 +1945,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   vp.ld_ctx = ld_ctx;
   vp.no_wait = 0;
   vp.bits = 16;
+  vp.raw_slots = 0;
   vp.code_row_bytes = Rv_pad * 2;
   vp.codes = nullptr;
   vp.scales = vp.zps = nullptr;
@@ -1833,9 +1977,22 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   PALU_REQUIRE(((uintptr_t)hv & 15) == 0, "palu_value_tc: unaligned H_v");
   PALU_REQUIRE(bits == 16 || (scales && zps), "palu_value_tc: quantised values need scales/zps");
   CUtensorMap map_v = {};
+  const int row_bytes = bits == 16 ? Rv_pad * 2 : Rv_pad * bits / 8;
   if (bits == 16) {
     int rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
     if (rc) return rc;
+  } else {
+    // packed V: code tiles {128 codes, 128 rows} and the per-token zero points
+    EncodeTiledFn fn = encode_fn();
+    PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)B * G * T_cap};
+    const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    const cuuint32_t box[2] = {(cuuint32_t)(16 * bits), (cuuint32_t)TILE_M}, es[2] = {1, 1};
+    CUresult r = fn(&map_v, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(hv), dims, strides,
+                    box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    PALU_REQUIRE(r == CUDA_SUCCESS, "palu_value_tc: code tensor map failed (%d)", (int)r);
+    PALU_REQUIRE(T_cap % TILE_M == 0, "palu_value_tc: packed V needs T_cap %% 128 == 0 (got %d)", T_cap);
   }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -1870,7 +2027,14 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
   const int dyn_limit = SMEM_LIMIT - 2048;
-  const size_t side = (size_t)2 * (V_SUB / 64) * 1024 + 1024 + 4 * V_HP * 4 + 16 * 64 + 64;
+  vp.raw_slots = 0;
+  size_t raw_bytes = 0;
+  if (bits != 16) {
+    const int rb = TILE_M * 16 * bits + TILE_M * 4;
+    vp.raw_slots = V_RAW_BYTES / rb;
+    raw_bytes = (size_t)vp.raw_slots * rb + 16 * vp.raw_slots + 256;
+  }
+  const size_t side = (size_t)2 * (V_SUB / 64) * 1024 + 1024 + 4 * V_HP * 4 + 16 * 64 + 64 + raw_bytes;
   vp.v_stages = (int)(((long long)dyn_limit - 1024 - (long long)side) / V_STAGE);
   PALU_REQUIRE(vp.v_stages >= 2, "palu_value_tc: value ring too small (%d)", vp.v_stages);
   if (vp.v_stages > 8) vp.v_stages = 8;  // 32 KB stages
@@ -1885,18 +2049,24 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   vp.ld_ctx = ld_ctx;
   vp.no_wait = 1;
   vp.bits = bits;
-  vp.code_row_bytes = bits == 16 ? Rv_pad * 2 : Rv_pad * bits / 8;
+  vp.code_row_bytes = row_bytes;
   vp.codes = reinterpret_cast<const uint8_t*>(hv);
   vp.scales = scales;
   vp.zps = zps;
   static bool attr = false;
   if (!attr) {
-    PALU_CK(cudaFuncSetAttribute(value_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 dyn_limit));
+    PALU_CK(cudaFuncSetAttribute(value_tc_kernel<VALUE_THREADS_BF16>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
+    PALU_CK(cudaFuncSetAttribute(value_tc_kernel<VALUE_THREADS_PACKED>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
     attr = true;
   }
-  PALU_CK(launch_k(value_tc_kernel, dim3(sms), dim3(THREADS), (size_t)dyn_limit, (cudaStream_t)stream,
-                   map_v, prm, vp));
+  if (bits == 16)
+    PALU_CK(launch_k(value_tc_kernel<VALUE_THREADS_BF16>, dim3(sms), dim3(VALUE_THREADS_BF16),
+                     (size_t)dyn_limit, (cudaStream_t)stream, map_v, prm, vp));
+  else
+    PALU_CK(launch_k(value_tc_kernel<VALUE_THREADS_PACKED>, dim3(sms), dim3(VALUE_THREADS_PACKED),
+                     (size_t)dyn_limit, (cudaStream_t)stream, map_v, prm, vp));
   PALU_LAUNCHED();
   return launch_value_merge(pm, pl, pctx, nc_max, Rv_pad, n_heads, s, G, B, t_dev, sms, vc, ranks_v,
                             o_off, ctx, ld_ctx, (cudaStream_t)stream);

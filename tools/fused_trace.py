@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--rank-v", type=int, default=256)
     ap.add_argument("--batch", type=int, default=1)
     ap.add_argument("--score-kernel", default="fused", help="fused | tcgen05 (standalone value kernel)")
+    ap.add_argument("--bits", default="16")
     a = ap.parse_args()
     import torch
 
@@ -34,8 +35,10 @@ def main():
     from paper_2407_21118_b200.harness import synthetic_engine
 
     _lib.load()
+    bl = [int(x) for x in a.bits.split(",")]
     w, f, c = synthetic_engine(layers=1, batch=a.batch, context=a.context, extra=64,
-                               rank_k=a.rank_k, rank_v=a.rank_v)
+                               rank_k=a.rank_k, rank_v=a.rank_v,
+                               bits=bl[0] if len(bl) == 1 else tuple(bl))
     s = _session(f, c, score_kernel=a.score_kernel)
     s.x.normal_(0, 0.5)
     for _ in range(3):
@@ -68,7 +71,9 @@ def main():
     merges = [(us(tr[i, 500]), us(tr[i, 501])) for i in value if tr[i, 500] > 0]
     print("merges (start, end) us:", [(round(a_, 1), round(b_, 1)) for a_, b_ in merges])
     for i in value[:6] + value[-2:]:
-        k = int((tr[i, 4::5][:100] > 0).sum())
+        k = int((tr[i, 4::5][:59] > 0).sum())
+        if k == 0:
+            continue
         rd = [us(tr[i, 4 + 5 * j]) for j in range(k)]
         dn = [us(tr[i, 5 + 5 * j]) for j in range(k)]
         ph = np.array([[tr[i, 6 + 5 * j] - tr[i, 4 + 5 * j], tr[i, 5 + 5 * j] - tr[i, 6 + 5 * j],
@@ -81,6 +86,19 @@ def main():
         print(f"value CTA {i} (sm {tr[i, 2]}): {k} chunks, start {us(tr[i, 0]):.1f} end "
               f"{us(tr[i, 1]):.1f}; busy {stream:.1f} us; first ready {rd[0]:.1f}, "
               f"per-chunk (ready->done):", [(round(r, 1), round(d, 1)) for r, d in zip(rd[:6], dn[:6])])
+
+
+
+    conv = [i for i in value if tr[i, 300] > 0]
+    if conv:
+        i = conv[0]
+        k = int((tr[i, 300:500:3] > 0).sum())
+        st = tr[i, 300:300 + 3 * k].reshape(k, 3)
+        w_raw = (st[:, 1] - st[:, 0]) / 1e3
+        w_empty = (st[:, 2] - st[:, 1]) / 1e3
+        conv_t = (st[1:, 0] - st[:-1, 2]) / 1e3
+        print(f"converter CTA {i}: {k} stages; wait raw-ring p50 {np.median(w_raw):.2f} us, "
+              f"wait empty stage p50 {np.median(w_empty):.2f} us, convert p50 {np.median(conv_t):.2f} us")
 
 
 if __name__ == "__main__":
