@@ -409,6 +409,19 @@ def main():
         roofline_head = {"bound": "tensor", "achieved": achieved_tf, "peak": tf_sus, "unit": "TFLOP/s",
                          "frac": achieved_tf / tf_sus, "traffic": None,
                          "peak_source": f"{src} sustained bf16"}
+    # measured DRAM traffic of the dominant kernel, from a committed ncu capture
+    # of the same workload (profiles/r01_traffic.json), else null
+    workload = (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
+                + ("rope" if args.rope == "on" else "norope"))
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_traffic.json")) as fh:
+            tr = json.load(fh).get(score_name)
+        if (tr and tr["workload"] == workload and tr["context"] == args.context
+                and tr["batch"] == args.batch and args.bits == 16):
+            roofline_head["traffic"] = tr["bytes"]
+            roofline_head["traffic_source"] = "profiles/" + tr["capture"]
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {**roofline_head,
                 "kernel": score_name, "kernel_ms": score_ms,
                 "share_of_step": sum(prof[score_name]) / total_kernel_ms,
