@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--shard", default="batch", choices=["batch", "heads"],
                     help="multi-GPU: batch replicas (weak scaling) or head-group shards with one "
                          "NCCL all-reduce of the layer output per layer (strong scaling)")
+    ap.add_argument("--rope-base", type=float, default=10000.0,
+                    help="1e6 for the Mistral-7B-shaped config (32 q-heads / 8 KV groups, SURVEY 8(d) C4)")
     ap.add_argument("--rope", default="on", choices=["on", "off"],
                     help="off: palu_decode_step_norope path (attention.py:365-389)")
     ap.add_argument("--score-kernel", default="auto")
@@ -320,7 +322,7 @@ def main():
                                              context=args.context, extra=extra, bits=args.bits,
                                              dtype=args.dtype, seed=1234 + (0 if heads else rank),
                                              rank_k=args.rank_k, rank_v=args.rank_v,
-                                             rope=args.rope == "on")
+                                             rope=args.rope == "on", rope_base=args.rope_base)
     if heads:
         # this rank keeps its head groups; one all-reduce per layer
         from paper_2407_21118_b200.sharding import attach_allreduce, shard_engine
@@ -454,7 +456,7 @@ def main():
                        "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
                        "batch_per_gpu": args.batch,
                        "global_batch": args.batch if heads else args.batch * world,
-                       "layers": args.layers, "bits": args.bits,
+                       "layers": args.layers, "bits": args.bits, "rope_base": args.rope_base,
                        "parallelism": (f"heads{world}" if heads else f"replicas{world}"),
                        "l2": "inputs larger than L2 (latent cache 17 GB/step)"},
             "tokens_per_s": (args.batch if heads else args.batch * world) / (ms * 1e-3),
