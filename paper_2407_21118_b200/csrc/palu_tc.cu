@@ -26,7 +26,6 @@
 namespace palu {
 namespace tc {
 
-constexpr int BASE_RING = 4;       // tile-base cos/sin rows in flight
 constexpr int PF_DIST = 3;         // L2 prefetch distance (work items)
 constexpr int BASE_BYTES = 64 * 8; // 64 float2
 constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
@@ -230,17 +229,14 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   const int halves = p.s_k / 2;
   uint8_t* s_uw = smem;                                  // [kblocks][halves] x 16 KB
   uint8_t* s_h = smem + kblocks * halves * HEAD_BYTES;   // stages x 16 KB
-  float2* s_base = reinterpret_cast<float2*>(s_h + p.stages * H_STAGE_BYTES);  // ring
-  uint64_t* bars = reinterpret_cast<uint64_t*>(s_base + BASE_RING * 64);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + p.stages * H_STAGE_BYTES);
   uint64_t* full = bars;                                 // [stages]   (leader's used)
   uint64_t* empty = bars + p.stages;                     // [stages]   (each SM's own)
   uint64_t* tfull = bars + 2 * p.stages;                 // [2]        (each SM's own)
   uint64_t* tempty = tfull + 2;                          // [2]        (leader's used)
   uint64_t* uw_full = tempty + 2;                        // [1]        (leader's used)
   uint64_t* uw_empty = uw_full + 1;                      // [1]        (each SM's own)
-  uint64_t* bfull = uw_empty + 1;                        // [BASE_RING] local
-  uint64_t* bempty = bfull + BASE_RING;                  // [BASE_RING] local
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bempty + BASE_RING);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_empty + 1);
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -265,10 +261,6 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EPI_WARPS);
-    }
-    for (int a = 0; a < BASE_RING; ++a) {
-      mbar_init(&bfull[a], 1);
-      mbar_init(&bempty[a], EPI_WARPS);
     }
     mbar_init(uw_full, 1);
     mbar_init(uw_empty, 1);
@@ -304,10 +296,6 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           cur = bg;
         }
         const int tile = 2 * st + (int)rank;  // this SM's 128-token tile
-        const int bs = it % BASE_RING;
-        mbar_wait(&bempty[bs], ((it / BASE_RING) & 1) ^ 1);
-        mbar_expect_tx(&bfull[bs], BASE_BYTES);
-        bulk_load(s_base + bs * 64, p.rope_tab + (size_t)tile * 64, BASE_BYTES, &bfull[bs]);
         const int h_row = bg * p.T_cap + tile * TILE_M;
         // warm L2 with this SM's rows of the item PF_DIST ahead: smem holds only
         // ~1.25 items next to the resident UW, so HBM latency must be hidden in L2
@@ -411,29 +399,32 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       const int bg = i / n_super, st = i - bg * n_super;
       const int b = bg / p.G, g = bg - b * p.G;
       const int tile = 2 * st + (int)rank;
-      const int bs = it % BASE_RING;
+      // this tile's cos/sin base row (fp64-reduced, L2-resident table): issued
+      // before the accumulator wait, so its latency hides behind the MMAs
+      float4 bv4[16];
+      {
+        const float4* base = reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile * 64 + jh * 32);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) bv4[k] = __ldg(base + k);
+      }
       // quantised keys: the converter wrote c - z, so logit = s_t x (epilogue sum)
       float sq = 1.f;
       if (p.bits != 16) {
         const int tq = tile * TILE_M + delta;
         if (tq < T_rows) sq = __ldg(p.scales + (size_t)bg * p.T_cap + tq);
       }
-      mbar_wait(&bfull[bs], (it / BASE_RING) & 1);
       // cos/sin((t0 + delta) th_j) = base (x) offset, for this thread's 32 frequencies
       float2 c2[16], s2[16];
       {
-        const float4* base = reinterpret_cast<const float4*>(s_base + bs * 64 + jh * 32);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-          const float4 bv = base[k];
+          const float4 bv = bv4[k];
           const float2 bc = make_float2(bv.x, bv.z), bsn = make_float2(bv.y, bv.w);
           const float2 t = fmul2(bsn, sd2[k]);
           c2[k] = ffma2(bc, cd2[k], make_float2(-t.x, -t.y));
           s2[k] = ffma2(bsn, cd2[k], fmul2(bc, sd2[k]));
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bempty[bs]);
       for (int h = 0; h < halves; ++h, ++unit) {
         const int slot = unit & 1;
         mbar_wait(&tfull[slot], (unit >> 1) & 1);
@@ -515,6 +506,9 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
   pdl_enter();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // no static shared memory here: the dynamic window starts 1024-aligned, and
+  // the host sizes it without an alignment pad (room for a 6th H stage)
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   score_role(map_h, map_uw, p, smem);
@@ -1705,7 +1699,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, TILE_M);
   if (rc) return rc;
   const int kblocks = R_pad / KB;
-  const int fixed = 1024 + kblocks * (s_k / 2) * HEAD_BYTES + BASE_RING * BASE_BYTES + 1024 +
+  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + 256 +
                     2 * 2 * TILE_M * 4;
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
@@ -1868,7 +1862,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   rc = make_map_2d(&map_uw, uw, Rk_pad, (uint64_t)B * G * s * 128, KB, TILE_M);
   if (rc) return rc;
   const int kblocks = Rk_pad / KB;
-  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + BASE_RING * BASE_BYTES + 1024 +
+  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + 256 +
                     2 * 2 * TILE_M * 4;
   const int dyn_limit = SMEM_LIMIT - 2048;  // the value role has ~1 KB of static smem
   int stages = (dyn_limit - fixed) / H_STAGE_BYTES;
