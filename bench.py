@@ -434,10 +434,19 @@ def main():
 
     uncompressed = None
     if not args.no_baseline:
+        # free the Palu engine first: the uncompressed caches are 2x the latent ones
         del sess
         cache._session = None
+        del weights, fused, cache
+        import gc
+
+        gc.collect()
         torch.cuda.empty_cache()
-        uncompressed = uncompressed_baseline(args, ms)
+        try:
+            uncompressed = uncompressed_baseline(args, ms)
+        except torch.OutOfMemoryError as exc:  # comparator only: keep the Palu line
+            uncompressed = {"error": f"OutOfMemoryError: {str(exc)[:120]}"}
+            torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:

@@ -39,7 +39,9 @@ class ShardedAttentionConfig(AttentionConfig):
 
 
 def _shard_layer(L: LayerFused, dec: LayerKV, n: int, dh: int, rope: bool, shard, dev):
-    torch = _torch()
+    # pure index slicing on whatever device L lives on (host-testable);
+    # shard_engine itself requires CUDA via the cache it builds
+    import torch
     h0, h1 = shard.heads[0], shard.heads[-1] + 1
     kg, vg = list(shard.k_groups), list(shard.v_groups)
     rk, rv = list(L.key_ranks), list(L.value_ranks)
