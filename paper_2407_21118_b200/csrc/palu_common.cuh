@@ -42,7 +42,19 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
+// Split form (score and value kernels): launch dependents first, wait for
+// the predecessor only where its output is read.  A kernel K starts once its
+// predecessor P executed launch_dependents: if P waits first (pdl_enter),
+// everything before P has completed; if P is split, everything before P's
+// predecessor has.  The step order gemv -> append -> absorb -> score (split)
+// -> value (split) -> merge therefore lets score read the latent rows and
+// value stream H_v before their waits.
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
+int pdl_split();  // PALU_PDL_SPLIT=0: split-form kernels wait at entry (A/B diagnostics)
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

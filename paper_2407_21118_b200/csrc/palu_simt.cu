@@ -21,6 +21,14 @@ bool pdl_enabled() {
   return on != 0;
 }
 
+int pdl_split() {
+  static const int on = [] {
+    const char* e = getenv("PALU_PDL_SPLIT");
+    return (e && e[0] == '0') ? 0 : 1;
+  }();
+  return on;
+}
+
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
@@ -41,8 +49,11 @@ constexpr int GEMV_UNROLL_DEF = 8;  // 16-byte weight loads in flight per lane
 template <typename T, int MAXB, int GEMV_UNROLL>
 __global__ void __launch_bounds__(GEMV_WARPS * 32)
 gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, int B, int ldx,
-            float* __restrict__ y, int ldy, int accumulate) {
-  pdl_enter();
+            float* __restrict__ y, int ldy, int accumulate, int split) {
+  // the weights are constant: the first batch of weight loads is issued
+  // before waiting for the predecessor that writes x (PDL split form)
+  pdl_launch();
+  if (!split) pdl_wait();
   using V = Vec16<T>;
   constexpr int VEC = V::N;
   constexpr int STEP = 32 * VEC;
@@ -53,11 +64,19 @@ gemv_kernel(const T* __restrict__ W, int N, int K, const float* __restrict__ x, 
   float acc[MAXB];
 #pragma unroll
   for (int b = 0; b < MAXB; ++b) acc[b] = 0.f;
+  uint4 nxt[GEMV_UNROLL];
+  auto load = [&](int k) {
+#pragma unroll
+    for (int u = 0; u < GEMV_UNROLL; ++u)
+      if (k + u * STEP < K) nxt[u] = ldg_stream(wr + k + u * STEP);
+  };
+  load(lane * VEC);
+  pdl_wait();
   for (int k = lane * VEC; k < K; k += GEMV_UNROLL * STEP) {
     uint4 v[GEMV_UNROLL];
 #pragma unroll
-    for (int u = 0; u < GEMV_UNROLL; ++u)
-      if (k + u * STEP < K) v[u] = ldg_stream(wr + k + u * STEP);
+    for (int u = 0; u < GEMV_UNROLL; ++u) v[u] = nxt[u];
+    if (k + GEMV_UNROLL * STEP < K) load(k + GEMV_UNROLL * STEP);  // next batch in flight
 #pragma unroll
     for (int u = 0; u < GEMV_UNROLL; ++u) {
       const int kk = k + u * STEP;
@@ -98,10 +117,10 @@ static int launch_gemv(const T* W, int N, int K, const float* x, int B, int ldx,
   static const int unroll = getenv("PALU_GEMV_UNROLL") ? atoi(getenv("PALU_GEMV_UNROLL")) : GEMV_UNROLL_DEF;
   if (unroll >= 16)
     PALU_CK(launch_k(gemv_kernel<T, MAXB, 16>, grid, dim3(GEMV_WARPS * 32), 0, st, W, N, K, x, B,
-                     ldx, y, ldy, acc));
+                     ldx, y, ldy, acc, pdl_split()));
   else
     PALU_CK(launch_k(gemv_kernel<T, MAXB, 8>, grid, dim3(GEMV_WARPS * 32), 0, st, W, N, K, x, B,
-                     ldx, y, ldy, acc));
+                     ldx, y, ldy, acc, pdl_split()));
   PALU_LAUNCHED();
   return PALU_OK;
 }

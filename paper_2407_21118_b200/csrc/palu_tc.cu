@@ -39,6 +39,7 @@ struct Params {
   int* ready;       // fused: per work item, epilogue warps that published its logits
   int mode;     // profiling only (bit flags): 1 epilogue skips math; 2 MMA skips TMA waits; 4 MMA skips TMEM-empty waits
   int pf_dist;  // L2 prefetch distance in work items (0 = off)
+  int pdl_split;  // 0: wait for the predecessor at entry (A/B diagnostics)
   const float2* rope_tab;  // [n_tab + 128][64]
   const int* t_dev;
   float* logits;
@@ -249,6 +250,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   const int per = (total + n_pairs - 1) / n_pairs;
   const int i0 = min(total, pair_id * per);
   const int i1 = min(total, i0 + per);
+  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0)
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     prefetch_map(&map_h);
@@ -278,10 +281,26 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0)
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = gtimer();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA producer (both SMs) ----------------
+      // standalone kernel: warm L2 with the first items' rows (latent append,
+      // two launches back) while the query absorb still runs, then wait for
+      // it before the first UW load
+      if (p.pf_dist > 0 && p.ready == nullptr)
+        for (int ip = i0; ip < min(i1, i0 + p.pf_dist); ++ip) {
+          const int bgp = ip / n_super, stp = ip - bgp * n_super;
+          const int rowp = bgp * p.T_cap + (2 * stp + (int)rank) * TILE_M;
+          if (p.bits == 16) {
+            for (int kb = 0; kb < kblocks; ++kb) tma_prefetch_l2(&map_h, kb * KB, rowp);
+          } else {
+            tma_prefetch_l2(&map_h, 0, rowp);
+          }
+        }
+      pdl_wait();
       int cur = -1, nloads = 0, kc = 0, it = 0;
       for (int i = i0; i < i1; ++i, ++it) {
         const int bg = i / n_super, st = i - bg * n_super;
@@ -504,7 +523,10 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
-  pdl_enter();
+  // setup overlaps the query absorb; only the UW loads read its output
+  // (score_role's producer waits before them)
+  pdl_launch();
+  if (!p.pdl_split) pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // no static shared memory here: the dynamic window starts 1024-aligned, and
   // the host sizes it without an alignment pad (room for a 6th H stage)
@@ -865,6 +887,8 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
+  unsigned long long* vtr = p.trace != nullptr ? p.trace + (size_t)blockIdx.x * TRACE_STRIDE : nullptr;
+  if (vtr != nullptr && tid == 0) vtr[495] = gtimer();  // setup done
   VIter it(sch, vcta, n_vctas);
   VUnit u;
   if (warp >= 10) {
@@ -965,6 +989,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
               tma_prefetch_l2(&map_v, j * 128 + 64, rowp);
             }
             mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
+            if (vtr != nullptr && ctr == 0) vtr[496] = gtimer();  // first TMA issue
             mbar_expect_tx(&full[st], V_STAGE);
             const int row = u.bg * p.T_cap + c0 + blk * TILE_M;
             tma_load_2d(&map_v, &full[st], ring + st * V_STAGE, j * 128, row);
@@ -994,6 +1019,8 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
               const int st = ctr % vs;
               mbar_wait(&full[st], (ctr / vs) & 1);
               fence_after();
+              if (vtr != nullptr && ctr == 0) vtr[497] = gtimer();  // first stage landed
+              if (vtr != nullptr && ctr == vs) vtr[498] = gtimer();  // ring wrapped
               if (p.mode & 1) {  // diagnostics: release the stage without MMAs
                 mbar_arrive(&empty[st]);
                 continue;
@@ -1026,6 +1053,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
 
   if (warp < 4) {
     // ======== group A (warps 0-3): logits -> statistics -> P operand ========
+    pdl_wait();  // the logits come from the preceding score launch
     const int ta = tid;  // 0..127
     int kk_trace = 0;
     auto trace = [&](int slot) {
@@ -1363,7 +1391,10 @@ constexpr int VALUE_THREADS_PACKED = 448;  // 4 converter warps (8 spill at 576 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1)
 value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const VParams vp) {
-  pdl_enter();
+  // H_v (written by the latent append, three launches back) streams into the
+  // ring while the score kernel drains; group A waits before reading logits
+  pdl_launch();
+  if (!p.pdl_split) pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -1714,7 +1745,8 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  Params prm;
+  Params prm = {};
+  prm.pdl_split = pdl_split();
   prm.B = B;
   prm.n_heads = n_heads;
   prm.s_k = s_k;
@@ -1891,7 +1923,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   unsigned* tickets = W.tickets;
   int* ready = W.ready;
   float *pm = W.pm, *pl = W.pl, *pctx = W.pctx;
-  Params prm;
+  Params prm = {};
+  prm.pdl_split = pdl_split();
   prm.B = B;
   prm.n_heads = n_heads;
   prm.s_k = s;
@@ -1999,6 +2032,7 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   int* ready = W.ready;
   float *pm = W.pm, *pl = W.pl, *pctx = W.pctx;
   Params prm = {};
+  prm.pdl_split = pdl_split();
   prm.B = B;
   prm.n_heads = n_heads;
   prm.s_k = s;

@@ -68,6 +68,13 @@ def main():
         ev = [us(x) for x in tr[i, 4:4 + cnt]]
         print(f"score CTA {i} (sm {tr[i, 2]}): {cnt} items, done at", [round(x, 1) for x in ev[:8]],
               "...", [round(x, 1) for x in ev[-3:]])
+    if value:
+        ph = np.array([[us(tr[i, c]) for c in (495, 496, 497, 498)] for i in value])
+        print("value setup done / first TMA / first stage landed / ring wrapped (median us):",
+              np.median(ph, axis=0).round(2), "vs end", round(float(np.median([us(tr[i, 1]) for i in value])), 1))
+        ev = np.array([us(tr[i, 1]) for i in value])
+        sm = np.array([tr[i, 2] for i in value])
+        print("end by SM parity: even", np.median(ev[sm % 2 == 0]).round(1), "odd", np.median(ev[sm % 2 == 1]).round(1))
     merges = [(us(tr[i, 500]), us(tr[i, 501])) for i in value if tr[i, 500] > 0]
     print("merges (start, end) us:", [(round(a_, 1), round(b_, 1)) for a_, b_ in merges])
     for i in value[:6] + value[-2:]:

@@ -42,7 +42,19 @@ def main():
     buf = np.zeros((1024, 512), dtype=np.uint64)
     n = _lib.call("palu_fused_trace", buf.ctypes.data_as(C.c_void_p), 1024)
     tr = buf[:n].astype(np.int64)
-    t0 = tr[:, 0][tr[:, 0] > 0].min() if (tr[:, 0] > 0).any() else tr[tr > 0].min()
+    t0 = tr[:, 0][tr[:, 0] > 0].min()  # earliest CTA entry
+    ent, setup, end = (tr[:, 0] - t0) / 1e3, (tr[:, 2] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
+    pc = lambda x: np.percentile(x, [0, 50, 100]).round(2)
+    print(f"CTA entry us min/med/max {pc(ent)}; setup done {pc(setup)}; exit {pc(end)}")
+    firsts, lasts = [], []
+    for cta in range(0, n, 2):
+        if tr[cta, 4] > 0:
+            firsts.append((tr[cta, 4] - t0) / 1e3)
+            u = int(tr[cta, 3]) * 2 - 1
+            while u >= 0 and (4 * u + 7 >= 512 or tr[cta, 7 + 4 * u] == 0):
+                u -= 1
+            lasts.append((tr[cta, 7 + 4 * u] - t0) / 1e3)
+    print(f"first MMA {pc(np.array(firsts))}; last epilogue done {pc(np.array(lasts))}")
     rows = []
     for cta in range(0, n, 2):  # leaders
         u = 0
