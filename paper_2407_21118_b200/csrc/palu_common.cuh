@@ -42,13 +42,15 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
-// Split form (score and value kernels): launch dependents first, wait for
-// the predecessor only where its output is read.  A kernel K starts once its
-// predecessor P executed launch_dependents: if P waits first (pdl_enter),
-// everything before P has completed; if P is split, everything before P's
-// predecessor has.  The step order gemv -> append -> absorb -> score (split)
-// -> value (split) -> merge therefore lets score read the latent rows and
-// value stream H_v before their waits.
+// Split form (GEMV, query absorb, score and value kernels): launch
+// dependents first, wait for the predecessor only where its output is read.
+// A kernel K starts once its predecessor P executed launch_dependents: if P
+// waits first (pdl_enter), everything before P has completed; if P is split,
+// everything before P's predecessor has.  In the step order
+//   gemv (split) -> append K -> append V -> absorb (split) -> score (split)
+//   -> value (split) -> merge -> gemv (split)
+// score may therefore read the key rows (append K) and value the H_v rows
+// (append V) before their waits; gemv and absorb read only constants early.
 __device__ __forceinline__ void pdl_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }

@@ -281,14 +281,18 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
                                     int s_k, const T* __restrict__ bk, int bk_rows, int R_pad,
                                     const double* __restrict__ theta, float scale,
                                     const int* __restrict__ t_dev, void* __restrict__ uw,
-                                    int layout) {
-  pdl_enter();
+                                    int layout, int split) {
+  // PDL split form: the fp64 angles (t, theta) and the B_k slice (constant)
+  // are prepared before waiting for the GEMV that produced q
+  pdl_launch();
+  if (!split) pdl_wait();
   // grid (n_heads, ceil(R_pad / 32), B): one head, 32 rank rows per CTA
-  extern __shared__ float qa_sm[];  // qr[dh] then bs[32][dh]
+  extern __shared__ float qa_sm[];  // qr[dh] then bs[32][dh] then cs/sn[dh/2] (fp64)
   float* qr = qa_sm;
   float* bs = qa_sm + dh;
   const int i = blockIdx.x, k0 = blockIdx.y * 32, b = blockIdx.z;
   const int half = dh / 2;
+  double* csn = reinterpret_cast<double*>(qa_sm + 33 * dh);  // [half] cos, [half] sin
   const int g = i / s_k, p = i - g * s_k;
   const int nk = min(32, R_pad - k0);
   const double pos = (double)(*t_dev);
@@ -296,9 +300,8 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
     double sn, cs;
     sincos_big(pos * theta[j], &sn, &cs);  // attention.py:108-112 (fp64 angles)
-    const double lo = qh[j], hi = qh[j + half];
-    qr[j] = (float)(lo * cs - hi * sn);
-    qr[j + half] = (float)(lo * sn + hi * cs);
+    csn[j] = cs;
+    csn[half + j] = sn;
   }
   const int width = s_k * dh;
   const T* bg = bk + ((size_t)g * bk_rows + k0) * width + (size_t)p * dh;
@@ -333,6 +336,13 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
       const int kk = idx / dh, c = idx - kk * dh;
       bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
     }
+  }
+  pdl_wait();  // q comes from the preceding GEMV
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    const double cs = csn[j], sn = csn[half + j];
+    const double lo = qh[j], hi = qh[j + half];
+    qr[j] = (float)(lo * cs - hi * sn);
+    qr[j + half] = (float)(lo * sn + hi * cs);
   }
   __syncthreads();
   if (layout == 0) {
@@ -1273,16 +1283,15 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
                n_heads);
   PALU_REQUIRE(layout >= 0 && layout <= 3, "palu_query_absorb: layout must be 0..3");
   dim3 grid(n_heads, (R_pad + 31) / 32, B);
-  const size_t smem = (size_t)33 * head_dim * sizeof(float);
+  const size_t smem = (size_t)33 * head_dim * sizeof(float) + (size_t)head_dim * sizeof(double);
   if (dtype == PALU_DTYPE_BF16)
-    PALU_CK(launch_k(query_absorb_kernel<bf16>, dim3(grid), dim3(256), smem, S(stream), q, ld_q, n_heads, head_dim, s_k,
-                                                              (const bf16*)bk, bk_rows, R_pad, theta,
-                                                              scale,
-                                                              t_dev, uw, layout));
+    PALU_CK(launch_k(query_absorb_kernel<bf16>, dim3(grid), dim3(256), smem, S(stream), q, ld_q,
+                     n_heads, head_dim, s_k, (const bf16*)bk, bk_rows, R_pad, theta, scale, t_dev,
+                     uw, layout, pdl_split()));
   else
-    PALU_CK(launch_k(query_absorb_kernel<float>, dim3(grid), dim3(256), smem, S(stream), q, ld_q, n_heads, head_dim, s_k,
-                                                               (const float*)bk, bk_rows, R_pad,
-                                                               theta, scale, t_dev, uw, layout));
+    PALU_CK(launch_k(query_absorb_kernel<float>, dim3(grid), dim3(256), smem, S(stream), q, ld_q,
+                     n_heads, head_dim, s_k, (const float*)bk, bk_rows, R_pad, theta, scale, t_dev,
+                     uw, layout, pdl_split()));
   PALU_LAUNCHED();
   return PALU_OK;
 }

@@ -343,6 +343,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
       int cur = -1, nloads = 0, kc = 0, unit = 0;
+      const unsigned long long c_start = clock64(), g_start = gtimer();
       for (int i = i0; i < i1; ++i) {
         const int bg = i / n_super;
         if (bg != cur) {
@@ -366,8 +367,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
               mbar_wait(&full[stage], (cnt / p.stages) & 1);
               fence_after();
             }
-            const uint32_t a0 = h_addr + stage * H_STAGE_BYTES;
-            const uint32_t b0 = uw_addr + (kb * halves + h) * HEAD_BYTES;
+            // profile modes 8 / 16 (diagnostics): pin the A / B operand tile
+            const uint32_t a0 = h_addr + ((p.mode & 8) ? 0 : stage) * H_STAGE_BYTES;
+            const uint32_t b0 = uw_addr + ((p.mode & 16) ? 0 : (kb * halves + h)) * HEAD_BYTES;
 #pragma unroll
             for (int kk = 0; kk < KB / 16; ++kk)
               umma2_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
@@ -378,6 +380,11 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = gtimer();
         }
         kc += kblocks;
+      }
+      if (p.trace != nullptr && p.ready == nullptr) {  // SM clocks vs wall time of the issue loop
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 508] = clock64() - c_start;
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 509] = gtimer() - g_start;
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 510] = (unsigned long long)unit * kblocks * (KB / 16);
       }
     }
   } else if (warp >= 2 + EPI_WARPS) {
@@ -1952,7 +1959,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   CUtensorMap map_v;
   rc = make_map_2d(&map_v, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
   if (rc) return rc;
-  VParams vp;
+  VParams vp = {};
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
   const size_t side = (size_t)2 * (V_SUB / 64) * 1024 + 1024 + 4 * V_HP * 4 + 16 * 64 + 64;
@@ -2051,7 +2058,7 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
     prm.trace = g_trace;
     g_trace_ctas = sms;
   }
-  VParams vp;
+  VParams vp = {};
   vp.Rv_pad = Rv_pad;
   vp.vc = vc;
   const int dyn_limit = SMEM_LIMIT - 2048;

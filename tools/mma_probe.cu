@@ -5,20 +5,26 @@
 //        -I include -o tools/mma_probe tools/mma_probe.cu
 #include <cstdio>
 #include <cstdint>
+#include <cstdlib>
 
 #include "palu_sm100.cuh"
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned long long gtimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 using namespace palu::tc;
 
 template <int M, int N, int CG>
-__global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int extra,
+__global__ void __launch_bounds__(320, 1) mma_probe(int iters, float* sink, int extra,
                                                     const __grid_constant__ CUtensorMap map) {
   extern __shared__ __align__(1024) uint8_t raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 96 * 1024);
-  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 128 * 1024);  // [0] end [1] unused [2] commit [4..7] TMA ring
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 8);
   const int warp = threadIdx.x >> 5;
   uint32_t rank = 0;
   if (CG == 2) rank = cluster_rank();
@@ -27,6 +33,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int 
     mbar_init(&bar[1], 1);
     mbar_init(&bar[2], 1);
     mbar_init(&bar[0], 1);
+    for (int r = 0; r < 4; ++r) mbar_init(&bar[4 + r], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -38,6 +45,16 @@ __global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int 
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
     }
   }
+  if (extra & 16) {  // random bf16 operands in [-1, 1) (all-zero smem toggles no datapath bits)
+    uint16_t* h = reinterpret_cast<uint16_t*>(sm);
+    for (int i = threadIdx.x; i < 96 * 512; i += blockDim.x) {
+      uint32_t x = (uint32_t)i * 2654435761u ^ (blockIdx.x * 40503u);
+      x ^= x >> 13; x *= 0x5bd1e995u; x ^= x >> 15;
+      const float f = (float)(x & 0xFFFF) / 32768.f - 1.f;
+      h[i] = (uint16_t)(__float_as_uint(f) >> 16);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
   fence_before();
   __syncthreads();
   if (CG == 2) cluster_sync();
@@ -46,6 +63,7 @@ __global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int 
   constexpr uint32_t ID = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) |
                           ((uint32_t)(M >> 4) << 24);
   if (threadIdx.x == 0 && (CG == 1 || rank == 0)) {
+    const unsigned long long c0 = clock64(), g0 = gtimer_ns();
     const uint32_t a0 = smem_u32(sm), b = smem_u32(sm + 32 * 1024);
     for (int i = 0; i < iters; ++i) {
       if (extra & 4) {  // a commit per 4 MMAs (the score kernel's per-k-block stage release)
@@ -54,15 +72,19 @@ __global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int 
       if ((extra & 8) && (i & 3) == 0) {  // different A stage per k-block (16 KB apart)
       }
       const uint32_t a = (extra & 8) ? a0 + (uint32_t)((i & 1) * 16384) : a0;
+      // extra 32: the score kernel's D pattern (slot alternates every 16 MMAs,
+      // first MMA of a unit overwrites); extra 64: accumulate flag only
+      const uint32_t dt = (extra & 32) ? tmem + (uint32_t)(((i >> 2) & 1) * 256) : tmem;
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
+        const uint32_t acc = ((extra & 96) && (i & 3) == 0 && kk == 0) ? 0u : 1u;
         if (CG == 1)
-          umma_bf16_id(tmem, sdesc(a + kk * 32), sdesc(b + kk * 32), ID, 1);
+          umma_bf16_id(dt, sdesc(a + kk * 32), sdesc(b + kk * 32), ID, acc);
         else
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
-              "l"(sdesc(a + kk * 32)), "l"(sdesc(b + kk * 32)), "r"(ID), "r"(1)
+              "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+              "l"(sdesc(a + kk * 32)), "l"(sdesc(b + kk * 32)), "r"(ID), "r"(acc)
               : "memory");
       }
     }
@@ -70,25 +92,37 @@ __global__ void __launch_bounds__(128, 1) mma_probe(int iters, float* sink, int 
       umma_commit(&bar[0]);
     else
       umma2_commit_both(&bar[0]);
+    mbar_wait(&bar[0], 0);
+    if (blockIdx.x == 0) {
+      sink[2] = (float)(clock64() - c0);
+      sink[3] = (float)(gtimer_ns() - g0);
+    }
   }
   volatile int* stop = reinterpret_cast<volatile int*>(slot + 4);
-  if (threadIdx.x == 0) { mbar_wait(&bar[0], 0); *stop = 1; }
+  if (threadIdx.x == 0) { if (!(CG == 1 || rank == 0)) mbar_wait(&bar[0], 0); *stop = 1; }
   if (warp == 1 && (extra & 1) && lane_id() == 0) {
-    // continuous 16 KB TMA tile loads into a 64 KB ring (no consumer)
-    uint64_t* tb = bar + 1;
-    for (int i = 0; *stop == 0 && i < 1000000; ++i) {
-      mbar_expect_tx(tb, 16384);
-      tma_load_2d(&map, tb, sm + 64 * 1024 - 16384 * 0 + 0 * (i & 3), 0, (blockIdx.x * 64 + (i % 64)) * 128 % 65536);
-      mbar_wait(tb, i & 1);
+    // continuous TMA tile loads, 4 x 16 KB in flight, into a ring at 64..128 KB
+    // (no consumer): the score kernel's H-stage write pressure on shared memory
+    for (int i = 0; *stop == 0 && i < 100000000; ++i) {
+      const int r = i & 3;
+      if (i >= 4) mbar_wait(&bar[4 + r], ((i >> 2) - 1) & 1);
+      mbar_expect_tx(&bar[4 + r], 16384);
+      tma_load_2d(&map, &bar[4 + r], sm + 64 * 1024 + r * 16384, 0,
+                  (int)(((blockIdx.x * 28331u + (unsigned)i) * 128u) % (1u << 22)));
     }
   }
-  if ((warp == 2 || warp == 3) && (extra & 2)) {
-    float v[16];
-    for (int i = 0; *stop == 0 && i < 1000000; ++i) {
-      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + 256 + (i & 7) * 16, v);
+  if (warp >= 2 && (extra & 2)) {
+    // 8 warps read the other TMEM slot like the score epilogue (2 x 16 columns, wait, FMAs)
+    float v[16], w[16], acc = 0.f;
+    for (int i = 0; *stop == 0 && i < 10000000; ++i) {
+      const uint32_t col = 256 + (i & 3) * 32 + ((warp - 2) >> 2) * 128;
+      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + col, v);
+      tmem_ld16(tmem + ((uint32_t)((warp & 3) * 32) << 16) + col + 16, w);
       tmem_wait_ld();
-      if (v[0] == 12345.f) sink[1] = v[1];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) acc = fmaf(v[k], w[k], acc);
     }
+    if (acc == 12345.f) sink[1] = acc;
   }
   fence_before();
   __syncthreads();
@@ -112,11 +146,11 @@ static int g_extra = 0;
 template <int M, int N, int CG>
 void run(const char* name) {
   auto k = mma_probe<M, N, CG>;
-  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(148);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = 100 * 1024;
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = 140 * 1024;
   cudaLaunchAttribute attr;
   attr.id = cudaLaunchAttributeClusterDimension;
   attr.val.clusterDim.x = CG;
@@ -126,7 +160,7 @@ void run(const char* name) {
   cfg.numAttrs = 1;
   float* sink;
   cudaMalloc(&sink, 64);
-  const int iters = 4000;
+  const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 4000;
   cudaLaunchKernelEx(&cfg, k, iters, sink, g_extra, g_map);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
@@ -140,23 +174,26 @@ void run(const char* name) {
   const double mmas = (double)iters * 4;  // per issuing CTA
   const int issuers = 148 / CG;
   const double flops = 2.0 * M * N * 16 * mmas * issuers;
-  printf("extra %d %-24s %7.2f ns/MMA  %7.1f TFLOP/s  (%s)\n", g_extra, name, ms * 1e6 / mmas, flops / (ms * 1e-3) / 1e12,
+  float hs[4];
+  cudaMemcpy(hs, sink, 16, cudaMemcpyDeviceToHost);
+  printf("extra %d %-24s %7.2f ns/MMA  %7.1f TFLOP/s  CTA0: %.3f GHz %.0f clk/MMA (%s)\n", g_extra, name,
+         ms * 1e6 / mmas, flops / (ms * 1e-3) / 1e12, hs[2] / hs[3], hs[2] / mmas,
          cudaGetErrorString(cudaGetLastError()));
 }
 
 int main() {
   void* buf;
-  cudaMalloc(&buf, (size_t)256 << 20);
+  cudaMalloc(&buf, (size_t)1024 << 20);
   void* fp = nullptr;
   cudaDriverEntryPointQueryResult q;
   cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fp, cudaEnableDefault, &q);
-  const cuuint64_t dims[2] = {64, 1u << 20};
+  const cuuint64_t dims[2] = {64, 1u << 22};
   const cuuint64_t strides[1] = {128};
   const cuuint32_t box[2] = {64, 128}, es[2] = {1, 1};
   ((EncodeFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  for (int e : {0, 4, 8, 12}) {
+  for (int e : {0, 32, 64, 96, 16, 48, 80}) {
     g_extra = e;
     run<256, 256, 2>("cta2 M256 N256 K16");
     run<128, 256, 1>("cta1 M128 N256 K16");

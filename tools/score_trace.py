@@ -55,6 +55,12 @@ def main():
                 u -= 1
             lasts.append((tr[cta, 7 + 4 * u] - t0) / 1e3)
     print(f"first MMA {pc(np.array(firsts))}; last epilogue done {pc(np.array(lasts))}")
+    ld = [i for i in range(0, n, 2) if tr[i, 509] > 0]
+    clk = np.array([tr[i, 508] for i in ld], dtype=float)
+    ns = np.array([tr[i, 509] for i in ld], dtype=float)
+    mm = np.array([tr[i, 510] for i in ld], dtype=float)
+    print(f"MMA loop: SM clock {np.median(clk / ns):.3f} GHz, {np.median(clk / mm):.0f} clk and "
+          f"{np.median(ns / mm):.1f} ns per pair-MMA (ideal 128 clk)")
     rows = []
     for cta in range(0, n, 2):  # leaders
         u = 0
@@ -67,6 +73,9 @@ def main():
         print("no trace")
         return
     mma_issue = (r[:, 3] - r[:, 2]) / 1e3
+    for par in (0, 1):
+        sel = r[:, 1] % 2 == par
+        print(f"  unit parity {par} (half h={par}): issue span p50 {np.median(mma_issue[sel]):.3f} us")
     epi_lat = (r[:, 4] - r[:, 3]) / 1e3     # commit -> epilogue wake (MMA execution + signal)
     epi_dur = (r[:, 5] - r[:, 4]) / 1e3     # epilogue work on the slot
     gaps = []
