@@ -26,7 +26,7 @@
 namespace palu {
 namespace tc {
 
-constexpr int PF_DIST = 3;         // L2 prefetch distance (work items)
+constexpr int PF_DIST = 0;         // L2 prefetch distance (work items); 0 measured best with PDL split (tools/pf_sweep.sh)
 constexpr int BASE_BYTES = 64 * 8; // 64 float2
 constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
 constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16

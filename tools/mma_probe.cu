@@ -34,6 +34,8 @@ __global__ void __launch_bounds__(320, 1) mma_probe(int iters, float* sink, int 
     mbar_init(&bar[2], 1);
     mbar_init(&bar[0], 1);
     for (int r = 0; r < 4; ++r) mbar_init(&bar[4 + r], 1);
+    mbar_init(&bar[3], 1);
+    mbar_arrive(&bar[3]);  // phase 0 complete: waits on it return at once
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -72,6 +74,13 @@ __global__ void __launch_bounds__(320, 1) mma_probe(int iters, float* sink, int 
       if ((extra & 8) && (i & 3) == 0) {  // different A stage per k-block (16 KB apart)
       }
       const uint32_t a = (extra & 8) ? a0 + (uint32_t)((i & 1) * 16384) : a0;
+      if (extra & 128) {  // the score kernel's per-k-block wait: satisfied mbarrier + tcgen05 fence
+        mbar_wait(&bar[3], 0);
+        fence_after();
+      }
+      if ((extra & 256) && (i & 3) == 0) {  // per unit: + a global store of a timestamp (trace)
+        sink[4 + (i & 7)] = (float)gtimer_ns();
+      }
       // extra 32: the score kernel's D pattern (slot alternates every 16 MMAs,
       // first MMA of a unit overwrites); extra 64: accumulate flag only
       const uint32_t dt = (extra & 32) ? tmem + (uint32_t)(((i >> 2) & 1) * 256) : tmem;
@@ -159,7 +168,7 @@ void run(const char* name) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   float* sink;
-  cudaMalloc(&sink, 64);
+  cudaMalloc(&sink, 256);
   const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 4000;
   cudaLaunchKernelEx(&cfg, k, iters, sink, g_extra, g_map);
   cudaEvent_t a, b;
@@ -193,7 +202,7 @@ int main() {
   ((EncodeFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  for (int e : {0, 32, 64, 96, 16, 48, 80}) {
+  for (int e : {0, 128, 256, 384, 416}) {
     g_extra = e;
     run<256, 256, 2>("cta2 M256 N256 K16");
     run<128, 256, 1>("cta1 M128 N256 K16");
