@@ -12,7 +12,8 @@ import os
 from .errors import ValidationError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpalu_b200.so")
+# PALU_LIB_PATH: load another build of the same ABI (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("PALU_LIB_PATH") or os.path.join(_HERE, "libpalu_b200.so")
 
 PALU_OK = 0
 PALU_EVALIDATION = -1
