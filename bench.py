@@ -200,21 +200,30 @@ def uncompressed_baseline(args, palu_ms):
     e1.record()
     torch.cuda.synchronize()
     k0_ms = e0.elapsed_time(e1) / K
-    # per-kernel split of one K0 layer (eager, events)
+    # per-kernel split of one K0 layer: each part timed over R back-to-back
+    # launches (steady state, like the graph-captured step; a single eager
+    # launch bracketed by events would add launch latency to the GEMVs)
     st_ = _stream()
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     d, n, dh = D, NH, DH
-    ev[0].record()
-    _lib.call("palu_gemv", m.code, _ptr(m.wqkv[0]), 3 * d, d, _ptr(m.x), B, d, _ptr(m.qkv), 3 * d, 0, st_)
-    ev[1].record()
-    _lib.call("palu_dense_decode", m.code, _ptr(m.qkv), B, n, dh, _ptr(m.kc[0]), _ptr(m.vc[0]), m.cap,
-              _ptr(m.theta), _ptr(m.t_dev), m.n_chunks, _ptr(m.ws), _ptr(m.attn), st_)
-    ev[2].record()
-    _lib.call("palu_gemv", m.code, _ptr(m.wo_t[0]), d, d, _ptr(m.attn), B, d, _ptr(m.x), d, 0, st_)
-    ev[3].record()
-    torch.cuda.synchronize()
-    proj_ms = ev[0].elapsed_time(ev[1]) + ev[2].elapsed_time(ev[3])
-    k0_attn_ms = ev[1].elapsed_time(ev[2])
+    R = 20
+
+    def timed(fn):
+        a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        a.record()
+        for _ in range(R):
+            fn()
+        b_.record()
+        torch.cuda.synchronize()
+        return a.elapsed_time(b_) / R
+
+    proj_ms = timed(lambda: (
+        _lib.call("palu_gemv", m.code, _ptr(m.wqkv[0]), 3 * d, d, _ptr(m.x), B, d, _ptr(m.qkv), 3 * d, 0, st_),
+        _lib.call("palu_gemv", m.code, _ptr(m.wo_t[0]), d, d, _ptr(m.attn), B, d, _ptr(m.qkv), d, 0, st_)))
+    k0_attn_ms = timed(lambda: _lib.call(
+        "palu_dense_decode", m.code, _ptr(m.qkv), B, n, dh, _ptr(m.kc[0]), _ptr(m.vc[0]), m.cap,
+        _ptr(m.theta), _ptr(m.t_dev), m.n_chunks, _ptr(m.ws), _ptr(m.attn), st_))
     out["own_k0_us_per_step"] = k0_ms * 1e3
     out["own_k0_attn_us_per_layer"] = k0_attn_ms * 1e3
     out["projections_us_per_layer"] = proj_ms * 1e3
@@ -237,16 +246,7 @@ def uncompressed_baseline(args, palu_ms):
             q, kv, ws, bt, sl, T, bmm1_scale=1.0 / math.sqrt(DH), bmm2_scale=1.0, kv_layout="HND")
         for _ in range(3):
             fn()
-        torch.cuda.synchronize()
-        times = []
-        for _ in range(10):
-            a, b_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            a.record()
-            fn()
-            b_.record()
-            torch.cuda.synchronize()
-            times.append(a.elapsed_time(b_))
-        fi_ms = st.median(times)
+        fi_ms = st.median(timed(fn) for _ in range(3))
         out["flashinfer_trtllm_attn_us_per_layer"] = fi_ms * 1e3
         out["flashinfer_attn_hbm_gbs"] = kv_bytes / (fi_ms * 1e-3) / 1e9
         del kv, ws
