@@ -518,7 +518,6 @@ __global__ void rope_score_generic_kernel(const void* __restrict__ hk, const flo
 // Softmax + value (attention.py:445-446, 350-362).  Split-T partials, then a
 // fixed-order merge (deterministic).
 // ---------------------------------------------------------------------------
-constexpr int SV_THREADS = 256;
 constexpr int SV_HP = 4;           // heads per pass
 constexpr int SV_MAX_CHUNK = 8192;  // tokens per chunk cap (smem)
 

@@ -27,7 +27,6 @@ namespace palu {
 namespace tc {
 
 constexpr int PF_DIST = 0;         // L2 prefetch distance (work items); 0 measured best with PDL split (tools/pf_sweep.sh)
-constexpr int BASE_BYTES = 64 * 8; // 64 float2
 constexpr int SUPER = 2 * TILE_M;  // tokens per work item (the CTA pair)
 constexpr int HEAD_BYTES = TILE_M * 128;  // one head's 128 UW rows x 64 bf16
 
@@ -1241,7 +1240,6 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
         if (tb == 0) mbar_arrive(&dempty[buf]);
       }
       // the unit's partial: columns of all heads, statistics
-#pragma unroll
       // TMEM lane m of pair j = column j*128 + m, except int4 / int2 values whose
       // converter stores rank k of each 8 / 16 group at position k < G/2 ? 2k : 2k-G+1
       const int m = wb * 32 + lane;
@@ -1907,7 +1905,6 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   int stages = (dyn_limit - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
   PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
-  const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
