@@ -1341,14 +1341,47 @@ value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
     nu += wcount[0] + wcount[1] + wcount[2] + wcount[3];
     __syncthreads();
   }
-  // (2) chunk weights exp(m_u - M) and 1 / sum_u w_u l_u
+  // (2) the partials of this block's columns are independent of the weights:
+  // every warp issues its first units' float4 loads before warp 0 computes the
+  // weights exp(m_u - M) and 1 / sum_u w_u l_u (one dependent round trip)
   const size_t base = ((size_t)b * n_heads + head) * ns;
+  __shared__ float4 part4[4][32];
+  const int r = ranks_v[g];
+  const int col = blockIdx.x * 128 + 4 * lane;
+  const float* src = pctx + base * (size_t)Rv_pad + min(col, Rv_pad - 4);
+  constexpr int PRE = 8;  // units preloaded per warp (4 warps: 32 units)
+  float4 pre[PRE];
+#pragma unroll
+  for (int i = 0; i < PRE; ++i) {
+    const int q = warp + 4 * i;
+    pre[i] = q < nu ? __ldcg(reinterpret_cast<const float4*>(src + (size_t)ulist[q] * Rv_pad))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   if (warp == 0) {
-    float M = -INFINITY;
-    for (int q = lane; q < nu; q += 32) M = fmaxf(M, __ldcg(pm + base + ulist[q]));
+    // units q = lane + 32 k: the first two per lane stay in registers
+    float mv[2] = {-INFINITY, -INFINITY}, lv[2] = {0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = lane + 32 * k;
+      if (q < nu) {
+        mv[k] = __ldcg(pm + base + ulist[q]);
+        lv[k] = __ldcg(pl + base + ulist[q]);
+      }
+    }
+    float M = fmaxf(mv[0], mv[1]);
+    for (int q = lane + 64; q < nu; q += 32) M = fmaxf(M, __ldcg(pm + base + ulist[q]));
     M = warp_reduce(M, [](float x, float y) { return fmaxf(x, y); });
     float Ls = 0.f;
-    for (int q = lane; q < nu; q += 32) {
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+      const int q = lane + 32 * k;
+      if (q < nu) {
+        const float wq = __expf(mv[k] - M);
+        w[q] = wq;
+        Ls += wq * lv[k];
+      }
+    }
+    for (int q = lane + 64; q < nu; q += 32) {
       const float wq = __expf(__ldcg(pm + base + ulist[q]) - M);
       w[q] = wq;
       Ls += wq * __ldcg(pl + base + ulist[q]);
@@ -1358,14 +1391,21 @@ value_merge_kernel(const float* __restrict__ pm, const float* __restrict__ pl,
   }
   __syncthreads();
   // (3) lane = 4 columns of this block's 128; warp w sums units w, w + 4, ...
-  // (8 float4 loads in flight), then the 4 warp sums combine in a fixed order
-  __shared__ float4 part4[4][32];
-  const int r = ranks_v[g];
-  const int col = blockIdx.x * 128 + 4 * lane;
-  const float* src = pctx + base * (size_t)Rv_pad + min(col, Rv_pad - 4);
+  // in unit order, then the 4 warp sums combine in a fixed order
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int i = 0; i < PRE; ++i) {
+    const int q = warp + 4 * i;
+    if (q < nu) {
+      const float wq = w[q];
+      acc.x = fmaf(wq, pre[i].x, acc.x);
+      acc.y = fmaf(wq, pre[i].y, acc.y);
+      acc.z = fmaf(wq, pre[i].z, acc.z);
+      acc.w = fmaf(wq, pre[i].w, acc.w);
+    }
+  }
 #pragma unroll 8
-  for (int q = warp; q < nu; q += 4) {
+  for (int q = warp + 4 * PRE; q < nu; q += 4) {
     const float wq = w[q];
     const float4 v = __ldcg(reinterpret_cast<const float4*>(src + (size_t)ulist[q] * Rv_pad));
     acc.x = fmaf(wq, v.x, acc.x);
