@@ -77,6 +77,20 @@ int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat,
                        const int* t_dev, void* stream);
 
 /*
+ * Both sides of one layer's append (palu_latent_append for keys and values)
+ * in one launch: lat_k / lat_v point at each side's latents inside the same
+ * GEMV output row (row stride ld_lat); quantised sides share one dynamic
+ * shared-memory size.  Same results as two palu_latent_append calls.
+ */
+int palu_latent_append_kv(int dtype, int bits_k, int bits_v, const float* lat_k, const float* lat_v,
+                          int B, int ld_lat, int G_k, int G_v, const int* ranks_k,
+                          const int* lat_off_k, const int* ranks_v, const int* lat_off_v,
+                          void* rows_k, float* scales_k, float* zps_k, double* scales64_k,
+                          int64_t* zps64_k, void* rows_v, float* scales_v, float* zps_v,
+                          double* scales64_v, int64_t* zps64_v, int R_pad_k, int R_pad_v,
+                          int T_cap, const int* t_dev, void* stream);
+
+/*
  * Bit-exact per-token quantiser on fp64 rows (quant.py:87-99): codes (uint8,
  * one per element), scales (fp64) and zero points (int64).  The cache uses
  * the same device function; this entry point exposes it for parity tests.

@@ -32,6 +32,8 @@ SIGNATURES = {
     "palu_device_check": (i32, [i32]),
     "palu_gemv": (i32, [i32, p, i32, i32, p, i32, i32, p, i32, i32, p]),
     "palu_latent_append": (i32, [i32, i32, p, i32, i32, i32, p, p, p, p, p, p, p, i32, i32, p, p]),
+    "palu_latent_append_kv": (i32, [i32, i32, i32, p, p, i32, i32, i32, i32, p, p, p, p,
+                                    p, p, p, p, p, p, p, p, p, p, i32, i32, i32, p, p]),
     "palu_quantize_rows": (i32, [p, i32, i32, i32, p, p, p, p]),
     "palu_pack_rows": (i32, [p, i32, i32, i32, p, p]),
     "palu_query_absorb": (i32, [i32, p, i32, i32, i32, i32, i32, p, i32, i32, p, f32, p, p, i32, p]),

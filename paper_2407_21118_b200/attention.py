@@ -32,6 +32,7 @@ from .model import (AttentionConfig, LayerKV, LayerWeights, ModelWeights, as_arr
                     validate_weights)
 
 FP_BITS = 16
+_APPEND_SPLIT = os.environ.get("PALU_APPEND_SPLIT") == "1"  # A/B diagnostics only
 SUPPORTED_BITS = (2, 3, 4, 8)
 DTYPES = ("float32", "bfloat16")
 
@@ -548,12 +549,22 @@ class _Session:
         qd = L.qdim if L.qdim else d
         _lib.call("palu_gemv", code, _ptr(L.w1), n1, d, _ptr(x), B, d, _ptr(y), self.n1, 0, st)
         yp = y.data_ptr()
-        _lib.call("palu_latent_append", code, K.bits, yp + 4 * qd, B, self.n1, K.G,
-                  _ptr(L.ranks_k_dev), _ptr(L.latoff_k_dev), _ptr(K.rows), _ptr(K.scales),
-                  _ptr(K.zps), _ptr(K.scales64), _ptr(K.zps64), K.r_pad, K.cap, _ptr(self.t_dev), st)
-        _lib.call("palu_latent_append", code, V.bits, yp + 4 * (qd + sk_sum), B, self.n1, V.G,
-                  _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev), _ptr(V.rows), _ptr(V.scales),
-                  _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64), V.r_pad, V.cap, _ptr(self.t_dev), st)
+        # attention.py:343-347 + _GroupStore.append (:248-255), both sides in one launch
+        # (PALU_APPEND_SPLIT=1: one launch per side, for A/B timing)
+        assert K.cap == V.cap
+        if _APPEND_SPLIT:
+            for S, lat, rk, lo in ((K, yp + 4 * qd, L.ranks_k_dev, L.latoff_k_dev),
+                                   (V, yp + 4 * (qd + sk_sum), L.ranks_v_dev, L.latoff_v_dev)):
+                _lib.call("palu_latent_append", code, S.bits, lat, B, self.n1, S.G, _ptr(rk),
+                          _ptr(lo), _ptr(S.rows), _ptr(S.scales), _ptr(S.zps), _ptr(S.scales64),
+                          _ptr(S.zps64), S.r_pad, S.cap, _ptr(self.t_dev), st)
+        else:
+            _lib.call("palu_latent_append_kv", code, K.bits, V.bits, yp + 4 * qd,
+                      yp + 4 * (qd + sk_sum), B, self.n1, K.G, V.G, _ptr(L.ranks_k_dev),
+                      _ptr(L.latoff_k_dev), _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev),
+                      _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), _ptr(K.scales64), _ptr(K.zps64),
+                      _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64),
+                      K.r_pad, V.r_pad, K.cap, _ptr(self.t_dev), st)
         if not self.rope:
             # attention.py:380-388: latent-cache GEMV against q_lat (no reconstruction)
             if self.ls_tc_layers[li]:

@@ -147,18 +147,24 @@ static int gemv_dispatch(const T* W, int N, int K, const float* x, int B, int ld
 // One CTA per (group, batch row).  Quantised sides run quant.py:87-99 in fp64.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void append_raw_kernel(const float* __restrict__ lat, int ld_lat, int G,
-                                  const int* __restrict__ ranks, const int* __restrict__ lat_off,
-                                  T* __restrict__ rows, int R_pad, int T_cap,
-                                  const int* __restrict__ t_dev) {
-  pdl_enter();
-  const int g = blockIdx.x, b = blockIdx.y;
-  const int t = *t_dev;
+__device__ __forceinline__ void append_raw_body(const float* __restrict__ lat, int ld_lat, int G,
+                                                const int* __restrict__ ranks,
+                                                const int* __restrict__ lat_off, T* __restrict__ rows,
+                                                int R_pad, int T_cap, int t, int g, int b) {
   if (t >= T_cap) return;
   const int r = ranks[g];
   const float* src = lat + (size_t)b * ld_lat + lat_off[g];
   T* dst = rows + (((size_t)b * G + g) * T_cap + t) * R_pad;
   for (int c = threadIdx.x; c < R_pad; c += blockDim.x) dst[c] = from_f<T>(c < r ? src[c] : 0.f);
+}
+
+template <typename T>
+__global__ void append_raw_kernel(const float* __restrict__ lat, int ld_lat, int G,
+                                  const int* __restrict__ ranks, const int* __restrict__ lat_off,
+                                  T* __restrict__ rows, int R_pad, int T_cap,
+                                  const int* __restrict__ t_dev) {
+  pdl_enter();
+  append_raw_body<T>(lat, ld_lat, G, ranks, lat_off, rows, R_pad, T_cap, *t_dev, blockIdx.x, blockIdx.y);
 }
 
 // Quantise one row held in shared memory (fp64).  Mirrors quant.py:93-98.
@@ -218,21 +224,19 @@ __device__ void pack_row_dev(const uint8_t* codes, int cols, int bits, uint8_t* 
   }
 }
 
-__global__ void append_quant_kernel(const float* __restrict__ lat, int ld_lat, int G, int bits,
-                                    const int* __restrict__ ranks, const int* __restrict__ lat_off,
-                                    uint8_t* __restrict__ rows, float* __restrict__ scales,
-                                    float* __restrict__ zps, double* __restrict__ scales64,
-                                    int64_t* __restrict__ zps64, int R_pad, int T_cap,
-                                    const int* __restrict__ t_dev) {
-  pdl_enter();
-  extern __shared__ double qsm[];  // [R_pad] values, 64 reduction slots, then codes
+__device__ __forceinline__ void append_quant_body(const float* __restrict__ lat, int ld_lat, int G,
+                                                  int bits, const int* __restrict__ ranks,
+                                                  const int* __restrict__ lat_off,
+                                                  uint8_t* __restrict__ rows, float* __restrict__ scales,
+                                                  float* __restrict__ zps, double* __restrict__ scales64,
+                                                  int64_t* __restrict__ zps64, int R_pad, int T_cap,
+                                                  int t, int g, int b, double* qsm) {
+  // qsm: [R_pad] values, 64 reduction slots, then codes
   double* xrow = qsm;
   double* red = qsm + R_pad;
   uint8_t* codes = reinterpret_cast<uint8_t*>(red + 64);
   __shared__ double s_sh;
   __shared__ int64_t z_sh;
-  const int g = blockIdx.x, b = blockIdx.y;
-  const int t = *t_dev;
   if (t >= T_cap) return;
   const int r = ranks[g];
   const float* src = lat + (size_t)b * ld_lat + lat_off[g];
@@ -249,6 +253,49 @@ __global__ void append_quant_kernel(const float* __restrict__ lat, int ld_lat, i
     if (scales64) scales64[tok] = s_sh;
     if (zps64) zps64[tok] = z_sh;
   }
+}
+
+__global__ void append_quant_kernel(const float* __restrict__ lat, int ld_lat, int G, int bits,
+                                    const int* __restrict__ ranks, const int* __restrict__ lat_off,
+                                    uint8_t* __restrict__ rows, float* __restrict__ scales,
+                                    float* __restrict__ zps, double* __restrict__ scales64,
+                                    int64_t* __restrict__ zps64, int R_pad, int T_cap,
+                                    const int* __restrict__ t_dev) {
+  pdl_enter();
+  extern __shared__ double qsm[];
+  append_quant_body(lat, ld_lat, G, bits, ranks, lat_off, rows, scales, zps, scales64, zps64, R_pad,
+                    T_cap, *t_dev, blockIdx.x, blockIdx.y, qsm);
+}
+
+// Both sides of one layer's append in one launch: blocks [0, G_k) of each
+// batch row append the key latents, [G_k, G_k + G_v) the value latents.
+struct AppendSide {
+  int bits, G, R_pad;
+  const float* lat;  // this side's latents inside the GEMV output
+  const int* ranks;
+  const int* lat_off;
+  void* rows;
+  float *scales, *zps;
+  double* scales64;
+  int64_t* zps64;
+};
+
+template <typename T>
+__global__ void append_kv_kernel(AppendSide k, AppendSide v, int ld_lat, int T_cap,
+                                 const int* __restrict__ t_dev) {
+  pdl_enter();
+  extern __shared__ double qsm[];
+  const bool is_k = (int)blockIdx.x < k.G;
+  const AppendSide& a = is_k ? k : v;
+  const int g = is_k ? (int)blockIdx.x : (int)blockIdx.x - k.G, b = blockIdx.y;
+  const int t = *t_dev;
+  if (a.bits == 16)
+    append_raw_body<T>(a.lat, ld_lat, a.G, a.ranks, a.lat_off, reinterpret_cast<T*>(a.rows), a.R_pad,
+                       T_cap, t, g, b);
+  else
+    append_quant_body(a.lat, ld_lat, a.G, a.bits, a.ranks, a.lat_off,
+                      reinterpret_cast<uint8_t*>(a.rows), a.scales, a.zps, a.scales64, a.zps64,
+                      a.R_pad, T_cap, t, g, b, qsm);
 }
 
 __global__ void quantize_rows_kernel(const double* __restrict__ x, int cols, int bits,
@@ -1244,6 +1291,38 @@ int palu_latent_append(int dtype, int bits, const float* lat, int B, int ld_lat,
   PALU_CK(launch_k(append_quant_kernel, dim3(grid), dim3(128), smem, S(stream), lat, ld_lat, G, bits, ranks, lat_off,
                                                       (uint8_t*)rows, scales, zps, scales64, zps64,
                                                       R_pad, T_cap, t_dev));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_latent_append_kv(int dtype, int bits_k, int bits_v, const float* lat_k, const float* lat_v,
+                          int B, int ld_lat, int G_k, int G_v, const int* ranks_k,
+                          const int* lat_off_k, const int* ranks_v, const int* lat_off_v,
+                          void* rows_k, float* scales_k, float* zps_k, double* scales64_k,
+                          int64_t* zps64_k, void* rows_v, float* scales_v, float* zps_v,
+                          double* scales64_v, int64_t* zps64_v, int R_pad_k, int R_pad_v,
+                          int T_cap, const int* t_dev, void* stream) {
+  PALU_REQUIRE(B > 0 && G_k > 0 && G_v > 0 && R_pad_k > 0 && R_pad_v > 0 && T_cap > 0,
+               "palu_latent_append_kv: bad sizes");
+  size_t smem = 0;
+  for (int side = 0; side < 2; ++side) {
+    const int bits = side ? bits_v : bits_k, R_pad = side ? R_pad_v : R_pad_k;
+    if (bits == 16) continue;
+    PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+                 "bits must be one of (2, 3, 4, 8), got %d", bits);
+    PALU_REQUIRE(R_pad % 32 == 0, "quantised rows need R_pad %% 32 == 0 (got %d)", R_pad);
+    const size_t need = (size_t)(R_pad + 64) * sizeof(double) + R_pad;
+    if (need > smem) smem = need;
+  }
+  const AppendSide k{bits_k, G_k, R_pad_k, lat_k, ranks_k, lat_off_k, rows_k,
+                     scales_k, zps_k, scales64_k, zps64_k};
+  const AppendSide v{bits_v, G_v, R_pad_v, lat_v, ranks_v, lat_off_v, rows_v,
+                     scales_v, zps_v, scales64_v, zps64_v};
+  const dim3 grid(G_k + G_v, B);
+  if (dtype == PALU_DTYPE_BF16)
+    PALU_CK(launch_k(append_kv_kernel<bf16>, grid, dim3(128), smem, S(stream), k, v, ld_lat, T_cap, t_dev));
+  else
+    PALU_CK(launch_k(append_kv_kernel<float>, grid, dim3(128), smem, S(stream), k, v, ld_lat, T_cap, t_dev));
   PALU_LAUNCHED();
   return PALU_OK;
 }
