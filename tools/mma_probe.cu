@@ -120,6 +120,20 @@ __global__ void __launch_bounds__(320, 1) mma_probe(int iters, float* sink, int 
                   (int)(((blockIdx.x * 28331u + (unsigned)i) * 128u) % (1u << 22)));
     }
   }
+  if (warp >= 2 && (extra & 512)) {
+    // 8 warps stream a 16 KB L1-resident table with 16-B __ldg loads (the
+    // score epilogue's cos/sin base rows) while the MMAs run
+    const float4* tab = reinterpret_cast<const float4*>(sink + 64);
+    float acc = 0.f;
+    for (int i = 0; *stop == 0 && i < 10000000; ++i) {
+      float4 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldg(tab + ((threadIdx.x + 256 * k + i * 8) & 1023));
+#pragma unroll
+      for (int k = 0; k < 8; ++k) acc += v[k].x * v[k].y + v[k].z * v[k].w;
+    }
+    if (acc == 12345.f) sink[1] = acc;
+  }
   if (warp >= 2 && (extra & 2)) {
     // 8 warps read the other TMEM slot like the score epilogue (2 x 16 columns, wait, FMAs)
     float v[16], w[16], acc = 0.f;
@@ -168,7 +182,8 @@ void run(const char* name) {
   cfg.attrs = &attr;
   cfg.numAttrs = 1;
   float* sink;
-  cudaMalloc(&sink, 256);
+  cudaMalloc(&sink, 64 * 1024);
+  cudaMemset(sink, 0, 64 * 1024);
   const int iters = getenv("ITERS") ? atoi(getenv("ITERS")) : 4000;
   cudaLaunchKernelEx(&cfg, k, iters, sink, g_extra, g_map);
   cudaEvent_t a, b;
@@ -202,7 +217,7 @@ int main() {
   ((EncodeFn)fp)(&g_map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, buf, dims, strides, box, es,
                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  for (int e : {0, 128, 256, 384, 416}) {
+  for (int e : {0, 512, 16, 528}) {
     g_extra = e;
     run<256, 256, 2>("cta2 M256 N256 K16");
     run<128, 256, 1>("cta1 M128 N256 K16");
