@@ -1804,7 +1804,10 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.score_pairs = (sms & ~1) / 2;
   prm.ready = nullptr;
   prm.mode = getenv("PALU_TC_PROFILE_MODE") ? atoi(getenv("PALU_TC_PROFILE_MODE")) : 0;
-  prm.pf_dist = getenv("PALU_TC_PF") ? atoi(getenv("PALU_TC_PF")) : PF_DIST;
+  // packed keys: the converter warps read code rows with plain loads, which
+  // the L2 prefetch 3 items ahead still helps (-0.5 % step, int4); raw keys
+  // stream through TMA and do better without it (tools/pf_sweep.sh)
+  prm.pf_dist = getenv("PALU_TC_PF") ? atoi(getenv("PALU_TC_PF")) : (bits == 16 ? PF_DIST : 3);
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
   prm.t_dev = t_dev;
   prm.logits = logits;
