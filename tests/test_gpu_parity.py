@@ -416,3 +416,53 @@ def test_head_group_shards_sum_to_full_step(P, world, rope):
         torch.cuda.synchronize()
         acc += ses.x.double().cpu().numpy()
     assert rel_err(acc, want) < 1e-4
+
+
+@pytest.mark.parametrize("bits_k,bits_v", [(16, 16), (4, 4), (16, 4), (3, 8), (2, 16)])
+def test_append_kv_equals_two_appends(P, bits_k, bits_v):
+    """palu_latent_append_kv (one launch for both sides) writes exactly what
+    two palu_latent_append calls write: rows, scales, zero points (bit-equal)."""
+    import torch
+    from paper_2407_21118_b200 import _lib
+    dev = torch.device("cuda")
+    B, T_cap, t = 2, 256, 37
+    G_k, G_v, R_k, R_v = 8, 4, 256, 384
+    g = torch.Generator(device="cpu").manual_seed(11)
+    rk = torch.randint(R_k // 2, R_k + 1, (G_k,), generator=g, dtype=torch.int32)
+    rv = torch.randint(R_v // 2, R_v + 1, (G_v,), generator=g, dtype=torch.int32)
+    off_k = torch.cat([torch.zeros(1, dtype=torch.int32), rk.cumsum(0)[:-1].int()])
+    off_v = torch.cat([torch.zeros(1, dtype=torch.int32), rv.cumsum(0)[:-1].int()])
+    ld = int(rk.sum() + rv.sum()) + 8
+    lat = (torch.randn(B, ld, generator=g) * 0.7).to(dev)
+    t_dev = torch.tensor([t], dtype=torch.int32, device=dev)
+    rk_d, rv_d, ok_d, ov_d = (x.to(dev) for x in (rk, rv, off_k, off_v))
+
+    def store(bits, G, R):
+        shape = (B, G, T_cap)
+        rows = (torch.zeros(shape + (R,), dtype=torch.bfloat16, device=dev) if bits == 16 else
+                torch.zeros(shape + (R * bits // 8,), dtype=torch.uint8, device=dev))
+        return dict(rows=rows, s=torch.zeros(shape, device=dev), z=torch.zeros(shape, device=dev),
+                    s64=torch.zeros(shape, dtype=torch.float64, device=dev),
+                    z64=torch.zeros(shape, dtype=torch.int64, device=dev))
+
+    p = lambda x: x.data_ptr()
+    a_k, a_v, b_k, b_v = store(bits_k, G_k, R_k), store(bits_v, G_v, R_v), store(bits_k, G_k, R_k), \
+        store(bits_v, G_v, R_v)
+    code = 1  # PALU_DTYPE_BF16
+    lat_v_ptr = p(lat) + 4 * int(rk.sum())
+    _lib.call("palu_latent_append", code, bits_k, p(lat), B, ld, G_k, p(rk_d), p(ok_d),
+              p(a_k["rows"]), p(a_k["s"]), p(a_k["z"]), p(a_k["s64"]), p(a_k["z64"]), R_k, T_cap,
+              p(t_dev), None)
+    _lib.call("palu_latent_append", code, bits_v, lat_v_ptr, B, ld, G_v, p(rv_d), p(ov_d),
+              p(a_v["rows"]), p(a_v["s"]), p(a_v["z"]), p(a_v["s64"]), p(a_v["z64"]), R_v, T_cap,
+              p(t_dev), None)
+    _lib.call("palu_latent_append_kv", code, bits_k, bits_v, p(lat), lat_v_ptr, B, ld, G_k, G_v,
+              p(rk_d), p(ok_d), p(rv_d), p(ov_d), p(b_k["rows"]), p(b_k["s"]), p(b_k["z"]),
+              p(b_k["s64"]), p(b_k["z64"]), p(b_v["rows"]), p(b_v["s"]), p(b_v["z"]),
+              p(b_v["s64"]), p(b_v["z64"]), R_k, R_v, T_cap, p(t_dev), None)
+    torch.cuda.synchronize()
+    for a, b in ((a_k, b_k), (a_v, b_v)):
+        for key in a:
+            assert torch.equal(a[key].view(torch.uint8) if a[key].dtype == torch.bfloat16 else a[key],
+                               b[key].view(torch.uint8) if b[key].dtype == torch.bfloat16 else b[key]), key
+        assert a["rows"].abs().sum() > 0 if a["rows"].dtype != torch.uint8 else a["rows"].any()
