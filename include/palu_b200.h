@@ -91,6 +91,15 @@ int palu_latent_append_kv(int dtype, int bits_k, int bits_v, const float* lat_k,
                           int T_cap, const int* t_dev, void* stream);
 
 /*
+ * Container export of one group's quantised latents (pipeline.py:513-531):
+ * pack_codes (quant.py:156-169) of the first `rank` codes of T stored rows
+ * (row_bytes apart, as palu_latent_append writes them) into one LSB-first
+ * bitstream of out_bytes = ceil(T * rank * bits / 8) bytes.
+ */
+int palu_pack_code_stream(int bits, const void* rows, int row_bytes, int rank, int T, void* out,
+                          long long out_bytes, void* stream);
+
+/*
  * Bit-exact per-token quantiser on fp64 rows (quant.py:87-99): codes (uint8,
  * one per element), scales (fp64) and zero points (int64).  The cache uses
  * the same device function; this entry point exposes it for parity tests.

@@ -20,6 +20,8 @@ from .attention import (
     palu_prefill,
     rope_apply,
 )
+from . import container
+from .container import export_latents
 from .dense import DecodeResult, DenseModel, reference_decode
 from .errors import GoldenMismatchError, NumericalError, PaluError, ValidationError
 from .model import (

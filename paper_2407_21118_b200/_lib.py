@@ -34,6 +34,7 @@ SIGNATURES = {
     "palu_latent_append": (i32, [i32, i32, p, i32, i32, i32, p, p, p, p, p, p, p, i32, i32, p, p]),
     "palu_latent_append_kv": (i32, [i32, i32, i32, p, p, i32, i32, i32, i32, p, p, p, p,
                                     p, p, p, p, p, p, p, p, p, p, i32, i32, i32, p, p]),
+    "palu_pack_code_stream": (i32, [i32, p, i32, i32, i32, p, i64, p]),
     "palu_quantize_rows": (i32, [p, i32, i32, i32, p, p, p, p]),
     "palu_pack_rows": (i32, [p, i32, i32, i32, p, p]),
     "palu_query_absorb": (i32, [i32, p, i32, i32, i32, i32, i32, p, i32, i32, p, f32, p, p, i32, p]),

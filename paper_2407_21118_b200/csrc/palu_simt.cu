@@ -1327,6 +1327,51 @@ int palu_latent_append_kv(int dtype, int bits_k, int bits_v, const float* lat_k,
   return PALU_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Container export (quant.py:156-169 pack_codes over a cache's stored rows):
+// the first `rank` codes of each padded row, concatenated over T rows, as one
+// LSB-first bitstream (code i at bits [i b, (i + 1) b)).  Thread = output byte.
+// ---------------------------------------------------------------------------
+__global__ void pack_stream_kernel(const uint8_t* __restrict__ rows, int row_bytes, int rank, int T,
+                                   int bits, uint8_t* __restrict__ out, long long out_bytes) {
+  pdl_enter();
+  const long long n_codes = (long long)T * rank;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < out_bytes;
+       j += (long long)gridDim.x * blockDim.x) {
+    uint32_t byte = 0;
+    for (int p = 0; p < 8; ++p) {
+      const long long pos = 8 * j + p;
+      const long long i = pos / bits;
+      if (i >= n_codes) break;
+      const int bit = (int)(pos - i * bits);
+      const long long t = i / rank;
+      const long long rb = (i - t * rank) * bits + bit;  // bit inside the stored row
+      const uint32_t v = rows[t * row_bytes + (rb >> 3)];
+      byte |= ((v >> (rb & 7)) & 1u) << p;
+    }
+    out[j] = (uint8_t)byte;
+  }
+}
+
+int palu_pack_code_stream(int bits, const void* rows, int row_bytes, int rank, int T, void* out,
+                          long long out_bytes, void* stream) {
+  PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+               "palu_pack_code_stream: bits must be one of (2, 3, 4, 8), got %d", bits);
+  PALU_REQUIRE(rank >= 0 && T >= 0 && (long long)rank * bits <= 8LL * row_bytes,
+               "palu_pack_code_stream: rank %d does not fit rows of %d bytes", rank, row_bytes);
+  const long long need = ((long long)T * rank * bits + 7) / 8;
+  PALU_REQUIRE(out_bytes == need, "palu_pack_code_stream: out_bytes %lld, expected %lld", out_bytes,
+               need);
+  if (need == 0) return PALU_OK;
+  const int threads = 256;
+  const long long blocks = (need + threads - 1) / threads;
+  PALU_CK(launch_k(pack_stream_kernel, dim3((unsigned)(blocks < 4096 ? blocks : 4096)),
+                   dim3(threads), 0, S(stream), (const uint8_t*)rows, row_bytes, rank, T, bits,
+                   (uint8_t*)out, out_bytes));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
 int palu_quantize_rows(const double* x, int rows, int cols, int bits, uint8_t* codes,
                        double* scales, int64_t* zps, void* stream) {
   PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
