@@ -413,10 +413,10 @@ class LatentKVCache:
 
 
 def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
+    """attention.py:334-340."""
     if fused.config is not None and fused.config.rope != cache.config.rope:
         raise ValidationError("fused weights were built for rope="
                               f"{fused.config.rope}, the cache config has rope={cache.config.rope}")
-    """attention.py:334-340."""
     if len(fused.layers) != len(cache._stores):
         raise ValidationError("cache and fused weights disagree on layer count")
     for li, lf in enumerate(fused.layers):
@@ -425,6 +425,23 @@ def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
             raise ValidationError(f"cache/fused rank mismatch at layer {li}")
     if fused.dtype != cache.dtype:
         raise ValidationError(f"cache dtype {cache.dtype} != fused weights dtype {fused.dtype}")
+
+
+# The (weights, fused, cache) triple validated by the last decode step: shapes
+# and ranks of these objects cannot change, so repeated steps skip the
+# per-layer checks (~50 us of Python per 32-layer step).  Only the most recent
+# triple is held, so no other objects are kept alive.
+_LAST_VALID: tuple = ()
+
+
+def _validate_step(weights, fused, cache) -> None:
+    global _LAST_VALID
+    if (len(_LAST_VALID) == 3 and _LAST_VALID[0] is weights and _LAST_VALID[1] is fused
+            and _LAST_VALID[2] is cache):
+        return
+    _check_cache_fused(cache, fused)
+    validate_weights(weights, cache.config)
+    _LAST_VALID = (weights, fused, cache)
 
 
 # ---------------------------------------------------------------------------
@@ -727,8 +744,7 @@ def palu_decode_step_rope(weights, fused: FusedWeights, cache: LatentKVCache, x_
         raise ValidationError("palu_decode_step_rope requires a rope-on config")
     if tile_len is not None and tile_len < 1:
         raise ValidationError(f"tile_len must be >= 1, got {tile_len}")
-    _check_cache_fused(cache, fused)
-    validate_weights(weights, cfg)
+    _validate_step(weights, fused, cache)
     x = _validate_x(x_t, cache)
     torch = _torch()
     cache.reserve(cache.t + 1)
@@ -754,8 +770,7 @@ def palu_decode_step_norope(weights, fused: FusedWeights, cache: LatentKVCache, 
     cfg = cache.config
     if cfg.rope:
         raise ValidationError("palu_decode_step_norope requires a rope-off config")
-    _check_cache_fused(cache, fused)
-    validate_weights(weights, cfg)
+    _validate_step(weights, fused, cache)
     x = _validate_x(x_t, cache)
     torch = _torch()
     cache.reserve(cache.t + 1)
