@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--context", type=int, default=65536)
     ap.add_argument("--rank-k", type=int, default=256)
     ap.add_argument("--rank-v", type=int, default=256)
+    ap.add_argument("--zero-keys", action="store_true", help="zero the key latents (data-power test)")
     a = ap.parse_args()
     import torch
 
@@ -32,6 +33,9 @@ def main():
     _lib.load()
     w, f, c = synthetic_engine(layers=1, batch=1, context=a.context, extra=64, rank_k=a.rank_k,
                                rank_v=a.rank_v)
+    if a.zero_keys:
+        for K, _ in c._stores:
+            K.rows.zero_()
     s = _session(f, c, score_kernel="tcgen05")
     s.x.normal_(0, 0.5)
     for _ in range(3):
