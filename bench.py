@@ -75,26 +75,33 @@ def _peaks():
 # ---------------------------------------------------------------------------
 # CPU baseline: the oracle port of palu_decode_step_rope (reference algorithm)
 # ---------------------------------------------------------------------------
-def cpu_layer_step_seconds(T: int, reps: int = 2, seed: int = 11):
-    """Best-of-reps seconds for one Llama-2-7B-layer RoPE decode step at T
-    cached tokens, run by the numpy oracle (attention.py:392-448 restated),
-    with all host threads available to BLAS."""
+def cpu_layer_step_seconds(T: int, reps: int = 2, seed: int = 11, rank_k: int = RANK,
+                           rank_v: int = RANK, rope: bool = True):
+    """Best-of-reps seconds for one Llama-2-7B-layer decode step at T cached
+    tokens, run by the numpy oracle (attention.py:392-448, or :365-389 with
+    rope off, restated), with all host threads available to BLAS."""
     import numpy as np
 
     from oracle import palu_oracle as po
 
     rng = np.random.default_rng(seed)
-    L = po.synth_layer(D, NH, DH, GS, RANK, GS, RANK, seed=seed)
+    L = po.synth_layer(D, NH, DH, GS, rank_k, GS, rank_v, seed=seed)
     cache = po.OracleCache([L], bits=16)
-    for st in cache.k_stores[0] + cache.v_stores[0]:
-        st.extend(rng.standard_normal((T, RANK)) / 3.0)
+    for st in cache.k_stores[0]:
+        st.extend(rng.standard_normal((T, rank_k)) / 3.0)
+    for st in cache.v_stores[0]:
+        st.extend(rng.standard_normal((T, rank_v)) / 3.0)
     cache.t = T
     wo_f = [po.build_wo_fused(L, NH, DH)]
+    wq_f = [po.build_wq_fused(L, NH, DH)] if not rope else None
     x = po.random_matrix(1, D, seed + 1)[0]
     best = float("inf")
     for _ in range(reps):
         t0 = time.perf_counter()
-        po.decode_step_rope([L], wo_f, cache, x, NH, DH, 10000.0)
+        if rope:
+            po.decode_step_rope([L], wo_f, cache, x, NH, DH, 10000.0)
+        else:
+            po.decode_step_norope([L], wq_f, wo_f, cache, x, NH, DH)
         best = min(best, time.perf_counter() - t0)
         for st in cache.k_stores[0] + cache.v_stores[0]:
             st.truncate(T)
@@ -102,20 +109,35 @@ def cpu_layer_step_seconds(T: int, reps: int = 2, seed: int = 11):
     return best
 
 
-def cpu_baseline(context: int, layers: int, batch: int, t_small=1024, t_big=4096):
+def cpu_baseline(args, t_small=1024, t_big=4096):
     """Fit a + b*T on two bounded samples, extrapolate to the workload."""
-    s1 = cpu_layer_step_seconds(t_small)
-    s2 = cpu_layer_step_seconds(t_big)
+    kw = dict(rank_k=args.rank_k, rank_v=args.rank_v, rope=args.rope == "on")
+    s1 = cpu_layer_step_seconds(t_small, **kw)
+    s2 = cpu_layer_step_seconds(t_big, **kw)
     b = (s2 - s1) / (t_big - t_small)
     a = s1 - b * t_small
-    per_layer = a + b * (context + 1)
-    us = per_layer * layers * batch * 1e6
+    per_layer = a + b * (args.context + 1)
+    us = per_layer * args.layers * args.batch * 1e6
+    step = "palu_decode_step_rope" if args.rope == "on" else "palu_decode_step_norope"
     return {
         "value": us, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
-        "sample": (f"oracle palu_decode_step_rope, one Llama-2-7B layer (gs4 r256 fp64), best of 2 at "
-                   f"T={t_small} ({s1 * 1e3:.0f} ms) and T={t_big} ({s2 * 1e3:.0f} ms); linear fit "
-                   f"extrapolated to T={context} x {layers} layers x batch {batch}"),
+        "sample": (f"oracle {step}, one Llama-2-7B layer (gs4 r_k {args.rank_k} r_v {args.rank_v} "
+                   f"fp64), best of 2 at T={t_small} ({s1 * 1e3:.0f} ms) and T={t_big} "
+                   f"({s2 * 1e3:.0f} ms); linear fit extrapolated to T={args.context} x "
+                   f"{args.layers} layers x batch {args.batch}"),
     }
+
+
+def workload_config(args, world: int, heads: bool) -> dict:
+    """The `config` of the bench line (shared by both arms)."""
+    return {"workload": (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
+                         + ("rope" if args.rope == "on" else "norope")),
+            "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
+            "batch_per_gpu": args.batch,
+            "global_batch": args.batch if heads else args.batch * world,
+            "layers": args.layers, "bits": args.bits, "rope_base": args.rope_base,
+            "parallelism": (f"heads{world}" if heads else f"replicas{world}"),
+            "l2": "inputs larger than L2 (latent cache 17 GB/step)"}
 
 
 # ---------------------------------------------------------------------------
@@ -267,23 +289,26 @@ def run_reference(args):
         return
     K, W = args.steps, args.warmup
     T_s = 2048
+    kw = dict(rank_k=args.rank_k, rank_v=args.rank_v, rope=args.rope == "on")
     per = []
     for i in range(W + K):
-        s = cpu_layer_step_seconds(T_s, reps=1, seed=11 + (i % 2))
+        s = cpu_layer_step_seconds(T_s, reps=1, seed=11 + (i % 2), **kw)
         if i >= W:
             per.append(s)
-    s_small = cpu_layer_step_seconds(512, reps=1)
+    s_small = cpu_layer_step_seconds(512, reps=1, **kw)
     b = (statistics.median(per) - s_small) / (T_s - 512)
     a = s_small - b * 512
     us = (a + b * (args.context + 1)) * args.layers * args.batch * 1e6
-    sample = (f"oracle port of palu_decode_step_rope (numpy fp64, {os.cpu_count()} host threads): "
+    step = "palu_decode_step_rope" if args.rope == "on" else "palu_decode_step_norope"
+    sample = (f"oracle port of {step} (numpy fp64, {os.cpu_count()} host threads): "
               f"each step = one Llama-2-7B layer at T={T_s}; linear fit with T=512 extrapolated to "
               f"T={args.context} x {args.layers} layers x batch {args.batch}")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {"metric": METRIC, "value": us, "unit": "us/step", "impl": "reference", "n_gpus": args.gpus,
             "steps": K, "warmup": W, "ms_per_step": us / 1e3, "higher_is_better": False,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "llama2-7b-32L-palu50-gs4-r256-rope", "context": args.context,
-                       "batch_per_gpu": args.batch, "layers": args.layers},
+            "scaling": "strong" if args.shard == "heads" else "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, world, args.shard == "heads"),
             "cpu_baseline": {"value": us, "unit": "us/step", "cores": os.cpu_count(), "kind": "port",
                              "sample": sample},
             "e2e": {"value": us, "unit": "us/step", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -450,7 +475,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(args.context, args.layers, args.batch)
+        cpu = cpu_baseline(args)
 
     if rank == 0:
         launches_per_step = sum(len(v) for v in prof.values())
@@ -460,14 +485,7 @@ def main():
             "scaling": "strong" if heads else "weak",
             "vs_baseline": None, "dtype": "bf16" if args.dtype == "bfloat16" else "f32",
             "data": "synthetic (random-init weights, N(0,1/9) latent cache rows)",
-            "config": {"workload": (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
-                                    + ("rope" if args.rope == "on" else "norope")),
-                       "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
-                       "batch_per_gpu": args.batch,
-                       "global_batch": args.batch if heads else args.batch * world,
-                       "layers": args.layers, "bits": args.bits, "rope_base": args.rope_base,
-                       "parallelism": (f"heads{world}" if heads else f"replicas{world}"),
-                       "l2": "inputs larger than L2 (latent cache 17 GB/step)"},
+            "config": workload_config(args, world, heads),
             "tokens_per_s": (args.batch if heads else args.batch * world) / (ms * 1e-3),
             "gpu_launches": launches_per_step * K,
             "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
