@@ -300,7 +300,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           }
         }
       pdl_wait();
-      int cur = -1, nloads = 0, kc = 0, it = 0;
+      int cur = -1, nloads = 0, it = 0, pst = 0, pph = 0;
       for (int i = i0; i < i1; ++i, ++it) {
         const int bg = i / n_super, st = i - bg * n_super;
         if (bg != cur) {
@@ -328,11 +328,14 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           }
         }
         if (p.bits != 16) continue;  // the converter warps fill the H stages
-        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
-          const int stage = kc % p.stages;
-          mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
-          if (leader) mbar_expect_tx(&full[stage], 2 * H_STAGE_BYTES);
-          tma_load_2d_pair(&map_h, &full[stage], s_h + stage * H_STAGE_BYTES, kb * KB, h_row);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          mbar_wait(&empty[pst], pph ^ 1);
+          if (leader) mbar_expect_tx(&full[pst], 2 * H_STAGE_BYTES);
+          tma_load_2d_pair(&map_h, &full[pst], s_h + pst * H_STAGE_BYTES, kb * KB, h_row);
+          if (++pst == p.stages) {
+            pst = 0;
+            pph ^= 1;
+          }
         }
       }
     }
@@ -341,7 +344,11 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       // ---------------- MMA issuer (leader SM issues for the pair) ----------------
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
-      int cur = -1, nloads = 0, kc = 0, unit = 0;
+      int cur = -1, nloads = 0, unit = 0;
+      // stage ring position of the item's first k-block, kept incrementally:
+      // a runtime modulo per k-block is an integer-division chain (~100
+      // dependent clocks) that the shallow MMA queue cannot hide
+      int st0 = 0, ph0 = 0;
       const unsigned long long c_start = clock64(), g_start = gtimer();
       for (int i = i0; i < i1; ++i) {
         const int bg = i / n_super;
@@ -360,10 +367,13 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 4 * unit] = gtimer();
           const uint32_t d_tmem = tmem_base + slot * N_CTA;
           for (int kb = 0; kb < kblocks; ++kb) {
-            const int cnt = kc + kb;
-            const int stage = cnt % p.stages;
+            int stage = st0 + kb, par = ph0;
+            if (stage >= p.stages) {  // kblocks <= stages: at most one wrap
+              stage -= p.stages;
+              par ^= 1;
+            }
             if (h == 0 && (p.mode & 2) == 0) {
-              mbar_wait(&full[stage], (cnt / p.stages) & 1);
+              mbar_wait(&full[stage], par);
               fence_after();
             }
             // profile modes 8 / 16 (diagnostics): pin the A / B operand tile
@@ -378,7 +388,11 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE)
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = gtimer();
         }
-        kc += kblocks;
+        st0 += kblocks;
+        if (st0 >= p.stages) {
+          st0 -= p.stages;
+          ph0 ^= 1;
+        }
       }
       if (p.trace != nullptr && p.ready == nullptr) {  // SM clocks vs wall time of the issue loop
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 508] = clock64() - c_start;
