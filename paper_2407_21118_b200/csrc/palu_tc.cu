@@ -75,10 +75,23 @@ constexpr int CODE_BIAS = 128;   // bits <= 4: bf16(128 + c) has bit pattern 0x4
 // bf16x2 (exact when |z| <= 128), else c - z goes through fp32 and one bf16
 // rounding; the epilogue multiplies by s.  quant.py:156-169 bit order (code
 // k at bits [k b, (k + 1) b)).
+// Position in an n-deep mbarrier ring (slot, phase parity), advanced
+// incrementally: a runtime modulo per step is an integer-division chain
+// (~100 dependent clocks) on the issuing thread.
+struct Ring {
+  int slot = 0, phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+};
+
 template <int BITS, class PP>
 __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t* full,
                                              uint64_t* empty, int bg, int tile, int T_rows,
-                                             int kblocks, int cl, int& kc) {
+                                             int kblocks, int cl, Ring& rg) {
   constexpr int NW = BITS;  // 8-byte words per row per 64-code k-block
   const int lane = threadIdx.x & 31;
   const uint8_t* rowp[2];
@@ -109,14 +122,14 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
                              : make_uint4(0u, 0u, 0u, 0u);
     };
     load4(0);
-    for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+    for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
         for (int q = 0; q < NV; ++q) cu[rr][q] = nx[rr][q];
       if (kb + 1 < kblocks) load4(kb + 1);
-      const int stage = kc % p.stages;
-      mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
+      const int stage = rg.slot;
+      mbar_wait(&empty[stage], rg.phase ^ 1);
       uint8_t* sb = s_h + stage * H_STAGE_BYTES;
 #pragma unroll
       for (int rr = 0; rr < 2; ++rr) {
@@ -170,14 +183,14 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
                             : 0ull;
   };
   load(0);
-  for (int kb = 0; kb < kblocks; ++kb, ++kc) {
+  for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr)
 #pragma unroll
       for (int q = 0; q < NW; ++q) cur[rr][q] = nxt[rr][q];
     if (kb + 1 < kblocks) load(kb + 1);
-    const int stage = kc % p.stages;
-    mbar_wait(&empty[stage], ((kc / p.stages) & 1) ^ 1);
+    const int stage = rg.slot;
+    mbar_wait(&empty[stage], rg.phase ^ 1);
     uint8_t* sb = s_h + stage * H_STAGE_BYTES;
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
@@ -404,15 +417,15 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     // ---------------- quantised keys: converter warps (both SMs) ----------------
     if (p.bits != 16) {
       const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // rows cl, cl + 64 of the SM's tile
-      int kc = 0;
+      Ring rg;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / n_super, st = i - bg * n_super;
         const int tile = 2 * st + (int)rank;
         switch (p.bits) {
-          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
         }
       }
     }
@@ -1539,12 +1552,12 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
   const uint32_t tmem = *tslot;
   if (warp == 0) {
     if (lane == 0 && p.bits == 16) {
-      int kc = 0;
+      Ring rg;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile, tile = i - bg * ntile;
-        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
-          const int st = kc % p.stages;
-          mbar_wait(&empty[st], ((kc / p.stages) & 1) ^ 1);
+        for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
+          const int st = rg.slot;
+          mbar_wait(&empty[st], rg.phase ^ 1);
           mbar_expect_tx(&full[st], H_STAGE_BYTES);
           tma_load_2d(&map_h, &full[st], s_h + st * H_STAGE_BYTES, kb * KB,
                       bg * p.T_cap + tile * TILE_M);
@@ -1555,20 +1568,21 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
     // quantised keys: converter warps (rows cl, cl + 64 of each 128-token tile)
     if (p.bits != 16) {
       const int cl = (warp - 6) * 32 + lane;
-      int kc = 0;
+      Ring rg;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile, tile = i - bg * ntile;
         switch (p.bits) {
-          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
-          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, kc); break;
+          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      int kc = 0, seg = -1, cur = -1;
+      int seg = -1, cur = -1;
+      Ring rg;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile;
         if (bg != cur) {
@@ -1582,9 +1596,9 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
         if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
         fence_after();
         const uint32_t q0 = smem_u32(s_q + (seg & 1) * QB);
-        for (int kb = 0; kb < kblocks; ++kb, ++kc) {
-          const int st = kc % p.stages;
-          mbar_wait(&full[st], (kc / p.stages) & 1);
+        for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
+          const int st = rg.slot;
+          mbar_wait(&full[st], rg.phase);
           fence_after();
           const uint32_t a0 = smem_u32(s_h + st * H_STAGE_BYTES);
 #pragma unroll
