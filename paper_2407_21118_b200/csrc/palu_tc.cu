@@ -795,11 +795,12 @@ __device__ __forceinline__ void value_converter_ring(VStageIter sit, uint8_t* ra
   const int row = cl / split, slab = split == 2 ? (cl & 1) : -1;
   VStage g;
   int k = 0;
+  Ring rr_, rs_;  // raw-code ring, operand ring
   const bool tr = trace != nullptr && cl == 0;
   while (sit.next(g)) {
-    const int rs = k % nslots, st = k % vs;
+    const int rs = rr_.slot, st = rs_.slot;
     if (tr && 3 * k + 302 < TRACE_STRIDE) trace[300 + 3 * k] = gtimer();
-    mbar_wait(&rfull[rs], (k / nslots) & 1);
+    mbar_wait(&rfull[rs], rr_.phase);
     if (tr && 3 * k + 302 < TRACE_STRIDE) trace[301 + 3 * k] = gtimer();
     const uint8_t* slot = raw + rs * (RB + TILE_M * 4);
     VCodes<BITS, 1> c;
@@ -810,7 +811,7 @@ __device__ __forceinline__ void value_converter_ring(VStageIter sit, uint8_t* ra
                       ? lds128(a + 16 * q)
                       : make_uint4(0u, 0u, 0u, 0u);
     c.z[0] = reinterpret_cast<const float*>(slot + RB)[row];
-    mbar_wait(&empty[st], ((k / vs) & 1) ^ 1);
+    mbar_wait(&empty[st], rs_.phase ^ 1);
     if (tr && 3 * k + 302 < TRACE_STRIDE) trace[302 + 3 * k] = gtimer();
     convert_v_codes<BITS, 1>(c, row, ring + st * V_STAGE, slab);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -820,6 +821,8 @@ __device__ __forceinline__ void value_converter_ring(VStageIter sit, uint8_t* ra
       mbar_arrive(&rempty[rs]);
     }
     ++k;
+    rr_.next(nslots);
+    rs_.next(vs);
   }
 }
 
@@ -835,15 +838,15 @@ __device__ __forceinline__ void value_converter(const VParams& vp, int T_cap, Ne
   next_stage(g1);
   load_v_codes<BITS, RPL>(vp, T_cap, g0, cl, b0);
   load_v_codes<BITS, RPL>(vp, T_cap, g1, cl, b1);
-  int ctr = 0;
+  Ring rg;
   auto emit = [&](const VCodes<BITS, RPL>& b) {
-    const int st = ctr % vs;
-    mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
+    const int st = rg.slot;
+    mbar_wait(&empty[st], rg.phase ^ 1);
     convert_v_codes<BITS, RPL>(b, cl, ring + st * V_STAGE);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0) mbar_arrive(&full[st]);
-    ++ctr;
+    rg.next(vs);
   };
   while (g0.bg >= 0) {
     emit(b0);
@@ -987,17 +990,17 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       const int RB = TILE_M * 16 * vp.bits;
       VStageIter sit(it, T_rows, NJ);
       VStage g;
-      int k = 0;
+      Ring rg;
       while (sit.next(g)) {
-        const int rs = k % nslots;
-        mbar_wait(&rempty[rs], ((k / nslots) & 1) ^ 1);
+        const int rs = rg.slot;
+        mbar_wait(&rempty[rs], rg.phase ^ 1);
         mbar_expect_tx(&rfull[rs], RB + TILE_M * 4);
         uint8_t* slot = raw + rs * (RB + TILE_M * 4);
         tma_load_2d(&map_v, &rfull[rs], slot, g.j * 16 * vp.bits, g.bg * p.T_cap + g.t0);
         // T_cap is a multiple of 128 (LatentKVCache): the tile's zero points are
         // 512 aligned bytes inside this sequence/group's row range
         bulk_load(slot + RB, vp.zps + (size_t)g.bg * p.T_cap + g.t0, TILE_M * 4, &rfull[rs]);
-        ++k;
+        rg.next(nslots);
       }
     }
     return;
@@ -1008,12 +1011,13 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     if (lane == 0 && vp.bits == 16) {
       prefetch_map(&map_v);
       int ctr = 0;
+      Ring rg;
       while (it.next(u)) {
         const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
         const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
         for (int blk = 0; blk < nblk; ++blk)
-          for (int j = 0; j < NJ; ++j, ++ctr) {
-            const int st = ctr % vs;
+          for (int j = 0; j < NJ; ++j, ++ctr, rg.next(vs)) {
+            const int st = rg.slot;
             // warm L2 with the rows V_PF blocks ahead: the ring turnaround then
             // sees L2 rather than loaded-HBM latency
             if (V_PF > 0 && blk + V_PF < nblk) {
@@ -1021,7 +1025,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
               tma_prefetch_l2(&map_v, j * 128, rowp);
               tma_prefetch_l2(&map_v, j * 128 + 64, rowp);
             }
-            mbar_wait(&empty[st], ((ctr / vs) & 1) ^ 1);
+            mbar_wait(&empty[st], rg.phase ^ 1);
             if (vtr != nullptr && ctr == 0) vtr[496] = gtimer();  // first TMA issue
             mbar_expect_tx(&full[st], V_STAGE);
             const int row = u.bg * p.T_cap + c0 + blk * TILE_M;
@@ -1037,6 +1041,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     // D[buf][j] = V^T x P^T over the sub-block's 128-token blocks
     if (lane == 0) {
       int ctr = 0, sb = 0;
+      Ring rg;
       while (it.next(u)) {
         const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
         const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
@@ -1048,9 +1053,9 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
           const uint32_t pb = smem_u32(pbuf + buf * PB);
           const int b1 = min(nblk, b0 + V_SUB / TILE_M);
           for (int blk = b0; blk < b1; ++blk)
-            for (int j = 0; j < NJ; ++j, ++ctr) {
-              const int st = ctr % vs;
-              mbar_wait(&full[st], (ctr / vs) & 1);
+            for (int j = 0; j < NJ; ++j, ++ctr, rg.next(vs)) {
+              const int st = rg.slot;
+              mbar_wait(&full[st], rg.phase);
               fence_after();
               if (vtr != nullptr && ctr == 0) vtr[497] = gtimer();  // first stage landed
               if (vtr != nullptr && ctr == vs) vtr[498] = gtimer();  // ring wrapped
