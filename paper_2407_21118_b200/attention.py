@@ -427,6 +427,15 @@ def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
         raise ValidationError(f"cache dtype {cache.dtype} != fused weights dtype {fused.dtype}")
 
 
+def _value_tc_choice(bits: int, r_pad: int) -> bool:
+    env = os.environ.get("PALU_VALUE_KERNEL", "")
+    if bits == FP_BITS:
+        return env != "simt"
+    if bits not in (2, 3, 4, 8) or r_pad % 128 != 0 or env == "simt":
+        return False
+    return env == "tc_quant" or bits in (2, 4)
+
+
 # The (weights, fused, cache) triple validated by the last decode step: shapes
 # and ranks of these objects cannot change, so repeated steps skip the
 # per-layer checks (~50 us of Python per 32-layer step).  Only the most recent
@@ -526,12 +535,11 @@ class _Session:
             self.value_tc_layers.append(
                 (self.tc_layers[li] or self.ls_tc_layers[li]) and not self.fused_layers[li]
                 and V.r_pad % 64 == 0 and V.r_pad <= 512 and L.s_v <= 4
-                # quantised values: the CUDA-core softmax-value kernel is faster than
-                # the converter-fed tcgen05 one on B200; opt in with
-                # PALU_VALUE_KERNEL=tc_quant
-                and ((V.bits == FP_BITS and os.environ.get("PALU_VALUE_KERNEL", "tc") != "simt")
-                     or (V.bits in (2, 3, 4, 8) and V.r_pad % 128 == 0
-                         and os.environ.get("PALU_VALUE_KERNEL") == "tc_quant")))
+                # quantised values: the converter-fed tcgen05 kernel wins for int4 /
+                # int2 (-1..-13 % step, profiles/r01_mma_probe.txt); the CUDA-core
+                # softmax-value kernel stays the default for 3 / 8 bits.
+                # PALU_VALUE_KERNEL=simt | tc_quant forces either side.
+                and _value_tc_choice(V.bits, V.r_pad))
         self.ws_fused = None
         if any(self.fused_layers) or any(self.value_tc_layers):
             nbytes = max(_lib.call("palu_rope_attend_workspace", self.B, self.n, V.G, V.r_pad, self.cap)

@@ -347,7 +347,7 @@ def test_tc_quantized_keys_match_simt(P, bits, vk, monkeypatch):
     for sk in ("simt", "tcgen05"):
         s = _Session(fused, cache, score_kernel=sk, use_graph=False)
         vbits = bits[1] if isinstance(bits, tuple) else bits
-        assert any(s.value_tc_layers) == (sk == "tcgen05" and (vbits == 16 or vk == "tc_quant"))
+        assert any(s.value_tc_layers) == (sk == "tcgen05" and (vbits in (16, 2, 4) or vk == "tc_quant"))
         assert s.tc_layers[0] == (sk == "tcgen05")
         s.x.copy_(x0)
         s.t_dev.fill_(cache.t)
