@@ -78,6 +78,28 @@ constexpr int CODE_BIAS = 128;   // bits <= 4: bf16(128 + c) has bit pattern 0x4
 // Position in an n-deep mbarrier ring (slot, phase parity), advanced
 // incrementally: a runtime modulo per step is an integer-division chain
 // (~100 dependent clocks) on the issuing thread.
+// (sequence x group, super-tile) of consecutive work items without a
+// per-item division (the score roles walk their items in order)
+struct ItemPos {
+  int bg, st, b, g;
+  __device__ __forceinline__ ItemPos(int i, int n_super, int G) {
+    bg = i / n_super;
+    st = i - bg * n_super;
+    b = bg / G;
+    g = bg - b * G;
+  }
+  __device__ __forceinline__ void next(int n_super, int G) {
+    if (++st == n_super) {
+      st = 0;
+      ++bg;
+      if (++g == G) {
+        g = 0;
+        ++b;
+      }
+    }
+  }
+};
+
 struct Ring {
   int slot = 0, phase = 0;
   __device__ __forceinline__ void next(int n) {
@@ -314,8 +336,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         }
       pdl_wait();
       int cur = -1, nloads = 0, it = 0, pst = 0, pph = 0;
-      for (int i = i0; i < i1; ++i, ++it) {
-        const int bg = i / n_super, st = i - bg * n_super;
+      ItemPos ip_(i0, n_super, p.G);
+      for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
+        const int bg = ip_.bg, st = ip_.st;
         if (bg != cur) {
           if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
           if (leader) mbar_expect_tx(uw_full, 2 * kblocks * halves * HEAD_BYTES);
@@ -363,8 +386,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       // dependent clocks) that the shallow MMA queue cannot hide
       int st0 = 0, ph0 = 0;
       const unsigned long long c_start = clock64(), g_start = gtimer();
-      for (int i = i0; i < i1; ++i) {
-        const int bg = i / n_super;
+      ItemPos ip_(i0, n_super, p.G);
+      for (int i = i0; i < i1; ++i, ip_.next(n_super, p.G)) {
+        const int bg = ip_.bg;
         if (bg != cur) {
           if (nloads > 0) umma2_commit_both(uw_empty);  // frees UW in both SMs
           mbar_wait(uw_full, nloads & 1);
@@ -418,8 +442,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     if (p.bits != 16) {
       const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // rows cl, cl + 64 of the SM's tile
       Ring rg;
-      for (int i = i0; i < i1; ++i) {
-        const int bg = i / n_super, st = i - bg * n_super;
+      ItemPos ip_(i0, n_super, p.G);
+      for (int i = i0; i < i1; ++i, ip_.next(n_super, p.G)) {
+        const int bg = ip_.bg, st = ip_.st;
         const int tile = 2 * st + (int)rank;
         switch (p.bits) {
           case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
@@ -447,9 +472,10 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
     int unit = 0, it = 0;
-    for (int i = i0; i < i1; ++i, ++it) {
-      const int bg = i / n_super, st = i - bg * n_super;
-      const int b = bg / p.G, g = bg - b * p.G;
+    ItemPos ip_(i0, n_super, p.G);
+    for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
+      const int bg = ip_.bg, st = ip_.st;
+      const int b = ip_.b, g = ip_.g;
       const int tile = 2 * st + (int)rank;
       // this tile's cos/sin base row (fp64-reduced, L2-resident table): issued
       // before the accumulator wait, so its latency hides behind the MMAs
