@@ -416,9 +416,12 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             // profile modes 8 / 16 (diagnostics): pin the A / B operand tile
             const uint32_t a0 = h_addr + ((p.mode & 8) ? 0 : stage) * H_STAGE_BYTES;
             const uint32_t b0 = uw_addr + ((p.mode & 16) ? 0 : (kb * halves + h)) * HEAD_BYTES;
+            // K16 steps are 32 B apart: +2 in the descriptor's address field
+            // (smem addresses < 256 KB, so the 14-bit field cannot carry)
+            const uint64_t da = sdesc(a0), db = sdesc(b0);
 #pragma unroll
             for (int kk = 0; kk < KB / 16; ++kk)
-              umma2_bf16(d_tmem, sdesc(a0 + kk * 32), sdesc(b0 + kk * 32), (kb | kk) != 0);
+              umma2_bf16(d_tmem, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
             if (h == halves - 1) umma2_commit_both(&empty[stage]);
           }
           umma2_commit_both(&tfull[slot]);
