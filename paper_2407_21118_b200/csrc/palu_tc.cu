@@ -1635,10 +1635,10 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
           mbar_wait(&full[st], rg.phase);
           fence_after();
           const uint32_t a0 = smem_u32(s_h + st * H_STAGE_BYTES);
+          const uint64_t da = sdesc(a0), dq = sdesc(q0 + kb * 2048);  // +2 per K16 step
 #pragma unroll
           for (int kk = 0; kk < KB / 16; ++kk)
-            umma_bf16_id(tmem + slot * 16, sdesc(a0 + kk * 32), sdesc(q0 + kb * 2048 + kk * 32),
-                         IDESC_LS, (kb | kk) != 0);
+            umma_bf16_id(tmem + slot * 16, da + 2 * kk, dq + 2 * kk, IDESC_LS, (kb | kk) != 0);
           umma_commit(&empty[st]);
         }
         umma_commit(&dfull[slot]);
