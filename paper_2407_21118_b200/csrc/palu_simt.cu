@@ -334,12 +334,16 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   pdl_launch();
   if (!split) pdl_wait();
   // grid (n_heads, ceil(R_pad / 32), B): one head, 32 rank rows per CTA
-  extern __shared__ float qa_sm[];  // qr[dh] then bs[32][dh] then cs/sn[dh/2] (fp64)
+  // qr[dh], then bs[32][dh + 1] (row pad: the bf16 layouts read one column
+  // across 32 rank rows per warp, which an unpadded dh stride maps to one
+  // bank), then cos/sin[dh/2] in fp64
+  extern __shared__ float qa_sm[];
   float* qr = qa_sm;
   float* bs = qa_sm + dh;
+  const int bstr = dh + 1;
   const int i = blockIdx.x, k0 = blockIdx.y * 32, b = blockIdx.z;
   const int half = dh / 2;
-  double* csn = reinterpret_cast<double*>(qa_sm + 33 * dh);  // [half] cos, [half] sin
+  double* csn = reinterpret_cast<double*>(qa_sm + dh + 32 * (dh + 1));  // [half] cos, [half] sin
   const int g = i / s_k, p = i - g * s_k;
   const int nk = min(32, R_pad - k0);
   const double pos = (double)(*t_dev);
@@ -374,14 +378,14 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
           float f[V];
           Vec16<T>::unpack(v[u], f);
 #pragma unroll
-          for (int e = 0; e < V; ++e) bs[kk * dh + c + e] = f[e];
+          for (int e = 0; e < V; ++e) bs[kk * bstr + c + e] = f[e];
         }
       }
     }
   } else {
     for (int idx = threadIdx.x; idx < nk * dh; idx += blockDim.x) {
       const int kk = idx / dh, c = idx - kk * dh;
-      bs[kk * dh + c] = to_f(bg[(size_t)kk * width + c]);
+      bs[kk * bstr + c] = to_f(bg[(size_t)kk * width + c]);
     }
   }
   pdl_wait();  // q comes from the preceding GEMV
@@ -394,12 +398,13 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   __syncthreads();
   if (layout == 0) {
     float* out = reinterpret_cast<float*>(uw) + (((size_t)b * n_heads + i) * R_pad + k0) * dh;
-    for (int idx = threadIdx.x; idx < nk * half; idx += blockDim.x) {
-      const int kk = idx / half, j = idx - kk * half;
-      const float b1 = bs[kk * dh + j], b2 = bs[kk * dh + j + half];
-      out[(size_t)kk * dh + j] = scale * (qr[j] * b1 + qr[j + half] * b2);
-      out[(size_t)kk * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
-    }
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int kk = threadIdx.x >> 5; kk < nk; kk += nw)
+      for (int j = lane; j < half; j += 32) {
+        const float b1 = bs[kk * bstr + j], b2 = bs[kk * bstr + j + half];
+        out[(size_t)kk * dh + j] = scale * (qr[j] * b1 + qr[j + half] * b2);
+        out[(size_t)kk * dh + j + half] = scale * (qr[j + half] * b1 - qr[j] * b2);
+      }
   } else {
     // bf16 [B][G][s_k*dh][R_pad]: row n = p*dh + c, c < half -> u_c, else w_{c-half}.
     // layouts 2/3: rank k stored at the K position the tcgen05 converter gives
@@ -408,9 +413,10 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
     bf16* out = reinterpret_cast<bf16*>(uw) +
                 (((size_t)b * (n_heads / s_k) + g) * width + (size_t)p * dh) * R_pad;
     const int grp = layout == 2 ? 8 : (layout == 3 ? 16 : 0);
-    for (int idx = threadIdx.x; idx < half * nk; idx += blockDim.x) {
-      const int j = idx / nk, kk = idx - j * nk;
-      const float b1 = bs[kk * dh + j], b2 = bs[kk * dh + j + half];
+    // lane = rank row kk (nk <= 32), warp strides over the frequencies j
+    const int kk = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int j = threadIdx.x >> 5; j < half && kk < nk; j += nw) {
+      const float b1 = bs[kk * bstr + j], b2 = bs[kk * bstr + j + half];
       int pos = k0 + kk;
       if (grp) {
         const int i = pos % grp;
@@ -1406,7 +1412,8 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
                n_heads);
   PALU_REQUIRE(layout >= 0 && layout <= 3, "palu_query_absorb: layout must be 0..3");
   dim3 grid(n_heads, (R_pad + 31) / 32, B);
-  const size_t smem = (size_t)33 * head_dim * sizeof(float) + (size_t)head_dim * sizeof(double);
+  const size_t smem = ((size_t)head_dim + 32 * ((size_t)head_dim + 1)) * sizeof(float) +
+                      (size_t)head_dim * sizeof(double);
   if (dtype == PALU_DTYPE_BF16)
     PALU_CK(launch_k(query_absorb_kernel<bf16>, dim3(grid), dim3(256), smem, S(stream), q, ld_q,
                      n_heads, head_dim, s_k, (const bf16*)bk, bk_rows, R_pad, theta, scale, t_dev,
