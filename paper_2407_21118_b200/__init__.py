@@ -31,7 +31,9 @@ from .model import (
     GroupFactors,
     LayerKV,
     LayerWeights,
+    Matrix,
     ModelWeights,
+    RotatedLayer,
     fuse_hadamard,
     hadamard,
 )

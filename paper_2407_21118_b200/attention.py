@@ -384,6 +384,8 @@ class LatentKVCache:
             raise ValidationError(f"score_kernel must be auto|simt|tcgen05|fused, got {score_kernel!r}")
         self.score_kernel = score_kernel
         self._session = None
+        self._validated = None   # (weights, fused) of the last validated step
+        self._allreduce = None   # head-group shard: per-layer partial-output reduction
 
     # reference-compatible accessors -------------------------------------
     @property
@@ -436,21 +438,17 @@ def _value_tc_choice(bits: int, r_pad: int) -> bool:
     return env == "tc_quant" or bits in (2, 4)
 
 
-# The (weights, fused, cache) triple validated by the last decode step: shapes
-# and ranks of these objects cannot change, so repeated steps skip the
-# per-layer checks (~50 us of Python per 32-layer step).  Only the most recent
-# triple is held, so no other objects are kept alive.
-_LAST_VALID: tuple = ()
-
-
 def _validate_step(weights, fused, cache) -> None:
-    global _LAST_VALID
-    if (len(_LAST_VALID) == 3 and _LAST_VALID[0] is weights and _LAST_VALID[1] is fused
-            and _LAST_VALID[2] is cache):
+    """Validation before any mutation.  The (weights, fused) pair a cache was
+    last validated with is remembered ON the cache (shapes and ranks of these
+    objects cannot change), so repeated steps skip the per-layer checks (~50 us
+    of Python per 32-layer step) and nothing outlives the cache."""
+    v = cache._validated
+    if v is not None and v[0] is weights and v[1] is fused:
         return
     _check_cache_fused(cache, fused)
     validate_weights(weights, cache.config)
-    _LAST_VALID = (weights, fused, cache)
+    cache._validated = (weights, fused)
 
 
 # ---------------------------------------------------------------------------
@@ -721,6 +719,10 @@ def _session(fused, cache, score_kernel=None) -> _Session:
     if (s is None or s.fused is not fused or s.cap != cache.capacity
             or s.score_kernel != score_kernel):
         s = _Session(fused, cache, score_kernel=score_kernel)
+        # a shard's reduction survives session rebuilds (capacity growth,
+        # another score kernel): without it every rank would silently return
+        # only its partial output
+        s.allreduce = cache._allreduce
         cache._session = s
     return s
 

@@ -46,11 +46,17 @@ __device__ __forceinline__ void pdl_enter() {
 // dependents first, wait for the predecessor only where its output is read.
 // A kernel K starts once its predecessor P executed launch_dependents: if P
 // waits first (pdl_enter), everything before P has completed; if P is split,
-// everything before P's predecessor has.  In the step order
-//   gemv (split) -> append K -> append V -> absorb (split) -> score (split)
-//   -> value (split) -> merge -> gemv (split)
-// score may therefore read the key rows (append K) and value the H_v rows
-// (append V) before their waits; gemv and absorb read only constants early.
+// only what precedes P's own wait is guaranteed.  In the step order
+//   gemv (split) -> append K+V (enter) -> absorb (split) -> score (split)
+//   -> value (split) -> merge (enter) -> gemv (split)
+// score and value start once the layer's first GEMV completed, while the
+// append of row t may still run.  Rule: every thread that reads a latent row,
+// scale or zero point of the NEWEST token (row t) executes pdl_wait() first
+// (griddepcontrol.wait returns after the whole predecessor chain completed).
+// Rows < t were written by earlier steps and may be read before the wait:
+// the value producer streams them early and waits before the last tile; the
+// score producer waits before its first UW load; the converter and epilogue
+// warps wait at entry.  gemv and absorb read only constants early.
 __device__ __forceinline__ void pdl_launch() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }

@@ -52,6 +52,14 @@ struct Params {
 };
 
 constexpr int TRACE_STRIDE = 512;
+
+// Profiling modes that skip MMAs or barrier waits (results invalid) exist only
+// in diagnostic builds (-DPALU_DIAG); the product library ignores the knobs.
+#ifdef PALU_DIAG
+static int diag_env(const char* name) { return getenv(name) ? atoi(getenv(name)) : 0; }
+#else
+static int diag_env(const char*) { return 0; }
+#endif
 __device__ __forceinline__ unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -443,6 +451,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   } else if (warp >= 2 + EPI_WARPS) {
     // ---------------- quantised keys: converter warps (both SMs) ----------------
     if (p.bits != 16) {
+      // the newest token's codes and zero point come from this step's latent
+      // append: wait for the predecessor chain before the first code load
+      pdl_wait();
       const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // rows cl, cl + 64 of the SM's tile
       Ring rg;
       ItemPos ip_(i0, n_super, p.G);
@@ -474,6 +485,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       }
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    // quantised keys: the newest token's scale comes from this step's append
+    pdl_wait();
     int unit = 0, it = 0;
     ItemPos ip_(i0, n_super, p.G);
     for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
@@ -863,6 +876,7 @@ __device__ __forceinline__ void value_converter(const VParams& vp, int T_cap, Ne
                                                 int vs, int cl, int lane) {
   VStage g0, g1, gn;
   VCodes<BITS, RPL> b0, b1;
+  pdl_wait();  // codes / zero points of the newest token come from this step's append
   next_stage(g0);
   next_stage(g1);
   load_v_codes<BITS, RPL>(vp, T_cap, g0, cl, b0);
@@ -1020,8 +1034,15 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       VStageIter sit(it, T_rows, NJ);
       VStage g;
       Ring rg;
+      bool waited = false;
       while (sit.next(g)) {
         const int rs = rg.slot;
+        // the tile holding the newest token (row T_rows - 1, written by this
+        // step's append) is loaded only after the predecessor chain completed
+        if (!waited && g.t0 + TILE_M >= T_rows) {
+          pdl_wait();
+          waited = true;
+        }
         mbar_wait(&rempty[rs], rg.phase ^ 1);
         mbar_expect_tx(&rfull[rs], RB + TILE_M * 4);
         uint8_t* slot = raw + rs * (RB + TILE_M * 4);
@@ -1040,6 +1061,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     if (lane == 0 && vp.bits == 16) {
       prefetch_map(&map_v);
       int ctr = 0;
+      bool waited = false;
       Ring rg;
       while (it.next(u)) {
         const int c0 = u.st0 * SUPER, c1 = min(T_rows, u.st1 * SUPER);
@@ -1047,6 +1069,11 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
         for (int blk = 0; blk < nblk; ++blk)
           for (int j = 0; j < NJ; ++j, ++ctr, rg.next(vs)) {
             const int st = rg.slot;
+            // newest token (this step's append): wait for the predecessor chain
+            if (!waited && c0 + (blk + 1) * TILE_M >= T_rows) {
+              pdl_wait();
+              waited = true;
+            }
             // warm L2 with the rows V_PF blocks ahead: the ring turnaround then
             // sees L2 rather than loaded-HBM latency
             if (V_PF > 0 && blk + V_PF < nblk) {
@@ -1497,8 +1524,9 @@ constexpr int VALUE_THREADS_PACKED = 448;  // 4 converter warps (8 spill at 576 
 template <int NT>
 __global__ void __launch_bounds__(NT, 1)
 value_tc_kernel(const __grid_constant__ CUtensorMap map_v, const Params p, const VParams vp) {
-  // H_v (written by the latent append, three launches back) streams into the
-  // ring while the score kernel drains; group A waits before reading logits
+  // H_v rows older than this step stream into the ring while the score kernel
+  // drains; the producer waits before the tile holding the newest row (this
+  // step's latent append, which may still be running), group A before the logits
   pdl_launch();
   if (!p.pdl_split) pdl_wait();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1865,7 +1893,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.stages = stages;
   prm.score_pairs = (sms & ~1) / 2;
   prm.ready = nullptr;
-  prm.mode = getenv("PALU_TC_PROFILE_MODE") ? atoi(getenv("PALU_TC_PROFILE_MODE")) : 0;
+  prm.mode = diag_env("PALU_TC_PROFILE_MODE");
   // packed keys: the converter warps read code rows with plain loads, which
   // the L2 prefetch 3 items ahead still helps (-0.5 % step, int4); raw keys
   // stream through TMA and do better without it (tools/pf_sweep.sh)
@@ -1879,7 +1907,6 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   prm.codes = reinterpret_cast<const uint8_t*>(hk);
   prm.scales = scales;
   prm.zps = zps;
-  if (bits != 16 && getenv("PALU_TC_PROFILE_MODE")) prm.mode = atoi(getenv("PALU_TC_PROFILE_MODE"));
   if (getenv("PALU_SCORE_TRACE")) {  // diagnostics: per-head-pair timeline (tools/score_trace.py)
     if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
     PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));
@@ -2149,7 +2176,7 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   prm.T_cap = T_cap;
   prm.ld_logits = ld_logits;
   prm.score_pairs = sms;  // one contiguous window of items per CTA (vc = per)
-  prm.mode = getenv("PALU_VALUE_DIAG") ? atoi(getenv("PALU_VALUE_DIAG")) : 0;  // diagnostics only
+  prm.mode = diag_env("PALU_VALUE_DIAG");  // diagnostic builds only
   prm.ready = ready;
   prm.t_dev = t_dev;
   prm.logits = const_cast<float*>(logits);

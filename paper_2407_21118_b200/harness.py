@@ -153,7 +153,7 @@ def synth_model(d, n_heads, head_dim, s_k, ranks_k, s_v, ranks_v, seed, layers=1
         key = DecomposedLayer(gran(s_k), tuple(kg), d, head_dim, n_heads)
         value = DecomposedLayer(gran(s_v), tuple(vg), d, head_dim, n_heads)
         if hadamard_fused:
-            key, value = fuse_hadamard(key), fuse_hadamard(value)
+            key, value = fuse_hadamard(key).layer, fuse_hadamard(value).layer
         wl.append(lw)
         dl.append(LayerKV(key=key, value=value))
     config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=rope, rope_base=rope_base)

@@ -185,7 +185,65 @@ class LayerKV:
     value: object
 
 
-def hadamard(dim: int) -> np.ndarray:
+class Matrix:
+    """Read-only 2-D float64 matrix with the reference's surface (core.py:21-66):
+    ``.data`` (non-writable ndarray), ``.rows``, ``.cols``, ``.shape``, ``wrap``,
+    ``t()`` and ``@``.  Returned by the offline helpers so callers written
+    against the reference (``hadamard(r).data``) run unchanged."""
+
+    __slots__ = ("data",)
+
+    def __init__(self, data, *, _own: bool = False):
+        arr = np.asarray(data, dtype=np.float64)
+        arr = np.ascontiguousarray(arr) if _own else np.array(arr, dtype=np.float64, order="C", copy=True)
+        if arr.ndim != 2:
+            raise ValidationError(f"Matrix requires a 2-D payload, got ndim={arr.ndim}")
+        if arr.shape[0] < 1 or arr.shape[1] < 1:
+            raise ValidationError(f"Matrix dimensions must be positive, got {arr.shape}")
+        if not np.all(np.isfinite(arr)):
+            raise ValidationError("Matrix entries must be finite (found NaN or Inf)")
+        arr.setflags(write=False)
+        object.__setattr__(self, "data", arr)
+
+    def __setattr__(self, name, value):
+        raise AttributeError("Matrix is immutable")
+
+    @classmethod
+    def wrap(cls, arr) -> "Matrix":
+        return cls(arr, _own=True)
+
+    @property
+    def rows(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def cols(self) -> int:
+        return self.data.shape[1]
+
+    @property
+    def shape(self) -> tuple:
+        return self.data.shape
+
+    def t(self) -> "Matrix":
+        return Matrix.wrap(self.data.T.copy())
+
+    def __matmul__(self, other) -> "Matrix":
+        return Matrix.wrap(self.data @ as_array(other))
+
+    def __array__(self, dtype=None, copy=None):
+        return self.data if dtype is None else self.data.astype(dtype)
+
+
+@dataclass(frozen=True)
+class RotatedLayer:
+    """quant.py:119-124: a DecomposedLayer whose factors carry a fused
+    Hadamard rotation, plus the per-group rotation sizes."""
+
+    layer: DecomposedLayer
+    rotation_dims: tuple
+
+
+def hadamard(dim: int) -> Matrix:
     """Offline prep (core.py:282-313): Sylvester blocks over the binary decomposition."""
     if dim <= 0:
         raise ValidationError(f"hadamard dimension must be positive, got {dim}")
@@ -199,14 +257,18 @@ def hadamard(dim: int) -> np.ndarray:
         out[at:at + p, at:at + p] = h / np.sqrt(p)
         at += p
         remaining -= p
-    return out
+    return Matrix.wrap(out)
 
 
-def fuse_hadamard(layer: DecomposedLayer) -> DecomposedLayer:
-    """Offline prep (quant.py:127-153): (A, B) -> (A H, H^T B) per group."""
-    groups = []
+def fuse_hadamard(layer: DecomposedLayer) -> RotatedLayer:
+    """Offline prep (quant.py:127-153): (A, B) -> (A H, H^T B) per group;
+    returns RotatedLayer(layer, rotation_dims) like the reference."""
+    groups, dims = [], []
     for g in layer.groups:
-        h = hadamard(g.rank)
-        groups.append(GroupFactors(a=as_array(g.a) @ h, b=h.T @ as_array(g.b), rank=g.rank))
-    return DecomposedLayer(granularity=layer.granularity, groups=tuple(groups),
-                           d_model=layer.d_model, head_dim=layer.head_dim, n_heads=layer.n_heads)
+        h = hadamard(g.rank).data
+        groups.append(GroupFactors(a=Matrix.wrap(as_array(g.a) @ h), b=Matrix.wrap(h.T @ as_array(g.b)),
+                                   rank=g.rank))
+        dims.append(g.rank)
+    rotated = DecomposedLayer(granularity=layer.granularity, groups=tuple(groups),
+                              d_model=layer.d_model, head_dim=layer.head_dim, n_heads=layer.n_heads)
+    return RotatedLayer(layer=rotated, rotation_dims=tuple(dims))

@@ -16,8 +16,8 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .attention import (FusedWeights, LatentKVCache, LayerFused, _head_offsets, _round_up,
-                        _torch)
+from .attention import (FusedWeights, LatentKVCache, LayerFused, _SideStore, _head_offsets,
+                        _round_up, _torch)
 from .errors import ValidationError
 from .model import AttentionConfig, DecomposedLayer, LayerKV
 from .parallel_plan import plan_groups
@@ -109,20 +109,33 @@ def shard_engine(fused: FusedWeights, cache: LatentKVCache, rank: int, world: in
                        batch=cache.batch, capacity=cache.capacity, device=cache.device,
                        score_kernel=cache.score_kernel)
     for li, (_, shard) in enumerate(decs):
+        stores = list(cs._stores[li])
         for side, groups in ((0, shard.k_groups), (1, shard.v_groups)):
-            src, dst = cache._stores[li][side], cs._stores[li][side]
+            src, dst = cache._stores[li][side], stores[side]
+            if dst.r_pad != src.r_pad:
+                # non-uniform ranks: the shard's widest group may be narrower
+                # than the source store's row; keep the source row width
+                dst = _SideStore(dst.ranks, dst.bits, src.r_pad, dst.batch, dst.cap, dst.dtype,
+                                 cache.device)
+                stores[side] = dst
             g0, g1 = groups[0], groups[-1] + 1
             dst.rows.copy_(src.rows[:, g0:g1])
             for k in ("scales", "zps", "scales64", "zps64"):
                 if getattr(src, k) is not None:
                     getattr(dst, k).copy_(getattr(src, k)[:, g0:g1])
+        cs._stores[li] = tuple(stores)
     cs.t = cache.t
     return fs, cs
 
 
-def attach_allreduce(session, fn) -> None:
-    """Install the per-layer partial-output reduction on a shard's session:
-    fn(x) reduces the [B x d] layer output in place on the current stream
-    (e.g. an NCCL all-reduce).  The step graph is re-captured with it."""
-    session.allreduce = fn
-    session.graph = None
+def attach_allreduce(target, fn) -> None:
+    """Install the per-layer partial-output reduction on a shard: fn(x)
+    reduces the [B x d] layer output in place on the current stream (e.g. an
+    NCCL all-reduce).  ``target`` is the shard's LatentKVCache (or a session
+    of it); the hook is kept on the cache, so sessions rebuilt after capacity
+    growth keep reducing.  The step graph is re-captured with it."""
+    cache = target if isinstance(target, LatentKVCache) else target.cache
+    cache._allreduce = fn
+    if cache._session is not None:
+        cache._session.allreduce = fn
+        cache._session.graph = None
