@@ -694,6 +694,14 @@ class _Session:
             self.eager_steps += 1
             return
         if self.graph is None:
+            import gc
+
+            # dead sessions (cache <-> session cycles) own CUDA graphs whose
+            # destruction is illegal while a capture is open: collect them now
+            # and keep the collector off until the capture ends
+            gc.collect()
+            gc_was_enabled = gc.isenabled()
+            gc.disable()
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
@@ -703,11 +711,15 @@ class _Session:
                     with torch.cuda.graph(g, stream=s):
                         self.launch_step()
             except Exception:  # a collective that cannot be captured: run eagerly
+                if gc_was_enabled:
+                    gc.enable()
                 torch.cuda.current_stream().wait_stream(s)
                 torch.cuda.synchronize()
                 self.use_graph = False
                 self.launch_step()
                 return
+            if gc_was_enabled:
+                gc.enable()
             torch.cuda.current_stream().wait_stream(s)
             self.graph = g
         self.graph.replay()

@@ -1035,6 +1035,43 @@ softmax_value_partial_kernel(const void* __restrict__ hv, const float* __restric
 
 __global__ void advance_kernel(int* t_dev) { pdl_enter(); *t_dev += 1; }
 
+// Comparator support (flashinfer trtllm-gen decode inside the uncompressed
+// step graph): RoPE + append row t into an HND paged bf16 cache
+// [page][2][n][P][d_h] (page = b * pages_per_seq + t / P), rotated q as bf16
+// [B][n][d_h] for the attention kernel.
+__global__ void dense_append_paged_kernel(const float* __restrict__ qkv, int n_heads, int dh,
+                                          bf16* __restrict__ kv, int P, int pages_per_seq,
+                                          const double* __restrict__ theta,
+                                          const int* __restrict__ t_dev, bf16* __restrict__ qout) {
+  pdl_enter();
+  const int i = blockIdx.x, b = blockIdx.y;
+  const int d = n_heads * dh, half = dh / 2;
+  const int t = *t_dev;
+  const float* q = qkv + (size_t)b * 3 * d + (size_t)i * dh;
+  const float* k = q + d;
+  const float* v = q + 2 * d;
+  const size_t page = (size_t)b * pages_per_seq + t / P;
+  bf16* krow = kv + (((page * 2 + 0) * n_heads + i) * P + t % P) * dh;
+  bf16* vrow = kv + (((page * 2 + 1) * n_heads + i) * P + t % P) * dh;
+  bf16* qo = qout + ((size_t)b * n_heads + i) * dh;
+  for (int j = threadIdx.x; j < half; j += blockDim.x) {
+    double sn, cs;
+    sincos_big((double)t * theta[j], &sn, &cs);
+    const double klo = k[j], khi = k[j + half], qlo = q[j], qhi = q[j + half];
+    krow[j] = __float2bfloat16_rn((float)(klo * cs - khi * sn));
+    krow[j + half] = __float2bfloat16_rn((float)(klo * sn + khi * cs));
+    qo[j] = __float2bfloat16_rn((float)(qlo * cs - qhi * sn));
+    qo[j + half] = __float2bfloat16_rn((float)(qlo * sn + qhi * cs));
+  }
+  for (int j = threadIdx.x; j < dh; j += blockDim.x) vrow[j] = __float2bfloat16_rn(v[j]);
+}
+
+__global__ void cast_bf16_f32_kernel(const bf16* __restrict__ src, float* __restrict__ dst, int n) {
+  pdl_enter();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = __bfloat162float(src[i]);
+}
+
 // ---------------------------------------------------------------------------
 // Uncompressed baseline K0 (reference_decode, attention.py:133-168)
 // ---------------------------------------------------------------------------
@@ -1507,6 +1544,23 @@ int palu_softmax_value(int dtype, int bits, const void* hv, const float* scales,
 
 int palu_advance(int* t_dev, void* stream) {
   PALU_CK(launch_k(advance_kernel, dim3(1), dim3(1), 0, S(stream), t_dev));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_dense_append_paged(const float* qkv, int B, int n_heads, int head_dim, void* kv_pages,
+                            int page_size, int pages_per_seq, const double* theta, const int* t_dev,
+                            void* q_out, void* stream) {
+  PALU_REQUIRE(head_dim % 2 == 0, "palu_dense_append_paged: head_dim %d", head_dim);
+  PALU_CK(launch_k(dense_append_paged_kernel, dim3(n_heads, B), dim3(64), 0, S(stream), qkv, n_heads,
+                   head_dim, (bf16*)kv_pages, page_size, pages_per_seq, theta, t_dev, (bf16*)q_out));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_cast_bf16_f32(const void* src, float* dst, int n, void* stream) {
+  PALU_CK(launch_k(cast_bf16_f32_kernel, dim3((n + 255) / 256 < 148 ? (n + 255) / 256 : 148), dim3(256),
+                   0, S(stream), (const bf16*)src, dst, n));
   PALU_LAUNCHED();
   return PALU_OK;
 }

@@ -89,7 +89,10 @@ class DenseModel:
             self.launch_step()
             return
         if self.graph is None:
+            import gc
+
             self.launch_step()  # warm (lazy module load) outside capture
+            gc.collect()  # no dead graph may be destroyed while the capture is open
             g = torch.cuda.CUDAGraph()
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
