@@ -79,7 +79,9 @@ def load(path: str = LIB_PATH):
             "(there is no CPU fallback for the Palu B200 path)")
     lib = C.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
-        fn = getattr(lib, name)
+        fn = getattr(lib, name, None)
+        if fn is None:  # an older build loaded through PALU_LIB_PATH (A/B timing)
+            continue
         fn.restype = res
         fn.argtypes = args
     _lib = lib

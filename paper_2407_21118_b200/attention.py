@@ -430,12 +430,16 @@ def _check_cache_fused(cache: LatentKVCache, fused: FusedWeights) -> None:
 
 
 def _value_tc_choice(bits: int, r_pad: int) -> bool:
+    """Packed 2/4/8-bit values run on the int8 tensor pipe (palu_vq.cuh); 3-bit
+    values keep the CUDA-core kernel unless PALU_VALUE_KERNEL=tc_quant (the
+    converter-to-bf16 tcgen05 kernel, also forced for 2/4/8 bits with
+    tc_quant_bf16).  PALU_VALUE_KERNEL=simt forces the CUDA-core kernel."""
     env = os.environ.get("PALU_VALUE_KERNEL", "")
     if bits == FP_BITS:
         return env != "simt"
     if bits not in (2, 3, 4, 8) or r_pad % 128 != 0 or env == "simt":
         return False
-    return env == "tc_quant" or bits in (2, 4)
+    return env in ("tc_quant", "tc_quant_bf16") or bits in (2, 4, 8)
 
 
 def _validate_step(weights, fused, cache) -> None:
@@ -533,10 +537,7 @@ class _Session:
             self.value_tc_layers.append(
                 (self.tc_layers[li] or self.ls_tc_layers[li]) and not self.fused_layers[li]
                 and V.r_pad % 64 == 0 and V.r_pad <= 512 and L.s_v <= 4
-                # quantised values: the converter-fed tcgen05 kernel wins for int4 /
-                # int2 (-1..-13 % step, profiles/r01_mma_probe.txt); the CUDA-core
-                # softmax-value kernel stays the default for 3 / 8 bits.
-                # PALU_VALUE_KERNEL=simt | tc_quant forces either side.
+                # quantised values: int8 tensor pipe for 2/4/8 bits (_value_tc_choice)
                 and _value_tc_choice(V.bits, V.r_pad))
         self.ws_fused = None
         if any(self.fused_layers) or any(self.value_tc_layers):

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libpalu_b200.so")
 
-SOURCES = ["palu_simt.cu", "palu_tc.cu"]
+SOURCES = ["palu_simt.cu", "palu_tc.cu", "palu_gemv.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

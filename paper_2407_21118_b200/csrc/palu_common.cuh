@@ -82,6 +82,11 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 
 typedef __nv_bfloat16 bf16;
 
+// Weight-streaming bf16 GEMV (palu_gemv.cu); PALU_EUNSUPPORTED if the shape
+// is not streamable (the caller falls back to the warp-per-row kernel).
+int gemv_stream(const bf16* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
+                int acc, cudaStream_t st);
+
 __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(bf16 v) { return __bfloat162float(v); }
 template <typename T> __device__ __forceinline__ T from_f(float v);

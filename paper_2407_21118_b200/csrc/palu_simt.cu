@@ -1305,8 +1305,14 @@ int palu_gemv(int dtype, const void* W, int N, int K, const float* x, int B, int
   PALU_REQUIRE(K % vec == 0, "palu_gemv: K=%d must be a multiple of %d", K, vec);
   PALU_REQUIRE(((uintptr_t)W & 15) == 0 && ((uintptr_t)x & 15) == 0 && ldx % 4 == 0,
                "palu_gemv: W/x must be 16-byte aligned");
-  if (dtype == PALU_DTYPE_BF16)
+  if (dtype == PALU_DTYPE_BF16) {
+    static const bool warp_rows = getenv("PALU_GEMV") && strcmp(getenv("PALU_GEMV"), "warp") == 0;
+    if (!warp_rows) {
+      const int rc = gemv_stream((const bf16*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
+      if (rc != PALU_EUNSUPPORTED) return rc;
+    }
     return gemv_dispatch<bf16>((const bf16*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
+  }
   PALU_REQUIRE(dtype == PALU_DTYPE_F32, "palu_gemv: unknown dtype %d", dtype);
   return gemv_dispatch<float>((const float*)W, N, K, x, B, ldx, y, ldy, accumulate, S(stream));
 }

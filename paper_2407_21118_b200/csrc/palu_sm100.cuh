@@ -17,6 +17,18 @@ constexpr int H_STAGE_BYTES = TILE_M * 128;  // 16 KB per (tile, k-block)
 constexpr int UW_KB_BYTES = N_CTA * 128;     // 32 KB per k-block
 constexpr int SMEM_LIMIT = 232448;           // 227 KB opt-in
 
+// Position in an n-deep mbarrier ring (slot, phase parity), advanced
+// incrementally (a runtime modulo per step is an integer-division chain).
+struct Ring {
+  int slot = 0, phase = 0;
+  __device__ __forceinline__ void next(int n) {
+    if (++slot == n) {
+      slot = 0;
+      phase ^= 1;
+    }
+  }
+};
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

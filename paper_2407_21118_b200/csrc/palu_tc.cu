@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <math.h>
 #include <stdlib.h>
+#include <string.h>
 
 #include "palu_sm100.cuh"
 
@@ -108,15 +109,6 @@ struct ItemPos {
   }
 };
 
-struct Ring {
-  int slot = 0, phase = 0;
-  __device__ __forceinline__ void next(int n) {
-    if (++slot == n) {
-      slot = 0;
-      phase ^= 1;
-    }
-  }
-};
 
 template <int BITS, class PP>
 __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t* full,
@@ -1810,6 +1802,8 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t
   return PALU_OK;
 }
 
+#include "palu_vq.cuh"
+
 }  // namespace tc
 }  // namespace palu
 
@@ -2126,6 +2120,86 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
 }
 
 
+// Packed V (2/4/8-bit codes) on the int8 tensor pipe (palu_vq.cuh), then the
+// deterministic merge.  PALU_VALUE_KERNEL=tc_quant_bf16 keeps the earlier
+// converter-to-bf16 kernel (A/B timing).
+static bool value_q_enabled() {
+  const char* e = getenv("PALU_VALUE_KERNEL");
+  return !(e && strcmp(e, "tc_quant_bf16") == 0);
+}
+
+static int launch_value_q(int bits, const void* hv, const float* scales, const float* zps, int B,
+                          int n_heads, int s, int G, int Rv_pad, int T_cap, const float* logits,
+                          int ld_logits, const int* t_dev, const int* ranks_v, const int* o_off,
+                          float* ctx, int ld_ctx, void* workspace, cudaStream_t st) {
+  using namespace palu::tc;
+  PALU_REQUIRE(Rv_pad % 128 == 0 && Rv_pad <= 512 && s <= V_HP,
+               "palu_value_tc (int8 pipe): unsupported shape (Rv %d, s %d)", Rv_pad, s);
+  PALU_REQUIRE(T_cap % TILE_M == 0, "palu_value_tc: packed V needs T_cap %% 128 == 0 (got %d)", T_cap);
+  const int row_bytes = Rv_pad * bits / 8;
+  const int box_bytes = row_bytes <= 256 ? row_bytes : 128;
+  PALU_REQUIRE(row_bytes % box_bytes == 0, "palu_value_tc: row of %d bytes", row_bytes);
+  EncodeTiledFn fn = encode_fn();
+  PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  CUtensorMap map_c = {};
+  const cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)B * G * T_cap};
+  const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+  const cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)TILE_M}, es[2] = {1, 1};
+  CUresult r = fn(&map_c, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(hv), dims, strides, box,
+                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  PALU_REQUIRE(r == CUDA_SUCCESS, "palu_value_tc: code tensor map failed (%d)", (int)r);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const ValueWs W = value_ws(workspace, B, n_heads, G, Rv_pad, T_cap);
+  VQParams p = {};
+  p.B = B;
+  p.n_heads = n_heads;
+  p.s = s;
+  p.G = G;
+  p.Rv_pad = Rv_pad;
+  p.T_cap = T_cap;
+  p.ld_logits = ld_logits;
+  p.row_bytes = row_bytes;
+  p.box_bytes = box_bytes;
+  p.ns_cap = fused_ns_cap(T_cap);
+  p.t_dev = t_dev;
+  p.logits = logits;
+  p.scales = scales;
+  p.zps = zps;
+  p.pm = W.pm;
+  p.pl = W.pl;
+  p.pctx = W.pctx;
+  const int RB = TILE_M * row_bytes;
+  const int dyn_limit = SMEM_LIMIT - 2048;
+  p.raw_slots = 72 * 1024 / RB;
+  if (p.raw_slots < 2) p.raw_slots = 2;
+  if (p.raw_slots > 4) p.raw_slots = 4;
+  const int fixed = 1024 + 2 * VQ_PBUF + p.raw_slots * RB + 2 * 3 * V_HP * 4 + 2 * V_HP * 8 +
+                    (2 * p.raw_slots + 6) * 8 + 16 + 16 * 8;
+  p.stages = (dyn_limit - fixed) / (VQ_STAGE + 16);
+  if (p.stages > 8) p.stages = 8;
+  PALU_REQUIRE(p.stages >= 2, "palu_value_tc (int8 pipe): ring too small (%d)", p.stages);
+  const size_t smem = (size_t)fixed + (size_t)p.stages * (VQ_STAGE + 16);
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(value_q_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
+    PALU_CK(cudaFuncSetAttribute(value_q_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
+    PALU_CK(cudaFuncSetAttribute(value_q_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
+    attr = true;
+  }
+  if (bits == 2)
+    PALU_CK(launch_k(value_q_kernel<2>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
+  else if (bits == 4)
+    PALU_CK(launch_k(value_q_kernel<4>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
+  else
+    PALU_CK(launch_k(value_q_kernel<8>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
+  PALU_LAUNCHED();
+  return launch_value_merge(W.pm, W.pl, W.pctx, p.ns_cap, Rv_pad, n_heads, s, G, B, t_dev, sms, 0,
+                            ranks_v, o_off, ctx, ld_ctx, st);
+}
+
 // Standalone tcgen05 softmax + value (the unfused path's second kernel).
 int palu_value_tc(int bits, const void* hv, const float* scales, const float* zps, int B,
                   int n_heads, int s, int G, int Rv_pad, int T_cap, const float* logits,
@@ -2139,6 +2213,9 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   }
   PALU_REQUIRE(((uintptr_t)hv & 15) == 0, "palu_value_tc: unaligned H_v");
   PALU_REQUIRE(bits == 16 || (scales && zps), "palu_value_tc: quantised values need scales/zps");
+  if ((bits == 2 || bits == 4 || bits == 8) && value_q_enabled())
+    return launch_value_q(bits, hv, scales, zps, B, n_heads, s, G, Rv_pad, T_cap, logits, ld_logits,
+                          t_dev, ranks_v, o_off, ctx, ld_ctx, workspace, (cudaStream_t)stream);
   CUtensorMap map_v = {};
   const int row_bytes = bits == 16 ? Rv_pad * 2 : Rv_pad * bits / 8;
   if (bits == 16) {

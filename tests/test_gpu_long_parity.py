@@ -25,6 +25,8 @@ CASES = [
     ("r256_int4had_64k", 65536, 2, 256, 256, 4, True, True, 10000.0),
     ("r256_int2had_64k", 65536, 2, 256, 256, 2, True, True, 10000.0),
     ("preset_k16v4had_64k", 65536, 2, 128, 384, (16, 4), True, True, 10000.0),
+    ("r256_int8_64k", 65536, 1, 256, 256, 8, False, True, 10000.0),
+    ("preset_k16v2had_64k", 65536, 1, 128, 384, (16, 2), True, True, 10000.0),
     ("r256_bf16_16k", 16384, 2, 256, 256, 16, False, True, 10000.0),
     ("r256_bf16_128k_edge", 131072, 1, 256, 256, 16, False, True, 10000.0),
     ("r256_bf16_64k_base1e6", 65536, 1, 256, 256, 16, False, True, 1e6),

@@ -328,26 +328,28 @@ def test_fused_attend_long_batched(P, batch, context, rk, rv, monkeypatch):
         assert e < 1e-3, (name, e)
 
 
-@pytest.mark.parametrize("vk", ["default", "tc_quant"])
-@pytest.mark.parametrize("bits", [2, 3, 4, 8, (4, 16), (16, 4)])
+@pytest.mark.parametrize("vk", ["default", "tc_quant", "tc_quant_bf16"])
+@pytest.mark.parametrize("bits", [2, 3, 4, 8, (4, 16), (16, 4), (16, 8), (16, 2)])
 def test_tc_quantized_keys_match_simt(P, bits, vk, monkeypatch):
     """Quantised (packed-code) keys on the tcgen05 score kernel (converter
-    warps write c - z, the epilogue scales) and, with tc_quant, quantised
-    values on the tcgen05 value kernel, against the CUDA-core quantised path
-    on the same cache: logits and the step output."""
+    warps write c - z, the epilogue scales) and quantised values on the int8
+    tensor pipe (default, 2/4/8 bits) or the converter-to-bf16 tcgen05 kernel
+    (tc_quant / tc_quant_bf16), against the CUDA-core quantised path: logits
+    and the step output.  Each arm gets its OWN identically seeded cache, so
+    the newest row is written by that arm's append (PDL ordering is live)."""
     import torch
     from paper_2407_21118_b200.attention import _Session
     from paper_2407_21118_b200.harness import synthetic_engine
-    if vk == "tc_quant":
-        monkeypatch.setenv("PALU_VALUE_KERNEL", "tc_quant")
-    _, fused, cache = synthetic_engine(layers=1, batch=2, context=3000, extra=8, bits=bits,
-                                       seed=7)
+    if vk != "default":
+        monkeypatch.setenv("PALU_VALUE_KERNEL", vk)
     x0 = torch.randn(2, 4096, device="cuda") * 0.5
     out, lg = {}, {}
     for sk in ("simt", "tcgen05"):
+        _, fused, cache = synthetic_engine(layers=1, batch=2, context=3000, extra=8, bits=bits,
+                                           seed=7)
         s = _Session(fused, cache, score_kernel=sk, use_graph=False)
         vbits = bits[1] if isinstance(bits, tuple) else bits
-        assert any(s.value_tc_layers) == (sk == "tcgen05" and (vbits in (16, 2, 4) or vk == "tc_quant"))
+        assert any(s.value_tc_layers) == (sk == "tcgen05" and (vbits in (16, 2, 4, 8) or vk != "default"))
         assert s.tc_layers[0] == (sk == "tcgen05")
         s.x.copy_(x0)
         s.t_dev.fill_(cache.t)
