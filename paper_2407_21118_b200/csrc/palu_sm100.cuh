@@ -184,6 +184,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       : "memory");
 }
 
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ---- CTA-pair (cta_group::2) primitives ---------------------------------------
 constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;  // shared::cluster address -> CTA rank 0
 

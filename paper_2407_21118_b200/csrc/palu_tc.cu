@@ -1163,17 +1163,16 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       // sub-block's are loaded while this one is processed
       constexpr int NP = V_SUB / 256;
       float2 x[NP][V_HP], xn[NP][V_HP];
+      // no value-dependent masking in the prefetch (an op on a loaded register
+      // waits for the load); the masks are applied where the values are used
       auto load = [&](int s0, float2 (&dst)[NP][V_HP]) {
 #pragma unroll
         for (int i = 0; i < NP; ++i) {
           const int t = s0 + 2 * ta + 256 * i;
 #pragma unroll
           for (int h = 0; h < V_HP; ++h) {
-            float2 v = make_float2(-INFINITY, -INFINITY);
-            if (h < s_v && t < nt) {
-              v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
-              if (t + 1 >= nt) v.y = -INFINITY;
-            }
+            float2 v = make_float2(0.f, 0.f);
+            if (h < s_v && t < nt) v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
             dst[i][h] = v;
           }
         }
@@ -1182,9 +1181,13 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       for (int s0 = 0; s0 < ntok; s0 += V_SUB, ++sb) {
         const int buf = sb & 1;
 #pragma unroll
-        for (int i = 0; i < NP; ++i)
+        for (int i = 0; i < NP; ++i) {
+          const int t = s0 + 2 * ta + 256 * i;
 #pragma unroll
-          for (int h = 0; h < V_HP; ++h) x[i][h] = xn[i][h];
+          for (int h = 0; h < V_HP; ++h)
+            x[i][h] = make_float2(h < s_v && t < nt ? xn[i][h].x : -INFINITY,
+                                  h < s_v && t + 1 < nt ? xn[i][h].y : -INFINITY);
+        }
         if (s0 + V_SUB < ntok) load(s0 + V_SUB, xn);
         // quantised values: P carries p s_t (the operand holds c - z)
         float2 sv[NP];
@@ -2137,7 +2140,7 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
                "palu_value_tc (int8 pipe): unsupported shape (Rv %d, s %d)", Rv_pad, s);
   PALU_REQUIRE(T_cap % TILE_M == 0, "palu_value_tc: packed V needs T_cap %% 128 == 0 (got %d)", T_cap);
   const int row_bytes = Rv_pad * bits / 8;
-  const int box_bytes = row_bytes <= 256 ? row_bytes : 128;
+  const int box_bytes = row_bytes <= 256 ? row_bytes : 128;  // tensor map (kept for tools)
   PALU_REQUIRE(row_bytes % box_bytes == 0, "palu_value_tc: row of %d bytes", row_bytes);
   EncodeTiledFn fn = encode_fn();
   PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
@@ -2162,7 +2165,8 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
   p.T_cap = T_cap;
   p.ld_logits = ld_logits;
   p.row_bytes = row_bytes;
-  p.box_bytes = box_bytes;
+  p.box_bytes = row_bytes;  // raw slots hold [128 rows][row_bytes] (1-D bulk copies)
+  p.codes = reinterpret_cast<const uint8_t*>(hv);
   p.ns_cap = fused_ns_cap(T_cap);
   p.t_dev = t_dev;
   p.logits = logits;
@@ -2171,17 +2175,29 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
   p.pm = W.pm;
   p.pl = W.pl;
   p.pctx = W.pctx;
+  p.trace = nullptr;
+  p.diag = diag_env("PALU_VQ_DIAG");
+  if (getenv("PALU_FUSED_TRACE")) {  // diagnostics: per-CTA timeline (tools/vq_trace.py)
+    if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
+    PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, st));
+    p.trace = g_trace;
+    g_trace_ctas = sms;
+  }
   const int RB = TILE_M * row_bytes;
   const int dyn_limit = SMEM_LIMIT - 2048;
-  p.raw_slots = 72 * 1024 / RB;
-  if (p.raw_slots < 2) p.raw_slots = 2;
-  if (p.raw_slots > 4) p.raw_slots = 4;
-  const int fixed = 1024 + 2 * VQ_PBUF + p.raw_slots * RB + 2 * 3 * V_HP * 4 + 2 * V_HP * 8 +
-                    (2 * p.raw_slots + 6) * 8 + 16 + 16 * 8;
-  p.stages = (dyn_limit - fixed) / (VQ_STAGE + 16);
-  if (p.stages > 8) p.stages = 8;
-  PALU_REQUIRE(p.stages >= 2, "palu_value_tc (int8 pipe): ring too small (%d)", p.stages);
-  const size_t smem = (size_t)fixed + (size_t)p.stages * (VQ_STAGE + 16);
+  // operand ring slots hold whole blocks (NJ column tiles); 2-4 of them, the
+  // raw code ring (bulk-copy landing zone) takes the rest, at most 6 blocks
+  const int NJ = Rv_pad / 128;
+  const int OB = NJ * VQ_STAGE;
+  const int RS = RB;  // raw slot: the block's codes
+  const int misc = 1024 + 2 * VQ_PBUF + (2 * (V_HP + 1) + 2) * 4 + 2 * VQ_A * V_HP * (4 + 8) + 6 * 8 + 16;
+  p.stages = (dyn_limit - misc - 2 * (RS + 16)) / (OB + 16);
+  if (p.stages > 4) p.stages = 4;
+  PALU_REQUIRE(p.stages >= 2, "palu_value_tc (int8 pipe): operand ring too small (%d)", p.stages);
+  p.raw_slots = (dyn_limit - misc - p.stages * (OB + 16)) / (RS + 16);
+  if (p.raw_slots > 6) p.raw_slots = 6;
+  PALU_REQUIRE(p.raw_slots >= 2, "palu_value_tc (int8 pipe): raw ring too small (%d)", p.raw_slots);
+  const size_t smem = (size_t)misc + (size_t)p.raw_slots * (RS + 16) + (size_t)p.stages * (OB + 16);
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(value_q_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));

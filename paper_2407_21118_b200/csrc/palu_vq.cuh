@@ -7,55 +7,69 @@
 //
 //   sum_t p_t x_t[c] = sum_t (p_t s_t) (c_t[c] - z_t)
 //
-// Per 512-token sub-block and head, u_t = p_t s_t / max_t(p_t s_t) is split
-// into two signed 8-bit digits, w_t = 254 hi_t + lo_t = round(127 * 254 u_t)
-// (|u_t - w_t / 32258| <= 1.6e-5 of the sub-block maximum).  The tensor pipe
-// then accumulates EXACT integer sums
-//   D[c][hi_h] = sum_t hi_t c_t,   D[c][lo_h] = sum_t lo_t c_t     (s32, TMEM)
-// with A = the raw codes as u8 (MN-major SW128: the cache's own [token][col]
-// order, nibbles / crumbs expanded to bytes by 4 converter warps; 8-bit codes
-// are copied), B = the digits (K-major SW128, N = 16 rows: 4 heads x {hi, lo},
-// 8 zero rows), K = 32 tokens per MMA.  The zero-point term
-// sum_t w_t z_t is an exact int64 sum on the CUDA cores, so
-//   ctx_sub[c] = (254 D_hi + D_lo - sum_t w_t z_t) * max(p s) / 32258
-// carries only the digit rounding of the weights.  An online softmax across
-// sub-blocks and the deterministic value_merge_kernel complete the path.
+// Per 384-token sub-block and head, u_t = p_t s_t / (max_t s_t) in [0, 1] is
+// split into two signed 8-bit digits, w_t = 254 hi_t + lo_t = round(32258 u_t)
+// (|u_t - w_t / 32258| <= 1.6e-5).  The tensor pipe accumulates EXACT integer
+// sums over the sub-block
+//   D[c][hi_h] = sum_t hi_t a_t[c],   D[c][lo_h] = sum_t lo_t a_t[c]  (s32, TMEM)
+// with B = the digits (K-major SW128, N = 16 rows: 4 heads x {hi, lo}, 8
+// zero rows), K = 32 tokens per MMA, and A in the cache's own [token][col]
+// order (MN-major SW128): a = the codes c as u8, nibbles / crumbs expanded to
+// bytes by 4 converter warps (8-bit codes copied); the zero-point term
+// sum_t w_t z_t is an exact int64 sum on the CUDA cores.  So
+//   ctx_sub[c] = (254 D_hi + D_lo - sum_t w_t z_t) * max(s) / 32258
+// carries only the digit rounding of the weights.  (Subtracting z in the
+// converters instead -- s8 operands, no int64 term -- measured slower: the
+// per-byte subtraction costs the converters more than the term costs group A.)  An online softmax across sub-blocks and
+// the deterministic value_merge_kernel complete the path.
 //
-// The only bytes streamed are the packed codes (TMA, 128-token tiles of the
-// whole row), the per-token fp32 scale and zero point, and the logits: the
-// HBM-bound stream the north star names, with no bf16 staging of values.
+// Bytes streamed: the packed codes (one 1-D bulk copy per 128-token block,
+// L2-prefetched ahead), per-token scales and zero points, and the logits: the HBM-bound stream the north star names, with no bf16 staging.
 //
-// Warps: 0-3 softmax + digits (group A), 4-7 TMEM readback + online softmax
-// (group B), 8 TMA producer, 9 MMA issuer + TMEM owner, 10-13 converters.
+// Warps: 0-5 softmax + digits (group A), 6-9 TMEM readback + online softmax
+// (group B), 10-13 converters, 14 bulk-copy producer, 15 MMA issuer + TMEM
+// owner.  Pipeline units are whole 128-token blocks (all column tiles):
+// every mbarrier hand-off costs ~0.1 us of a warp's time, so per-tile
+// hand-offs capped the converter at ~1.2 us per block; group A uses one
+// named barrier per sub-block and leaves per-warp partial sums for group B.
 
-constexpr int VQ_THREADS = 448;
-constexpr int VQ_SUB = 512;                 // tokens per digit sub-block
+// 16 warps = 4 per scheduler quadrant: 128 registers per thread (18 warps
+// put 5 on two quadrants and capped the kernel at 96, with spills)
+constexpr int VQ_A = 6, VQ_B0 = 6, VQ_CV0 = 10, VQ_CONV = 4, VQ_PROD = 14, VQ_MMA = 15;
+constexpr int VQ_THREADS = (VQ_MMA + 1) * 32;
+constexpr int VQ_SUB = 384;                 // tokens per digit sub-block (one pair per group-A thread)
 constexpr int VQ_NB = VQ_SUB / TILE_M;      // 128-token blocks per sub-block
 constexpr int VQ_PBUF = VQ_NB * 2048;       // digits: per block 16 rows x 128 B
-constexpr int VQ_STAGE = TILE_M * 128;      // one (block, 128-column tile) u8 operand
+constexpr int VQ_STAGE = TILE_M * 128;      // one (block, 128-column tile) u8 operand;
+                                            // an operand ring slot holds NJ of them
 constexpr int VQ_TMEM = 128;                // 2 buffers x up to 4 tiles x 16 columns
+constexpr int VQ_PF = 8;                    // L2 prefetch distance of the code stream (blocks)
 constexpr float VQ_W = 127.f * 254.f;       // digit weight scale
-// D s32, A u8 (MN-major), B s8 (K-major), M 128, N 16
+// D s32, A u8 (codes, MN-major), B s8 (digits, K-major), M 128, N 16
 constexpr uint32_t IDESC_Q = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) |
                              ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
 
 struct VQParams {
   int B, n_heads, s, G, Rv_pad, T_cap, ld_logits;
-  int row_bytes, box_bytes;  // packed row; TMA box width (row_bytes or 128)
+  int row_bytes, box_bytes;  // packed row; raw-slot row pitch (= row_bytes: 1-D bulk copies)
+  const uint8_t* codes;      // [B][G][T_cap][row_bytes] packed codes
   int raw_slots, stages, ns_cap;
   const int* t_dev;
   const float* logits;
   const float* scales;
   const float* zps;
   float *pm, *pl, *pctx;
+  unsigned long long* trace;  // diagnostics (PALU_FUSED_TRACE): per-CTA timeline, else null
+  int diag;  // diagnostic builds only (results invalid): 1 no MMAs, 2 no converter stores, 4 no converter loads
 };
 
-__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t accum) {
+__device__ __forceinline__ void umma_i8(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(IDESC_Q), "r"(accum)
+      "l"(a), "l"(b), "r"(idesc), "r"(accum)
       : "memory");
 }
 
@@ -91,23 +105,109 @@ __device__ __forceinline__ int vq_column(int m) {
   }
 }
 
+// Warps 0-3 of group A: one sub-block's integer accumulators (TMEM lane
+// quarter = warp) -> online softmax across the unit's sub-blocks -> the
+// unit's partial at its last sub-block (value_merge_kernel layout).
+struct VQPend {
+  int sb, b, g, s0u;
+  bool first, last;
+};
+template <int BITS>
+__device__ __forceinline__ void vq_readback(const VQParams& p, const VQPend& q, int NJ, int warp, int ta,
+                                          int col_in, uint32_t tmem, const float* stat_m,
+                                          const float* stat_l, const long long* stat_z,
+                                          uint64_t* pfull, uint64_t* dfull, uint64_t* dempty,
+                                          float (&acc)[4][V_HP], float (&mr)[V_HP], float (&lr)[V_HP]) {
+    const int buf = q.sb & 1;
+    mbar_wait(&pfull[buf], (q.sb >> 1) & 1);  // every warp's partials (acquire)
+    mbar_wait(&dfull[buf], (q.sb >> 1) & 1);  // the sub-block's accumulators
+    fence_after();
+    if (q.first) {
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h) {
+        mr[h] = -INFINITY;
+        lr[h] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[j][h] = 0.f;
+      }
+    }
+    float sc_old[V_HP], sc_new[V_HP];
+    long long zw[V_HP];
+    const float scl = stat_m[buf * (V_HP + 1) + V_HP] / VQ_W;
+#pragma unroll
+    for (int h = 0; h < V_HP; ++h) {
+      const float ms = stat_m[buf * (V_HP + 1) + h];
+      float ls = 0.f;
+      zw[h] = 0;
+#pragma unroll
+      for (int w = 0; w < VQ_A; ++w) {
+        ls += stat_l[(buf * VQ_A + w) * V_HP + h];
+        zw[h] += stat_z[(buf * VQ_A + w) * V_HP + h];
+      }
+      const float mn = fmaxf(mr[h], ms);
+      sc_old[h] = mr[h] == -INFINITY ? 0.f : __expf(mr[h] - mn);
+      sc_new[h] = ms == -INFINITY ? 0.f : __expf(ms - mn);
+      lr[h] = lr[h] * sc_old[h] + ls * sc_new[h];
+      mr[h] = mn;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j < NJ) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)((buf * NJ + j) * 16), v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h) {
+          const long long r = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + V_HP]) + zw[h];
+          acc[j][h] = acc[j][h] * sc_old[h] + __ll2float_rn(r) * scl * sc_new[h];
+        }
+      }
+    }
+    fence_before();
+    named_bar_sync(4, 128);
+    if (ta == 0) mbar_arrive(&dempty[buf]);
+    if (q.last) {
+      // the unit's partial (value_merge_kernel layout): slot = first super-tile
+      for (int j = 0; j < NJ && j < 4; ++j) {
+        const int col = j * 128 + col_in;
+#pragma unroll
+        for (int h = 0; h < V_HP; ++h)
+          if (h < p.s)
+            p.pctx[(((size_t)q.b * p.n_heads + q.g * p.s + h) * p.ns_cap + q.s0u) * p.Rv_pad + col] =
+                acc[j][h];
+      }
+#pragma unroll
+      for (int h = 0; h < V_HP; ++h)
+        if (ta == h && h < p.s) {
+          const size_t pi = ((size_t)q.b * p.n_heads + q.g * p.s + h) * p.ns_cap + q.s0u;
+          p.pm[pi] = mr[h];
+          p.pl[pi] = lr[h];
+        }
+    }
+  }
+
 template <int BITS>
 __global__ void __launch_bounds__(VQ_THREADS, 1)
 value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
   // codes of older tokens stream while the score kernel drains; the producer
-  // waits before the newest token's tile, group A before the logits
+  // waits before the newest token's block, group A before the logits
   pdl_launch();
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   const int NJ = p.Rv_pad / 128;
   const int RB = TILE_M * p.row_bytes;
-  uint8_t* ring = smem;                                          // stages x 16 KB
-  uint8_t* pbuf = ring + p.stages * VQ_STAGE;                    // 2 x 8 KB digits
-  uint8_t* raw = pbuf + 2 * VQ_PBUF;                             // raw_slots x RB codes
-  float* stat = reinterpret_cast<float*>(raw + (size_t)p.raw_slots * RB);  // [2][3][V_HP]
-  long long* statz = reinterpret_cast<long long*>(stat + 2 * 3 * V_HP);    // [2][V_HP]
-  uint64_t* full = reinterpret_cast<uint64_t*>(statz + 2 * V_HP);
+  const int RS = RB;                                             // raw slot: the block's codes
+  const int OB = NJ * VQ_STAGE;                                  // operand bytes per block
+  uint8_t* ring = smem;                                          // stages x OB
+  uint8_t* pbuf = ring + p.stages * OB;                          // 2 x 8 KB digits
+  uint8_t* raw = pbuf + 2 * VQ_PBUF;                             // raw_slots x RS
+  // per sub-block buffer: max logit per head + max scale (group A), and
+  // per-warp partial sums of p and of the int64 zero-point term
+  float* stat_m = reinterpret_cast<float*>(raw + (size_t)p.raw_slots * RS);  // [2][V_HP + 1]
+  float* stat_l = stat_m + 2 * (V_HP + 1) + 2;                               // [2][VQ_A][V_HP]
+  long long* stat_z = reinterpret_cast<long long*>(stat_l + 2 * VQ_A * V_HP);  // [2][VQ_A][V_HP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(stat_z + 2 * VQ_A * V_HP);
   uint64_t* empty = full + p.stages;
   uint64_t* rfull = empty + p.stages;
   uint64_t* rempty = rfull + p.raw_slots;
@@ -115,8 +215,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
   uint64_t* dfull = pfull + 2;             // [2] sub-block accumulators complete
   uint64_t* dempty = dfull + 2;            // [2] sub-block accumulators read back
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
-  __shared__ float red_f[2][4][V_HP];
-  __shared__ long long red_z[4][V_HP];
+  __shared__ float red_m[2][VQ_A][V_HP + 1];  // per-warp max logit per head + max scale
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
   const int T_rows = *p.t_dev + 1;  // final: advanced by the previous step's last launch
@@ -127,15 +226,15 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
 
   if (tid == 0) {
     for (int st = 0; st < p.stages; ++st) {
-      mbar_init(&full[st], 4);  // one arrive per converter warp
+      mbar_init(&full[st], VQ_CONV);  // one arrive per converter warp
       mbar_init(&empty[st], 1);
     }
     for (int r = 0; r < p.raw_slots; ++r) {
       mbar_init(&rfull[r], 1);
-      mbar_init(&rempty[r], 4);
+      mbar_init(&rempty[r], VQ_CONV);
     }
     for (int a = 0; a < 2; ++a) {
-      mbar_init(&pfull[a], 1);
+      mbar_init(&pfull[a], VQ_A);  // one arrive per group-A warp
       mbar_init(&dfull[a], 1);
       mbar_init(&dempty[a], 1);
     }
@@ -146,7 +245,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
     const int blk = i >> 6, w = i & 63;
     reinterpret_cast<uint4*>(pbuf + blk * 2048 + 1024)[w] = make_uint4(0u, 0u, 0u, 0u);
   }
-  if (warp == 9) {
+  if (warp == VQ_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tslot)),
                  "r"(VQ_TMEM));
@@ -158,54 +257,90 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
   fence_after();
   const uint32_t tmem = *tslot;
   int bg, s0u, s1u;
+  unsigned long long* tr = p.trace ? p.trace + (size_t)blockIdx.x * TRACE_STRIDE : nullptr;
+  // SM clock (cheap; %globaltimer reads cost ~0.1 us); slots 0 / 1 keep the
+  // global timer for cross-CTA alignment, slot 2 the clock at entry
+  auto mark = [&](int slot) {
+    if (tr != nullptr && slot < TRACE_STRIDE) tr[slot] = slot < 2 ? gtimer() : (unsigned long long)clock64();
+  };
+  if (tid == 0 && tr != nullptr) {
+    tr[2] = (unsigned long long)clock64();
+    mark(0);
+  }
 
-  if (warp == 8) {
-    // ---------------- TMA producer: packed code tiles {row, 128 tokens} ----------------
+  if (warp == VQ_PROD) {
+    // ---------------- producer: one 1-D bulk copy per 128-token block ----------------
     if (lane == 0) {
-      prefetch_map(&map_c);
       VQIter it(i0, i1, n_super);
       Ring rg;
       bool waited = false;
+      int kblk = 0;
+      // L2 prefetch cursor VQ_PF blocks ahead of the loads: the HBM latency
+      // then overlaps the ring turnaround instead of gating it
+      VQIter pit(i0, i1, n_super);
+      int pbg = 0, pc = 0, pc1 = 0;
+      auto prefetch_next = [&]() {
+        if (pc >= pc1) {
+          int a, b;
+          if (!pit.next(pbg, a, b)) return;
+          pc = a * SUPER;
+          pc1 = min(T_rows, b * SUPER);
+        }
+        bulk_prefetch_l2(p.codes + ((size_t)pbg * p.T_cap + pc) * p.row_bytes, RB);
+        pc += TILE_M;
+      };
+      for (int k = 0; k < VQ_PF; ++k) prefetch_next();
       while (it.next(bg, s0u, s1u)) {
         const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
         for (int t0 = c0; t0 < c1; t0 += TILE_M) {
+          prefetch_next();
           // the newest token (row T_rows - 1) comes from this step's append
           if (!waited && t0 + TILE_M >= T_rows) {
             pdl_wait();
             waited = true;
           }
           mbar_wait(&rempty[rg.slot], rg.phase ^ 1);
+          mark(8 + min(kblk++, 47));
+          // a block of one (sequence, group) is one contiguous range of the cache
           mbar_expect_tx(&rfull[rg.slot], RB);
-          uint8_t* dst = raw + (size_t)rg.slot * RB;
-          for (int x = 0; x < p.row_bytes; x += p.box_bytes)
-            tma_load_2d(&map_c, &rfull[rg.slot], dst + x * TILE_M, x, bg * p.T_cap + t0);
+          bulk_load(raw + (size_t)rg.slot * RS, p.codes + ((size_t)bg * p.T_cap + t0) * p.row_bytes,
+                    (uint32_t)RB, &rfull[rg.slot]);
           rg.next(p.raw_slots);
         }
       }
     }
-  } else if (warp >= 10) {
-    // ---------------- converters: packed row -> u8 MN-major SW128 operand ----------------
-    // work item (row, q): 16-byte raw chunk q of the row's slice for column
-    // tile j; RC consecutive lanes share a row (conflict-free raw reads)
-    constexpr int RC = BITS;  // raw 16-byte chunks per row per 128 columns
-    const int ct = tid - 320;
+  } else if (warp >= VQ_CV0 && warp < VQ_CV0 + VQ_CONV) {
+    // ---------------- converters: packed block -> u8 MN-major SW128 tiles ----------------
+    // work item (row, q) = 16-byte raw chunk q of the row's slice of column
+    // tile j; RCR consecutive lanes share a row (conflict-free raw reads)
+    constexpr int RCR = BITS;                     // raw chunks per row per 128 columns
+    constexpr int RC = RCR * TILE_M / (VQ_CONV * 32);  // items per thread per column tile
+    const int ct = tid - VQ_CV0 * 32;
     VQIter it(i0, i1, n_super);
     Ring rr, rs;
+    int kblk = 0;
     while (it.next(bg, s0u, s1u)) {
       const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
-      for (int t0 = c0; t0 < c1; t0 += TILE_M) {
+      for (int t0 = c0; t0 < c1; t0 += TILE_M, ++kblk) {
         mbar_wait(&rfull[rr.slot], rr.phase);
-        const uint8_t* slot = raw + (size_t)rr.slot * RB;
+        mbar_wait(&empty[rs.slot], rs.phase ^ 1);
+        if (ct == 0) mark(56 + min(kblk, 47));
+        const uint8_t* slot = raw + (size_t)rr.slot * RS;
+        uint8_t* ob = ring + (size_t)rs.slot * OB;
         for (int j = 0; j < NJ; ++j) {
-          mbar_wait(&empty[rs.slot], rs.phase ^ 1);
-          uint8_t* st = ring + rs.slot * VQ_STAGE;
+          uint4 vv[RC];
 #pragma unroll
           for (int k = 0; k < RC; ++k) {
-            const int w = ct + 128 * k;
-            const int row = w / RC, q = w % RC;
-            const int kb = j * 16 * BITS + 16 * q;  // byte inside the packed row
-            const uint4 v = lds128(smem_u32(slot + (kb / p.box_bytes) * (TILE_M * p.box_bytes) +
-                                            row * p.box_bytes + kb % p.box_bytes));
+            const int w = ct + VQ_CONV * 32 * k;
+            const int row = w / RCR, q = w % RCR;
+            vv[k] = lds128(smem_u32(slot + row * p.row_bytes + j * 16 * BITS + 16 * q));
+          }
+          uint8_t* st = ob + j * VQ_STAGE;
+#pragma unroll
+          for (int k = 0; k < RC; ++k) {
+            const int w = ct + VQ_CONV * 32 * k;
+            const int row = w / RCR, q = w % RCR;
+            const uint4 v = vv[k];
             const uint32_t rowa = smem_u32(st + row * 128);
             const int sw = row & 7;
             if constexpr (BITS == 8) {
@@ -233,17 +368,19 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
                              : "memory");
             }
           }
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&full[rs.slot]);
-          rs.next(p.stages);
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[rr.slot]);
+        if (lane == 0) {
+          mbar_arrive(&full[rs.slot]);
+          mbar_arrive(&rempty[rr.slot]);
+        }
+        if (ct == 0) mark(104 + min(kblk, 47));
         rr.next(p.raw_slots);
+        rs.next(p.stages);
       }
     }
-  } else if (warp == 9) {
+  } else if (warp == VQ_MMA) {
     // ---------------- MMA issuer ----------------
     if (lane == 0) {
       VQIter it(i0, i1, n_super);
@@ -257,33 +394,39 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
           mbar_wait(&pfull[buf], (sb >> 1) & 1);
           if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
           fence_after();
+          mark(152 + min(sb, 15));
           const uint32_t pb = smem_u32(pbuf + buf * VQ_PBUF);
           const int b1 = min(nblk, b0 + VQ_NB);
-          for (int blk = b0; blk < b1; ++blk)
+          for (int blk = b0; blk < b1; ++blk, rs.next(p.stages)) {
+            mbar_wait(&full[rs.slot], rs.phase);
+            fence_after();
+            const uint64_t db = sdesc(pb + (blk - b0) * 2048);
             for (int j = 0; j < NJ; ++j) {
-              mbar_wait(&full[rs.slot], rs.phase);
-              fence_after();
-              const uint32_t a0 = smem_u32(ring + rs.slot * VQ_STAGE);
               const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
-              const uint64_t da = sdesc_mn(a0, VQ_STAGE, 1024);
-              const uint64_t db = sdesc(pb + (blk - b0) * 2048);
+              const uint64_t da = sdesc_mn(smem_u32(ring + rs.slot * OB + j * VQ_STAGE), VQ_STAGE, 1024);
+              if ((p.diag & 1) == 0)
 #pragma unroll
-              for (int kk = 0; kk < TILE_M / 32; ++kk)  // K = 32 tokens: 4 KB of A, 32 B of B
-                umma_i8(d, da + (uint64_t)(kk * 256), db + (uint64_t)(kk * 2), (blk != b0) || (kk != 0));
-              umma_commit(&empty[rs.slot]);
-              rs.next(p.stages);
+                for (int kk = 0; kk < TILE_M / 32; ++kk)  // K = 32 tokens: 4 KB of A, 32 B of B
+                  umma_i8(d, da + (uint64_t)(kk * 256), db + (uint64_t)(kk * 2), IDESC_Q,
+                          (blk != b0) || (kk != 0));
             }
+            umma_commit(&empty[rs.slot]);
+          }
           umma_commit(&dfull[buf]);
+          mark(168 + min(sb, 15));
         }
       }
     }
-  } else if (warp < 4) {
-    // ---------------- group A: logits -> statistics -> digits ----------------
+  } else if (warp < VQ_A) {
+    // ---------------- group A (warps 0-7): logits -> statistics -> digits ----------------
+    // thread = one token pair of each 512-token sub-block; one named barrier
+    // per sub-block (max logit per head, max scale); the sums of p and of the
+    // zero-point term are left as per-warp partials for the readback
     pdl_wait();  // logits (score kernel), scales / zero points of the newest token
+    constexpr int NT = VQ_A * 32;
     const int ta = tid;
     VQIter it(i0, i1, n_super);
     int sb = 0;
-    constexpr int NP = VQ_SUB / 256;  // token pairs per thread per sub-block
     while (it.next(bg, s0u, s1u)) {
       const int b = bg / p.G, g = bg - b * p.G;
       const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
@@ -292,215 +435,155 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       const float* lg = p.logits + ((size_t)b * p.n_heads + g * p.s) * p.ld_logits + c0;
       const float* sc = p.scales + (size_t)bg * p.T_cap + c0;
       const float* zp = p.zps + (size_t)bg * p.T_cap + c0;
-      float2 x[NP][V_HP], xn[NP][V_HP];
-      auto load = [&](int s0, float2 (&dst)[NP][V_HP]) {
+      float2 x[V_HP], xn[V_HP], sv, svn, zv, zvn;
+      // the sub-block's logits, scales and zero points; the next sub-block's
+      // are in flight while this one runs
+      // (no value-dependent masking here: any op on a loaded register would
+      // wait for the load and turn the prefetch into a synchronous read; the
+      // masks are applied where the values are used)
+      auto load = [&](int s0, float2 (&dst)[V_HP], float2& sd, float2& zd) {
+        const int t = s0 + 2 * ta;
 #pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const int t = s0 + 2 * ta + 256 * i;
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) {
-            float2 v = make_float2(-INFINITY, -INFINITY);
-            if (h < p.s && t < nt) {
-              v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
-              if (t + 1 >= nt) v.y = -INFINITY;
-            }
-            dst[i][h] = v;
+        for (int h = 0; h < V_HP; ++h) {
+          float2 v = make_float2(0.f, 0.f);
+          if (h < p.s && t < nt) v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
+          dst[h] = v;
+        }
+        sd = make_float2(0.f, 0.f);
+        zd = make_float2(0.f, 0.f);
+        if (t < nt) {
+          sd.x = __ldg(sc + t);
+          zd.x = __ldg(zp + t);
+          if (t + 1 < nt) {
+            sd.y = __ldg(sc + t + 1);
+            zd.y = __ldg(zp + t + 1);
           }
         }
       };
-      load(0, xn);
+      load(0, xn, svn, zvn);
       for (int s0 = 0; s0 < ntok; s0 += VQ_SUB, ++sb) {
         const int buf = sb & 1;
+        {
+          const int t = s0 + 2 * ta;
 #pragma unroll
-        for (int i = 0; i < NP; ++i)
-#pragma unroll
-          for (int h = 0; h < V_HP; ++h) x[i][h] = xn[i][h];
-        if (s0 + VQ_SUB < ntok) load(s0 + VQ_SUB, xn);
-        float2 sv[NP], zv[NP];
-#pragma unroll
-        for (int i = 0; i < NP; ++i) {
-          const int t = s0 + 2 * ta + 256 * i;
-          sv[i] = make_float2(0.f, 0.f);
-          zv[i] = make_float2(0.f, 0.f);
-          if (t < nt) {
-            sv[i].x = __ldg(sc + t);
-            zv[i].x = __ldg(zp + t);
-            if (t + 1 < nt) {
-              sv[i].y = __ldg(sc + t + 1);
-              zv[i].y = __ldg(zp + t + 1);
-            }
-          }
+          for (int h = 0; h < V_HP; ++h)
+            x[h] = make_float2(h < p.s && t < nt ? xn[h].x : -INFINITY,
+                               h < p.s && t + 1 < nt ? xn[h].y : -INFINITY);
         }
-        // (1) logit maximum of the sub-block
-        float m[V_HP];
+        sv = svn;
+        zv = zvn;
+        if (s0 + VQ_SUB < ntok) load(s0 + VQ_SUB, xn, svn, zvn);
+        if (ta == 0) mark(184 + min(sb, 15));
+        // (1) max logit per head and max scale of the sub-block (red_m is
+        // double-buffered: the next sub-block's writes cannot race these reads)
+        float m[V_HP + 1];
 #pragma unroll
-        for (int h = 0; h < V_HP; ++h) {
-          m[h] = -INFINITY;
+        for (int h = 0; h < V_HP; ++h) m[h] = fmaxf(x[h].x, x[h].y);
+        m[V_HP] = fmaxf(sv.x, sv.y);
 #pragma unroll
-          for (int i = 0; i < NP; ++i) m[h] = fmaxf(m[h], fmaxf(x[i][h].x, x[i][h].y));
+        for (int h = 0; h <= V_HP; ++h) {
           m[h] = warp_reduce(m[h], [](float a, float c) { return fmaxf(a, c); });
-          if (lane == 0) red_f[0][warp][h] = m[h];
+          if (lane == 0) red_m[buf][warp][h] = m[h];
         }
-        named_bar_sync(3, 128);
-        // (2) p = exp(x - m), q = p s, and max q
-        float l[V_HP], mx[V_HP];
-        float2 q[NP][V_HP];
+        if (ta == 0) mark(300 + min(sb, 15));
+        named_bar_sync(3, NT);
+        if (ta == 0) mark(316 + min(sb, 15));
 #pragma unroll
-        for (int h = 0; h < V_HP; ++h) {
-          m[h] = fmaxf(fmaxf(red_f[0][0][h], red_f[0][1][h]), fmaxf(red_f[0][2][h], red_f[0][3][h]));
-          l[h] = 0.f;
-          mx[h] = 0.f;
+        for (int h = 0; h <= V_HP; ++h) {
+          float v = red_m[buf][0][h];
 #pragma unroll
-          for (int i = 0; i < NP; ++i) {
-            float p0 = 0.f, p1 = 0.f;
-            if (h < p.s) {
-              p0 = __expf(x[i][h].x - m[h]);
-              p1 = __expf(x[i][h].y - m[h]);
-            }
-            l[h] += p0 + p1;
-            q[i][h] = make_float2(p0 * sv[i].x, p1 * sv[i].y);
-            mx[h] = fmaxf(mx[h], fmaxf(q[i][h].x, q[i][h].y));
-          }
-          mx[h] = warp_reduce(mx[h], [](float a, float c) { return fmaxf(a, c); });
-          if (lane == 0) red_f[1][warp][h] = mx[h];
+          for (int w = 1; w < VQ_A; ++w) v = fmaxf(v, red_m[buf][w][h]);
+          m[h] = v;
         }
-        // the digit buffer is free once sub-block sb - 2 was read back
+        // the digit buffer and statistics slot are free once sub-block sb - 2
+        // was read back (by warps 0-3 of this group, one iteration ago)
         if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
-        named_bar_sync(3, 128);
-        // (3) digits w = 254 hi + lo = round(32258 q / max q); exact int64 sum w z
+        if (ta == 0) mark(216 + min(sb, 15));
+        // (2) p = exp(x - m), u = p s / max s in [0, 1]; digits w = 254 hi + lo
+        const float inv = m[V_HP] > 0.f ? 127.f / m[V_HP] : 0.f;
         uint8_t* pb = pbuf + buf * VQ_PBUF;
+        const int tl = 2 * ta;
+        const bool live = s0 + tl < ntok;
+        const int blk = tl >> 7, tk = tl & 127;
+        uint8_t* rb = pb + blk * 2048 + (tk & 15);
+        const int z0 = (int)zv.x, z1 = (int)zv.y;  // zero points (integers)
+        float l[V_HP];
         long long zw[V_HP];
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
-          mx[h] = fmaxf(fmaxf(red_f[1][0][h], red_f[1][1][h]), fmaxf(red_f[1][2][h], red_f[1][3][h]));
-          const float inv = mx[h] > 0.f ? 127.f / mx[h] : 0.f;
+          l[h] = 0.f;
           zw[h] = 0;
-#pragma unroll
-          for (int i = 0; i < NP; ++i) {
-            const int tl = 2 * ta + 256 * i;
-            if (h < p.s && s0 + tl < ntok) {
-              const float v0 = q[i][h].x * inv, v1 = q[i][h].y * inv;
-              const float h0 = rintf(v0), h1 = rintf(v1);
-              const float l0 = fminf(fmaxf(rintf((v0 - h0) * 254.f), -127.f), 127.f);
-              const float l1 = fminf(fmaxf(rintf((v1 - h1) * 254.f), -127.f), 127.f);
-              zw[h] += (long long)(254 * (int)h0 + (int)l0) * (long long)zv[i].x +
-                       (long long)(254 * (int)h1 + (int)l1) * (long long)zv[i].y;
-              // K-major SW128: row r, token tk -> 16-byte chunk (tk / 16) ^ (r & 7)
-              const int blk = tl >> 7, tk = tl & 127;
-              uint8_t* rb = pb + blk * 2048 + (tk & 15);
-              *reinterpret_cast<uint16_t*>(rb + h * 128 + ((((tk >> 4) ^ h) & 7) << 4)) =
-                  (uint16_t)((uint8_t)(int)h0 | ((uint32_t)(uint8_t)(int)h1 << 8));
-              *reinterpret_cast<uint16_t*>(rb + (h + 4) * 128 + ((((tk >> 4) ^ (h + 4)) & 7) << 4)) =
-                  (uint16_t)((uint8_t)(int8_t)(int)l0 | ((uint32_t)(uint8_t)(int8_t)(int)l1 << 8));
-            }
+          int w0 = 0, w1 = 0;
+          if (h < p.s && live) {
+            const float p0 = __expf(x[h].x - m[h]), p1 = __expf(x[h].y - m[h]);
+            l[h] = p0 + p1;
+            const float v0 = p0 * sv.x * inv, v1 = p1 * sv.y * inv;
+            const float h0 = rintf(v0), h1 = rintf(v1);
+            const int l0 = (int)fminf(fmaxf(rintf((v0 - h0) * 254.f), -127.f), 127.f);
+            const int l1 = (int)fminf(fmaxf(rintf((v1 - h1) * 254.f), -127.f), 127.f);
+            w0 = 254 * (int)h0 + l0;
+            w1 = 254 * (int)h1 + l1;
+            // K-major SW128: row r, token tk -> 16-byte chunk (tk / 16) ^ (r & 7)
+            *reinterpret_cast<uint16_t*>(rb + h * 128 + ((((tk >> 4) ^ h) & 7) << 4)) =
+                (uint16_t)((uint32_t)(int)h0 | ((uint32_t)(int)h1 << 8));
+            *reinterpret_cast<uint16_t*>(rb + (h + 4) * 128 + ((((tk >> 4) ^ (h + 4)) & 7) << 4)) =
+                (uint16_t)((uint32_t)(uint8_t)(int8_t)l0 | ((uint32_t)(uint8_t)(int8_t)l1 << 8));
+          } else if (live) {
+            *reinterpret_cast<uint16_t*>(rb + h * 128 + ((((tk >> 4) ^ h) & 7) << 4)) = 0;
+            *reinterpret_cast<uint16_t*>(rb + (h + 4) * 128 + ((((tk >> 4) ^ (h + 4)) & 7) << 4)) = 0;
           }
+          zw[h] = -((long long)w0 * z0 + (long long)w1 * z1);  // - sum w z (exact)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (ta == 0) mark(332 + min(sb, 15));
+        // (3) per-warp partial sums; statistics; release this warp's digits
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
           l[h] = warp_reduce(l[h], [](float a, float c) { return a + c; });
 #pragma unroll
           for (int o = 16; o > 0; o >>= 1) zw[h] += __shfl_xor_sync(0xffffffffu, zw[h], o);
-          if (lane == 0) {
-            red_f[0][warp][h] = l[h];
-            red_z[warp][h] = zw[h];
+        }
+        if (lane == 0) {
+#pragma unroll
+          for (int h = 0; h < V_HP; ++h) {
+            stat_l[(buf * VQ_A + warp) * V_HP + h] = l[h];
+            stat_z[(buf * VQ_A + warp) * V_HP + h] = zw[h];
+          }
+          if (warp == 0) {
+#pragma unroll
+            for (int h = 0; h <= V_HP; ++h) stat_m[buf * (V_HP + 1) + h] = m[h];
           }
         }
-        named_bar_sync(3, 128);
-        if (ta < V_HP) {
-          const int h = ta;
-          float mh = m[0], lh = 0.f, sh = 0.f;
-          long long zh = 0;
-#pragma unroll
-          for (int k = 0; k < V_HP; ++k)
-            if (k == h) {
-              mh = m[k];
-              lh = (red_f[0][0][k] + red_f[0][1][k]) + (red_f[0][2][k] + red_f[0][3][k]);
-              sh = mx[k] / VQ_W;
-              zh = (red_z[0][k] + red_z[1][k]) + (red_z[2][k] + red_z[3][k]);
-            }
-          stat[(buf * 3 + 0) * V_HP + h] = mh;
-          stat[(buf * 3 + 1) * V_HP + h] = lh;
-          stat[(buf * 3 + 2) * V_HP + h] = sh;
-          statz[buf * V_HP + h] = zh;
-        }
-        named_bar_sync(3, 128);
-        if (ta == 0) mbar_arrive(&pfull[buf]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&pfull[buf]);  // release: this warp's digits and partials
+        if (ta == 0) mark(200 + min(sb, 15));
       }
     }
   } else {
-    // ---------------- group B: integer sub-block sums -> online softmax -> partial ----------------
-    const int tb = tid - 128, wb = warp - 4;
-    const int mpos = wb * 32 + lane;  // TMEM lane = operand position in a column tile
-    const int col_in = vq_column<BITS>(mpos);
+    // ---------------- group B (warps 8-11): readback -> online softmax -> partial ----------------
+    const int wq = warp & 3, tb = tid - VQ_B0 * 32;  // TMEM lane quarter = warp % 4
+    const int col_in = vq_column<BITS>(wq * 32 + lane);
+    float acc[4][V_HP], mr[V_HP], lr[V_HP];
     VQIter it(i0, i1, n_super);
     int sb = 0;
     while (it.next(bg, s0u, s1u)) {
       const int b = bg / p.G, g = bg - b * p.G;
       const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
       const int nblk = (c1 - c0 + TILE_M - 1) / TILE_M;
-      float acc[4][V_HP], mr[V_HP], lr[V_HP];
-#pragma unroll
-      for (int h = 0; h < V_HP; ++h) {
-        mr[h] = -INFINITY;
-        lr[h] = 0.f;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[j][h] = 0.f;
-      }
       for (int b0 = 0; b0 < nblk; b0 += VQ_NB, ++sb) {
-        const int buf = sb & 1;
-        mbar_wait(&dfull[buf], (sb >> 1) & 1);
-        fence_after();
-        float sc_old[V_HP], sc_new[V_HP], scl[V_HP];
-        long long zw[V_HP];
-#pragma unroll
-        for (int h = 0; h < V_HP; ++h) {
-          const float ms = stat[(buf * 3 + 0) * V_HP + h], ls = stat[(buf * 3 + 1) * V_HP + h];
-          scl[h] = stat[(buf * 3 + 2) * V_HP + h];
-          zw[h] = statz[buf * V_HP + h];
-          const float mn = fmaxf(mr[h], ms);
-          sc_old[h] = mr[h] == -INFINITY ? 0.f : __expf(mr[h] - mn);
-          sc_new[h] = ms == -INFINITY ? 0.f : __expf(ms - mn);
-          lr[h] = lr[h] * sc_old[h] + ls * sc_new[h];
-          mr[h] = mn;
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (j < NJ) {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(wb * 32) << 16) + (uint32_t)((buf * NJ + j) * 16), v);
-            tmem_wait_ld();
-#pragma unroll
-            for (int h = 0; h < V_HP; ++h) {
-              const long long r = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + V_HP]) - zw[h];
-              acc[j][h] = acc[j][h] * sc_old[h] + __ll2float_rn(r) * scl[h] * sc_new[h];
-            }
-          }
-        }
-        fence_before();
-        named_bar_sync(4, 128);
-        if (tb == 0) mbar_arrive(&dempty[buf]);
+        const VQPend q = {sb, b, g, s0u, b0 == 0, b0 + VQ_NB >= nblk};
+        vq_readback<BITS>(p, q, NJ, wq, tb, col_in, tmem, stat_m, stat_l, stat_z, pfull, dfull, dempty,
+                          acc, mr, lr);
       }
-      // the unit's partial (value_merge_kernel layout): slot = first super-tile
-      for (int j = 0; j < NJ && j < 4; ++j) {
-        const int col = j * 128 + col_in;
-#pragma unroll
-        for (int h = 0; h < V_HP; ++h)
-          if (h < p.s)
-            p.pctx[(((size_t)b * p.n_heads + g * p.s + h) * p.ns_cap + s0u) * p.Rv_pad + col] = acc[j][h];
-      }
-#pragma unroll
-      for (int h = 0; h < V_HP; ++h)
-        if (tb == h && h < p.s) {
-          const size_t pi = ((size_t)b * p.n_heads + g * p.s + h) * p.ns_cap + s0u;
-          p.pm[pi] = mr[h];
-          p.pl[pi] = lr[h];
-        }
     }
   }
   fence_before();
   __syncthreads();
-  if (warp == 9) {
+  if (tid == 0) {
+    mark(1);
+    if (tr != nullptr) tr[3] = 2000000ull + (unsigned long long)(i1 - i0);
+  }
+  if (warp == VQ_MMA) {
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(VQ_TMEM));
   }

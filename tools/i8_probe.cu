@@ -80,7 +80,85 @@ __global__ void probe(const uint8_t* C, const int8_t* P, int* out) {
   }
 }
 
+// back-to-back MMA issue rate: ITERS x 4 MMAs on fixed operands, one CTA per SM
+template <int KIND, int N>  // KIND 0: kind::i8 (K 32), 1: kind::f16 bf16 (K 16)
+__global__ void rate(int iters, float* out) {
+  extern __shared__ __align__(1024) uint8_t raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sm + 65536);
+  uint32_t* slot = reinterpret_cast<uint32_t*>(bar + 2);
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 65536 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x01020304u * (i & 7);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *slot;
+  if (tid == 0) {
+    const uint32_t a = smem_u32(sm), b = smem_u32(sm + 32768);
+    const long long c0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        if (KIND == 0) {
+          constexpr uint32_t ID = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                       "l"(sdesc_mn(a + kk * 4096, 16384, 1024)), "l"(sdesc(b + kk * 32)), "r"(ID), "r"(1)
+                       : "memory");
+        } else {
+          constexpr uint32_t ID = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+          asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                       "l"(sdesc_mn(a + kk * 2048, 16384, 1024)), "l"(sdesc(b + kk * 32)), "r"(ID), "r"(1)
+                       : "memory");
+        }
+      }
+    }
+    umma_commit(&bar[0]);
+    mbar_wait(&bar[0], 0);
+    if (blockIdx.x == 0) out[0] = (float)(clock64() - c0) / (4.f * iters);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  }
+}
+
+template <int KIND, int N>
+static void run_rate(const char* name) {
+  float* d;
+  cudaMalloc(&d, 4);
+  cudaFuncSetAttribute(rate<KIND, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024);
+  rate<KIND, N><<<148, 128, 70 * 1024>>>(2000, d);
+  cudaDeviceSynchronize();
+  rate<KIND, N><<<148, 128, 70 * 1024>>>(20000, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  float h = 0;
+  cudaMemcpy(&h, d, 4, cudaMemcpyDeviceToHost);
+  printf("rate %-22s N %3d: %6.1f SM clocks per MMA (%s)\n", name, N, h, cudaGetErrorString(e));
+  cudaFree(d);
+}
+
 int main() {
+  run_rate<0, 8>("i8 M128 K32");
+  run_rate<0, 16>("i8 M128 K32");
+  run_rate<0, 32>("i8 M128 K32");
+  run_rate<0, 64>("i8 M128 K32");
+  run_rate<0, 128>("i8 M128 K32");
+  run_rate<1, 16>("bf16 M128 K16 (MN A)");
+  run_rate<1, 64>("bf16 M128 K16 (MN A)");
+  run_rate<1, 256>("bf16 M128 K16 (MN A)");
   std::vector<uint8_t> C(128 * 128);
   std::vector<int8_t> P(16 * 128);
   srand(7);
