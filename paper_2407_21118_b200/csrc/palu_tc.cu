@@ -258,21 +258,34 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
 // whose rows 128 r .. land in SM r's TMEM.  Each SM's epilogue reduces its
 // own 128 tokens x 2 heads per head pair.  Every latent byte crosses L2 -> SM
 // once and both SMs' tensor pipes run at the 2-SM rate.
+// UH = heads per accumulator unit.  UH 2: one M256 x N256 MMA covers a head
+// pair (each SM holds the UW rows of one head), 2 TMEM slots of 256 columns.
+// UH 1: one M256 x N128 MMA per head (each SM holds half of every head's UW
+// rows: u_j on the leader, w_j on the peer), 4 slots of 128 columns -- for
+// short ranks (r <= 128: 8 MMAs per unit) the accumulator must be quad-
+// buffered to cover the ~1 us from a unit's last MMA issue to its epilogue
+// (tools/score_trace.py: 2 slots left the tensor pipe ~45 % idle at r 128).
+template <int UH>
 __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUtensorMap& map_uw,
                                            const Params& p, uint8_t* smem) {
+  constexpr int NSLOT = UH == 2 ? 2 : 4;
+  constexpr int SLOT_COLS = 128 * UH;
+  constexpr int UWB = HEAD_BYTES / 2 * UH;               // UW bytes per (k-block, unit) per SM
+  constexpr uint32_t IDESC_U = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(SLOT_COLS >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
   const int kblocks = p.R_pad / KB;
-  const int halves = p.s_k / 2;
-  uint8_t* s_uw = smem;                                  // [kblocks][halves] x 16 KB
-  uint8_t* s_h = smem + kblocks * halves * HEAD_BYTES;   // stages x 16 KB
+  const int units = p.s_k / UH;                          // accumulator units per item
+  uint8_t* s_uw = smem;                                  // [kblocks][units] x UWB
+  uint8_t* s_h = smem + kblocks * units * UWB;           // stages x 16 KB
   uint64_t* bars = reinterpret_cast<uint64_t*>(s_h + p.stages * H_STAGE_BYTES);
   uint64_t* full = bars;                                 // [stages]   (leader's used)
   uint64_t* empty = bars + p.stages;                     // [stages]   (each SM's own)
-  uint64_t* tfull = bars + 2 * p.stages;                 // [2]        (each SM's own)
-  uint64_t* tempty = tfull + 2;                          // [2]        (leader's used)
-  uint64_t* uw_full = tempty + 2;                        // [1]        (leader's used)
+  uint64_t* tfull = bars + 2 * p.stages;                 // [NSLOT]    (each SM's own)
+  uint64_t* tempty = tfull + NSLOT;                      // [NSLOT]    (leader's used)
+  uint64_t* uw_full = tempty + NSLOT;                    // [1]        (leader's used)
   uint64_t* uw_empty = uw_full + 1;                      // [1]        (each SM's own)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(uw_empty + 1);
-  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [2 slots][2 heads][128]
+  float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [NSLOT][UH heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -295,7 +308,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       mbar_init(&full[s], p.bits == 16 ? 1 : 2 * CONV_WARPS);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NSLOT; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 2 * EPI_WARPS);
     }
@@ -315,8 +328,10 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0)
+  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0) {
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = gtimer();
+    p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 511] = clock64();  // per-unit marks are SM clocks
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -341,11 +356,12 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         const int bg = ip_.bg, st = ip_.st;
         if (bg != cur) {
           if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
-          if (leader) mbar_expect_tx(uw_full, 2 * kblocks * halves * HEAD_BYTES);
+          if (leader) mbar_expect_tx(uw_full, 2 * kblocks * units * UWB);
           for (int kb = 0; kb < kblocks; ++kb)
-            for (int h = 0; h < halves; ++h)
-              tma_load_2d_pair(&map_uw, uw_full, s_uw + (kb * halves + h) * HEAD_BYTES, kb * KB,
-                               (bg * p.s_k + 2 * h + (int)rank) * 128);
+            for (int h = 0; h < units; ++h)
+              tma_load_2d_pair(&map_uw, uw_full, s_uw + (kb * units + h) * UWB, kb * KB,
+                               UH == 2 ? (bg * p.s_k + 2 * h + (int)rank) * 128
+                                       : (bg * p.s_k + h) * 128 + 64 * (int)rank);
           ++nloads;
           cur = bg;
         }
@@ -376,8 +392,11 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       // ---------------- MMA issuer (leader SM issues for the pair) ----------------
+      // The whole warp runs the loop (warp-uniform descriptors stay in uniform
+      // registers); one elected lane -- always the same one, so its commits
+      // track its own MMAs -- issues the tcgen05 instructions.
       const uint32_t uw_addr = smem_u32(s_uw);
       const uint32_t h_addr = smem_u32(s_h);
       int cur = -1, nloads = 0, unit = 0;
@@ -390,19 +409,19 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       for (int i = i0; i < i1; ++i, ip_.next(n_super, p.G)) {
         const int bg = ip_.bg;
         if (bg != cur) {
-          if (nloads > 0) umma2_commit_both(uw_empty);  // frees UW in both SMs
+          if (nloads > 0 && elect_one()) umma2_commit_both(uw_empty);  // frees UW in both SMs
           mbar_wait(uw_full, nloads & 1);
           fence_after();
           ++nloads;
           cur = bg;
         }
-        for (int h = 0; h < halves; ++h, ++unit) {
-          const int slot = unit & 1;
-          if ((p.mode & 4) == 0) mbar_wait(&tempty[slot], ((unit >> 1) & 1) ^ 1);
+        for (int h = 0; h < units; ++h, ++unit) {
+          const int slot = unit & (NSLOT - 1);
+          if ((p.mode & 4) == 0) mbar_wait(&tempty[slot], ((unit / NSLOT) & 1) ^ 1);
           fence_after();
-          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE)
-            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 4 * unit] = gtimer();
-          const uint32_t d_tmem = tmem_base + slot * N_CTA;
+          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE && lane == 0)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 4 * unit] = clock64();
+          const uint32_t d_tmem = tmem_base + slot * SLOT_COLS;
           for (int kb = 0; kb < kblocks; ++kb) {
             int stage = st0 + kb, par = ph0;
             if (stage >= p.stages) {  // kblocks <= stages: at most one wrap
@@ -415,18 +434,22 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             }
             // profile modes 8 / 16 (diagnostics): pin the A / B operand tile
             const uint32_t a0 = h_addr + ((p.mode & 8) ? 0 : stage) * H_STAGE_BYTES;
-            const uint32_t b0 = uw_addr + ((p.mode & 16) ? 0 : (kb * halves + h)) * HEAD_BYTES;
+            const uint32_t b0 = uw_addr + ((p.mode & 16) ? 0 : (kb * units + h)) * UWB;
             // K16 steps are 32 B apart: +2 in the descriptor's address field
             // (smem addresses < 256 KB, so the 14-bit field cannot carry)
             const uint64_t da = sdesc(a0), db = sdesc(b0);
+            if (elect_one()) {
 #pragma unroll
-            for (int kk = 0; kk < KB / 16; ++kk)
-              umma2_bf16(d_tmem, da + 2 * kk, db + 2 * kk, (kb | kk) != 0);
-            if (h == halves - 1) umma2_commit_both(&empty[stage]);
+              for (int kk = 0; kk < KB / 16; ++kk)
+                umma2_bf16_id(d_tmem, da + 2 * kk, db + 2 * kk, IDESC_U, (kb | kk) != 0);
+              if (h == units - 1) umma2_commit_both(&empty[stage]);
+            }
+            __syncwarp();
           }
-          umma2_commit_both(&tfull[slot]);
-          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE)
-            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = gtimer();
+          if (elect_one()) umma2_commit_both(&tfull[slot]);
+          __syncwarp();
+          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE && lane == 0)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = clock64();
         }
         st0 += kblocks;
         if (st0 >= p.stages) {
@@ -434,7 +457,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           ph0 ^= 1;
         }
       }
-      if (p.trace != nullptr && p.ready == nullptr) {  // SM clocks vs wall time of the issue loop
+      if (p.trace != nullptr && p.ready == nullptr && lane == 0) {  // SM clocks vs wall time of the issue loop
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 508] = clock64() - c_start;
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 509] = gtimer() - g_start;
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 510] = (unsigned long long)unit * kblocks * (KB / 16);
@@ -511,22 +534,22 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           s2[k] = ffma2(bsn, cd2[k], fmul2(bc, sd2[k]));
         }
       }
-      for (int h = 0; h < halves; ++h, ++unit) {
-        const int slot = unit & 1;
-        mbar_wait(&tfull[slot], (unit >> 1) & 1);
+      for (int h = 0; h < units; ++h, ++unit) {
+        const int slot = unit & (NSLOT - 1);
+        mbar_wait(&tfull[slot], (unit / NSLOT) & 1);
         fence_after();
         const bool tr = p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 &&
                         4 * unit + 7 < TRACE_STRIDE;
-        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + 4 * unit] = gtimer();
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + 4 * unit] = clock64();
         float v[2] = {0.f, 0.f};
         if ((p.mode & 1) == 0)
 #pragma unroll
-        for (int hp = 0; hp < 2; ++hp) {
+        for (int hp = 0; hp < UH; ++hp) {
           float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
           for (int jc = 0; jc < 2; ++jc) {
             float u[16], w[16];
-            const uint32_t col = slot * N_CTA + hp * 128 + jh * 32 + jc * 16;
+            const uint32_t col = slot * SLOT_COLS + hp * 128 + jh * 32 + jc * 16;
             tmem_ld16(lane_base + col, u);
             tmem_ld16(lane_base + col + 64, w);
             tmem_wait_ld();
@@ -538,33 +561,36 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           }
           v[hp] = acc2.x + acc2.y;
         }
-        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + 4 * unit] = gtimer();
-        float* r = red + slot * 2 * TILE_M;
+        // (staging the whole unit in registers to release the slot earlier
+        // needs 128 more registers than the 168 this kernel gets: it spilled)
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + 4 * unit] = clock64();
+        float* r = red + slot * UH * TILE_M;
         if (jh == 1) {
           r[delta] = v[0];
-          r[TILE_M + delta] = v[1];
+          if (UH == 2) r[TILE_M + delta] = v[1];
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           named_bar_arrive(1 + slot, EPI_WARPS * 32);
         } else {
           named_bar_sync(1 + slot, EPI_WARPS * 32);
-          const float v0 = v[0] + r[delta], v1 = v[1] + r[TILE_M + delta];
+          const float v0 = v[0] + r[delta], v1 = UH == 2 ? v[1] + r[TILE_M + delta] : 0.f;
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           const int t = tile * TILE_M + delta;
           if (t < T_rows) {
-            // D columns 0..127 = head 2h (leader's UW rows), 128..255 = head 2h + 1
-            const int head0 = g * p.s_k + 2 * h;
+            // UH 2: D columns 0..127 = head 2h (leader's UW rows), 128..255 =
+            // head 2h + 1; UH 1: columns 0..63 u_j (leader), 64..127 w_j (peer)
+            const int head0 = g * p.s_k + UH * h;
             float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
             lg[0] = v0 * sq;
-            lg[p.ld_logits] = v1 * sq;
+            if (UH == 2) lg[p.ld_logits] = v1 * sq;
           }
-          if (p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == halves - 1 &&
+          if (p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == units - 1 &&
               it < TRACE_STRIDE - 8)
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + it] = gtimer();
-          if (p.ready != nullptr && h == halves - 1) {
+          if (p.ready != nullptr && h == units - 1) {
             // publish this warp's logits of the item to the value role
             __threadfence();
             __syncwarp();
@@ -587,6 +613,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   }
 }
 
+template <int UH>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
@@ -600,7 +627,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  score_role(map_h, map_uw, p, smem);
+  score_role<UH>(map_h, map_uw, p, smem);
 }
 
 // ===========================================================================
@@ -1373,7 +1400,7 @@ rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
   }
   if ((int)(blockIdx.x >> 1) < p.score_pairs) {
-    score_role(map_h, map_uw, p, smem);
+    score_role<2>(map_h, map_uw, p, smem);
   } else {
     const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
     value_role(map_v, p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
@@ -1859,18 +1886,25 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   int rc = bits == 16 ? make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M)
                       : make_map_u8(&map_h, hk, row_bytes, (uint64_t)B * G * T_cap);
   if (rc) return rc;
-  rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, TILE_M);
-  if (rc) return rc;
   const int kblocks = R_pad / KB;
-  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + 256 +
-                    2 * 2 * TILE_M * 4;
+  // heads per accumulator unit: 1 (quad-buffered N128) for short ranks
+  // (UH 1 measured slower at r 128: an N128 pair-MMA costs as much as an N256
+  // one, tools/score_trace.py; kept as an option)
+  const int uh = getenv("PALU_SCORE_UH") ? atoi(getenv("PALU_SCORE_UH")) : 2;
+  PALU_REQUIRE(uh == 1 || uh == 2, "PALU_SCORE_UH must be 1 or 2");
+  rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, uh == 2 ? TILE_M : 64);
+  if (rc) return rc;
+  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + 512 +
+                    4 * 2 * TILE_M * 4;
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
   PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
   const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
   static bool attr = false;
   if (!attr) {
-    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_LIMIT));
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_LIMIT));
     attr = true;
   }
@@ -1910,8 +1944,12 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
     prm.trace = g_trace;
     g_trace_ctas = sms & ~1;
   }
-  PALU_CK(launch_k(rope_score_tc_kernel, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream, map_h,
-                   map_uw, prm));
+  if (uh == 1)
+    PALU_CK(launch_k(rope_score_tc_kernel<1>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+                     map_h, map_uw, prm));
+  else
+    PALU_CK(launch_k(rope_score_tc_kernel<2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+                     map_h, map_uw, prm));
   PALU_LAUNCHED();
   return PALU_OK;
 }
@@ -2028,8 +2066,8 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   rc = make_map_2d(&map_uw, uw, Rk_pad, (uint64_t)B * G * s * 128, KB, TILE_M);
   if (rc) return rc;
   const int kblocks = Rk_pad / KB;
-  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + 256 +
-                    2 * 2 * TILE_M * 4;
+  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + 512 +
+                    4 * 2 * TILE_M * 4;
   const int dyn_limit = SMEM_LIMIT - 2048;  // the value role has ~1 KB of static smem
   int stages = (dyn_limit - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;

@@ -50,21 +50,14 @@ def main():
     ent, setup, end = (tr[:, 0] - t0) / 1e3, (tr[:, 2] - t0) / 1e3, (tr[:, 1] - t0) / 1e3
     pc = lambda x: np.percentile(x, [0, 50, 100]).round(2)
     print(f"CTA entry us min/med/max {pc(ent)}; setup done {pc(setup)}; exit {pc(end)}")
-    firsts, lasts = [], []
-    for cta in range(0, n, 2):
-        if tr[cta, 4] > 0:
-            firsts.append((tr[cta, 4] - t0) / 1e3)
-            u = int(tr[cta, 3]) * 2 - 1
-            while u >= 0 and (4 * u + 7 >= 512 or tr[cta, 7 + 4 * u] == 0):
-                u -= 1
-            lasts.append((tr[cta, 7 + 4 * u] - t0) / 1e3)
-    print(f"first MMA {pc(np.array(firsts))}; last epilogue done {pc(np.array(lasts))}")
+
     ld = [i for i in range(0, n, 2) if tr[i, 509] > 0]
     clk = np.array([tr[i, 508] for i in ld], dtype=float)
     ns = np.array([tr[i, 509] for i in ld], dtype=float)
     mm = np.array([tr[i, 510] for i in ld], dtype=float)
     print(f"MMA loop: SM clock {np.median(clk / ns):.3f} GHz, {np.median(clk / mm):.0f} clk and "
           f"{np.median(ns / mm):.1f} ns per pair-MMA (ideal 128 clk)")
+    ghz = float(np.median(clk / ns)) if len(ld) else 1.9
     rows = []
     for cta in range(0, n, 2):  # leaders
         u = 0
@@ -76,25 +69,27 @@ def main():
     if not len(r):
         print("no trace")
         return
-    mma_issue = (r[:, 3] - r[:, 2]) / 1e3
+    # per-unit marks are SM clock64 values (cycles); convert with the measured clock
+    mma_issue = (r[:, 3] - r[:, 2]) / ghz / 1e3
     for par in (0, 1):
         sel = r[:, 1] % 2 == par
         print(f"  unit parity {par} (half h={par}): issue span p50 {np.median(mma_issue[sel]):.3f} us")
-    epi_lat = (r[:, 4] - r[:, 3]) / 1e3     # commit -> epilogue wake (MMA execution + signal)
-    epi_dur = (r[:, 5] - r[:, 4]) / 1e3     # epilogue work on the slot
+    epi_lat = (r[:, 4] - r[:, 3]) / ghz / 1e3   # commit -> epilogue wake (other SM's clock: approx.)
+    epi_dur = (r[:, 5] - r[:, 4]) / ghz / 1e3   # epilogue work on the slot
     gaps = []
     for cta in np.unique(r[:, 0]):
         rr = r[r[:, 0] == cta]
-        gaps += list((rr[1:, 2] - rr[:-1, 3]) / 1e3)  # MMA idle between units (waiting slot/data)
+        gaps += list((rr[1:, 2] - rr[:-1, 3]) / ghz / 1e3)  # MMA idle between units (slot/data)
     pct = lambda x: np.percentile(x, [10, 50, 90]).round(3)
     print(f"units {len(r)}: MMA issue span us p10/50/90 {pct(mma_issue)}")
     print(f"  commit->epilogue wake {pct(epi_lat)}; epilogue on slot {pct(epi_dur)}")
     print(f"  MMA idle between units {pct(np.array(gaps))}")
     cta = r[0, 0]
-    rr = r[r[:, 0] == cta][:8]
+    c0 = tr[cta, 511]
+    rr = r[r[:, 0] == cta][:12]
+    us = lambda v: round((v - c0) / ghz / 1e3, 2)
     for x in rr:
-        print("  unit", x[1], "mma", round((x[2] - t0) / 1e3, 2), "->", round((x[3] - t0) / 1e3, 2),
-              "epi", round((x[4] - t0) / 1e3, 2), "->", round((x[5] - t0) / 1e3, 2))
+        print("  unit", x[1], "mma", us(x[2]), "->", us(x[3]), "epi", us(x[4]), "->", us(x[5]))
 
 
 if __name__ == "__main__":
