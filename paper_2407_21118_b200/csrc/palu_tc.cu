@@ -2164,8 +2164,9 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
 // Packed V (2/4/8-bit codes) on the int8 tensor pipe (palu_vq.cuh), then the
 // deterministic merge.  PALU_VALUE_KERNEL=tc_quant_bf16 keeps the earlier
 // converter-to-bf16 kernel (A/B timing).
-static bool value_q_enabled() {
+static bool value_q_enabled(int bits) {
   const char* e = getenv("PALU_VALUE_KERNEL");
+  if (bits == 16) return !(e && strcmp(e, "tc_bf16_role") == 0);  // earlier bf16 value role
   return !(e && strcmp(e, "tc_quant_bf16") == 0);
 }
 
@@ -2178,18 +2179,13 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
                "palu_value_tc (int8 pipe): unsupported shape (Rv %d, s %d)", Rv_pad, s);
   PALU_REQUIRE(T_cap % TILE_M == 0, "palu_value_tc: packed V needs T_cap %% 128 == 0 (got %d)", T_cap);
   const int row_bytes = Rv_pad * bits / 8;
-  const int box_bytes = row_bytes <= 256 ? row_bytes : 128;  // tensor map (kept for tools)
-  PALU_REQUIRE(row_bytes % box_bytes == 0, "palu_value_tc: row of %d bytes", row_bytes);
-  EncodeTiledFn fn = encode_fn();
-  PALU_REQUIRE(fn != nullptr, "cuTensorMapEncodeTiled unavailable");
+  // packed codes move as 1-D bulk copies (the tensor map is unused); raw bf16
+  // rows as {64 columns, 128 tokens} SW128 boxes straight into the operand
   CUtensorMap map_c = {};
-  const cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)B * G * T_cap};
-  const cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
-  const cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)TILE_M}, es[2] = {1, 1};
-  CUresult r = fn(&map_c, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(hv), dims, strides, box,
-                  es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  PALU_REQUIRE(r == CUDA_SUCCESS, "palu_value_tc: code tensor map failed (%d)", (int)r);
+  if (bits == 16) {
+    const int rc = make_map_2d(&map_c, hv, Rv_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
+    if (rc) return rc;
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -2224,29 +2220,42 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
   const int RB = TILE_M * row_bytes;
   const int dyn_limit = SMEM_LIMIT - 2048;
   // operand ring slots hold whole blocks (NJ column tiles); 2-4 of them, the
-  // raw code ring (bulk-copy landing zone) takes the rest, at most 6 blocks
+  // raw code ring (bulk-copy landing zone) takes the rest, at most 6 blocks.
+  // bf16: no raw ring, the operand ring holds up to 8 tiles of 32 KB
   const int NJ = Rv_pad / 128;
-  const int OB = NJ * VQ_STAGE;
+  const int OB = bits == 16 ? VQ_BSTAGE : NJ * VQ_STAGE;
   const int RS = RB;  // raw slot: the block's codes
-  const int misc = 1024 + 2 * VQ_PBUF + (2 * (V_HP + 1) + 2) * 4 + 2 * VQ_A * V_HP * (4 + 8) + 6 * 8 + 16;
-  p.stages = (dyn_limit - misc - 2 * (RS + 16)) / (OB + 16);
-  if (p.stages > 4) p.stages = 4;
-  PALU_REQUIRE(p.stages >= 2, "palu_value_tc (int8 pipe): operand ring too small (%d)", p.stages);
-  p.raw_slots = (dyn_limit - misc - p.stages * (OB + 16)) / (RS + 16);
-  if (p.raw_slots > 6) p.raw_slots = 6;
-  PALU_REQUIRE(p.raw_slots >= 2, "palu_value_tc (int8 pipe): raw ring too small (%d)", p.raw_slots);
+  const int pbuf = VQ_NB * (bits == 16 ? 4096 : 2048);
+  const int misc = 1024 + 2 * pbuf + (2 * (V_HP + 1) + 2) * 4 + 2 * VQ_A * V_HP * (4 + 4) + 6 * 8 + 16;
+  if (bits == 16) {
+    p.raw_slots = 0;
+    p.stages = (dyn_limit - misc) / (OB + 16);
+    if (p.stages > 8) p.stages = 8;
+    PALU_REQUIRE(p.stages >= 2, "palu_value_tc (bf16): operand ring too small (%d)", p.stages);
+  } else {
+    // two operand blocks (the MMA drains a block in ~0.3 us); the raw ring --
+    // bytes in flight per SM -- takes the rest (2 slots left the converters
+    // waiting ~1 us per block on bulk-copy latency at r_v 384)
+    p.stages = 2;
+    p.raw_slots = (dyn_limit - misc - p.stages * (OB + 16)) / (RS + 16);
+    if (p.raw_slots > 6) p.raw_slots = 6;
+    PALU_REQUIRE(p.raw_slots >= 2, "palu_value_tc (int8 pipe): raw ring too small (%d)", p.raw_slots);
+  }
   const size_t smem = (size_t)misc + (size_t)p.raw_slots * (RS + 16) + (size_t)p.stages * (OB + 16);
   static bool attr = false;
   if (!attr) {
     PALU_CK(cudaFuncSetAttribute(value_q_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
     PALU_CK(cudaFuncSetAttribute(value_q_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
     PALU_CK(cudaFuncSetAttribute(value_q_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
+    PALU_CK(cudaFuncSetAttribute(value_q_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_limit));
     attr = true;
   }
   if (bits == 2)
     PALU_CK(launch_k(value_q_kernel<2>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
   else if (bits == 4)
     PALU_CK(launch_k(value_q_kernel<4>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
+  else if (bits == 16)
+    PALU_CK(launch_k(value_q_kernel<16>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
   else
     PALU_CK(launch_k(value_q_kernel<8>, dim3(sms), dim3(VQ_THREADS), smem, st, map_c, p));
   PALU_LAUNCHED();
@@ -2267,7 +2276,8 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
   }
   PALU_REQUIRE(((uintptr_t)hv & 15) == 0, "palu_value_tc: unaligned H_v");
   PALU_REQUIRE(bits == 16 || (scales && zps), "palu_value_tc: quantised values need scales/zps");
-  if ((bits == 2 || bits == 4 || bits == 8) && value_q_enabled())
+  if ((bits == 2 || bits == 4 || bits == 8 || (bits == 16 && Rv_pad % 128 == 0)) &&
+      value_q_enabled(bits))
     return launch_value_q(bits, hv, scales, zps, B, n_heads, s, G, Rv_pad, T_cap, logits, ld_logits,
                           t_dev, ranks_v, o_off, ctx, ld_ctx, workspace, (cudaStream_t)stream);
   CUtensorMap map_v = {};

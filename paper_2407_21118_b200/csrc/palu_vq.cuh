@@ -23,6 +23,12 @@
 // per-byte subtraction costs the converters more than the term costs group A.)  An online softmax across sub-blocks and
 // the deterministic value_merge_kernel complete the path.
 //
+// Raw bf16 values (BITS 16) take the same pipeline without converters: the
+// producer TMA-loads {64 columns x 128 tokens} SW128 boxes straight into the
+// MN-major operand (one 32 KB stage per 128-column tile), the digits are the
+// bf16 pair hi = bf16(p), lo = bf16(p - hi) (~16 significant bits), and
+// kind::f16 MMAs accumulate fp32 in TMEM.
+//
 // Bytes streamed: the packed codes (one 1-D bulk copy per 128-token block,
 // L2-prefetched ahead), per-token scales and zero points, and the logits: the HBM-bound stream the north star names, with no bf16 staging.
 //
@@ -39,7 +45,9 @@ constexpr int VQ_A = 6, VQ_B0 = 6, VQ_CV0 = 10, VQ_CONV = 4, VQ_PROD = 14, VQ_MM
 constexpr int VQ_THREADS = (VQ_MMA + 1) * 32;
 constexpr int VQ_SUB = 384;                 // tokens per digit sub-block (one pair per group-A thread)
 constexpr int VQ_NB = VQ_SUB / TILE_M;      // 128-token blocks per sub-block
-constexpr int VQ_PBUF = VQ_NB * 2048;       // digits: per block 16 rows x 128 B
+// digits per block: 16 rows x 128 tokens of s8 (2 KB) or bf16 (4 KB)
+template <int BITS>
+constexpr int vq_pblk() { return BITS == 16 ? 4096 : 2048; }
 constexpr int VQ_STAGE = TILE_M * 128;      // one (block, 128-column tile) u8 operand;
                                             // an operand ring slot holds NJ of them
 constexpr int VQ_TMEM = 128;                // 2 buffers x up to 4 tiles x 16 columns
@@ -48,6 +56,10 @@ constexpr float VQ_W = 127.f * 254.f;       // digit weight scale
 // D s32, A u8 (codes, MN-major), B s8 (digits, K-major), M 128, N 16
 constexpr uint32_t IDESC_Q = (2u << 4) | (0u << 7) | (1u << 10) | (1u << 15) |
                              ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+// raw bf16 values: D f32, A bf16 (MN-major), B bf16 (K-major), M 128, N 16
+constexpr uint32_t IDESC_QB = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 15) |
+                              ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+constexpr int VQ_BSTAGE = TILE_M * 256;    // bf16: one (block, 128-column tile) stage, two 64-col boxes
 
 struct VQParams {
   int B, n_heads, s, G, Rv_pad, T_cap, ld_logits;
@@ -115,7 +127,7 @@ struct VQPend {
 template <int BITS>
 __device__ __forceinline__ void vq_readback(const VQParams& p, const VQPend& q, int NJ, int warp, int ta,
                                           int col_in, uint32_t tmem, const float* stat_m,
-                                          const float* stat_l, const long long* stat_z,
+                                          const float* stat_l, const float* stat_z,
                                           uint64_t* pfull, uint64_t* dfull, uint64_t* dempty,
                                           float (&acc)[4][V_HP], float (&mr)[V_HP], float (&lr)[V_HP]) {
     const int buf = q.sb & 1;
@@ -132,13 +144,13 @@ __device__ __forceinline__ void vq_readback(const VQParams& p, const VQPend& q, 
       }
     }
     float sc_old[V_HP], sc_new[V_HP];
-    long long zw[V_HP];
+    float zw[V_HP];
     const float scl = stat_m[buf * (V_HP + 1) + V_HP] / VQ_W;
 #pragma unroll
     for (int h = 0; h < V_HP; ++h) {
       const float ms = stat_m[buf * (V_HP + 1) + h];
       float ls = 0.f;
-      zw[h] = 0;
+      zw[h] = 0.f;
 #pragma unroll
       for (int w = 0; w < VQ_A; ++w) {
         ls += stat_l[(buf * VQ_A + w) * V_HP + h];
@@ -158,8 +170,13 @@ __device__ __forceinline__ void vq_readback(const VQParams& p, const VQPend& q, 
         tmem_wait_ld();
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
-          const long long r = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + V_HP]) + zw[h];
-          acc[j][h] = acc[j][h] * sc_old[h] + __ll2float_rn(r) * scl * sc_new[h];
+          if constexpr (BITS == 16) {
+            acc[j][h] = acc[j][h] * sc_old[h] + (v[h] + v[h + V_HP]) * sc_new[h];
+          } else {
+            // exact integer sum of the two digit planes, then the zero-point term
+            const long long r = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + V_HP]);
+            acc[j][h] = acc[j][h] * sc_old[h] + (__ll2float_rn(r) + zw[h]) * scl * sc_new[h];
+          }
         }
       }
     }
@@ -198,15 +215,17 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
   const int NJ = p.Rv_pad / 128;
   const int RB = TILE_M * p.row_bytes;
   const int RS = RB;                                             // raw slot: the block's codes
-  const int OB = NJ * VQ_STAGE;                                  // operand bytes per block
+  // operand ring slot: a whole block of u8 tiles; bf16: one 32 KB tile
+  const int OB = BITS == 16 ? VQ_BSTAGE : NJ * VQ_STAGE;
   uint8_t* ring = smem;                                          // stages x OB
   uint8_t* pbuf = ring + p.stages * OB;                          // 2 x 8 KB digits
-  uint8_t* raw = pbuf + 2 * VQ_PBUF;                             // raw_slots x RS
+  constexpr int PBLK = vq_pblk<BITS>(), PBUF = VQ_NB * PBLK;
+  uint8_t* raw = pbuf + 2 * PBUF;                                // raw_slots x RS
   // per sub-block buffer: max logit per head + max scale (group A), and
   // per-warp partial sums of p and of the int64 zero-point term
   float* stat_m = reinterpret_cast<float*>(raw + (size_t)p.raw_slots * RS);  // [2][V_HP + 1]
   float* stat_l = stat_m + 2 * (V_HP + 1) + 2;                               // [2][VQ_A][V_HP]
-  long long* stat_z = reinterpret_cast<long long*>(stat_l + 2 * VQ_A * V_HP);  // [2][VQ_A][V_HP]
+  float* stat_z = stat_l + 2 * VQ_A * V_HP;                                  // [2][VQ_A][V_HP]
   uint64_t* full = reinterpret_cast<uint64_t*>(stat_z + 2 * VQ_A * V_HP);
   uint64_t* empty = full + p.stages;
   uint64_t* rfull = empty + p.stages;
@@ -226,7 +245,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
 
   if (tid == 0) {
     for (int st = 0; st < p.stages; ++st) {
-      mbar_init(&full[st], VQ_CONV);  // one arrive per converter warp
+      mbar_init(&full[st], BITS == 16 ? 1 : VQ_CONV);  // TMA tx | one arrive per converter warp
       mbar_init(&empty[st], 1);
     }
     for (int r = 0; r < p.raw_slots; ++r) {
@@ -241,9 +260,11 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // digit rows 8..15 of every block stay zero (N = 16 > 4 heads x 2 digits)
-  for (int i = tid; i < 2 * VQ_NB * 64; i += VQ_THREADS) {
-    const int blk = i >> 6, w = i & 63;
-    reinterpret_cast<uint4*>(pbuf + blk * 2048 + 1024)[w] = make_uint4(0u, 0u, 0u, 0u);
+  // (u8 digits: per block one 1 KB group of 8 rows each; bf16 digits: per
+  // 64-token atom of a block)
+  for (int i = tid; i < 2 * PBUF / 2048 * 64; i += VQ_THREADS) {
+    const int a = i >> 6, w = i & 63;
+    reinterpret_cast<uint4*>(pbuf + a * 2048 + 1024)[w] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (warp == VQ_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -290,7 +311,28 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         pc += TILE_M;
       };
       for (int k = 0; k < VQ_PF; ++k) prefetch_next();
-      while (it.next(bg, s0u, s1u)) {
+      if constexpr (BITS == 16) prefetch_map(&map_c);
+      while (BITS == 16 && it.next(bg, s0u, s1u)) {
+        // raw bf16: per block and 128-column tile two {64 col, 128 token} SW128
+        // boxes straight into the MN-major operand stage
+        const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
+        for (int t0 = c0; t0 < c1; t0 += TILE_M) {
+          prefetch_next();
+          if (!waited && t0 + TILE_M >= T_rows) {
+            pdl_wait();
+            waited = true;
+          }
+          mark(8 + min(kblk++, 47));
+          for (int j = 0; j < NJ; ++j, rg.next(p.stages)) {
+            mbar_wait(&empty[rg.slot], rg.phase ^ 1);
+            mbar_expect_tx(&full[rg.slot], VQ_BSTAGE);
+            uint8_t* dst = ring + (size_t)rg.slot * OB;
+            tma_load_2d(&map_c, &full[rg.slot], dst, j * 128, bg * p.T_cap + t0);
+            tma_load_2d(&map_c, &full[rg.slot], dst + VQ_BSTAGE / 2, j * 128 + 64, bg * p.T_cap + t0);
+          }
+        }
+      }
+      while (BITS != 16 && it.next(bg, s0u, s1u)) {
         const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
         for (int t0 = c0; t0 < c1; t0 += TILE_M) {
           prefetch_next();
@@ -310,12 +352,25 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       }
     }
   } else if (warp >= VQ_CV0 && warp < VQ_CV0 + VQ_CONV) {
+    if constexpr (BITS != 16) {
     // ---------------- converters: packed block -> u8 MN-major SW128 tiles ----------------
     // work item (row, q) = 16-byte raw chunk q of the row's slice of column
     // tile j; RCR consecutive lanes share a row (conflict-free raw reads)
     constexpr int RCR = BITS;                     // raw chunks per row per 128 columns
     constexpr int RC = RCR * TILE_M / (VQ_CONV * 32);  // items per thread per column tile
+    constexpr int OC = 8 / BITS;                  // output 16-byte chunks per raw chunk
     const int ct = tid - VQ_CV0 * 32;
+    // per-thread item geometry is the same for every block and column tile:
+    // raw source offsets and swizzled destination offsets, computed once
+    uint32_t src_off[RC], dst_off[RC][OC];
+#pragma unroll
+    for (int k = 0; k < RC; ++k) {
+      const int w = ct + VQ_CONV * 32 * k;
+      const int row = w / RCR, q = w % RCR;
+      src_off[k] = (uint32_t)(row * p.row_bytes + 16 * q);
+#pragma unroll
+      for (int e = 0; e < OC; ++e) dst_off[k][e] = (uint32_t)(row * 128 + (((OC * q + e) ^ (row & 7)) << 4));
+    }
     VQIter it(i0, i1, n_super);
     Ring rr, rs;
     int kblk = 0;
@@ -325,46 +380,30 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         mbar_wait(&rfull[rr.slot], rr.phase);
         mbar_wait(&empty[rs.slot], rs.phase ^ 1);
         if (ct == 0) mark(56 + min(kblk, 47));
-        const uint8_t* slot = raw + (size_t)rr.slot * RS;
-        uint8_t* ob = ring + (size_t)rs.slot * OB;
+        const uint32_t slot = smem_u32(raw + (size_t)rr.slot * RS);
+        const uint32_t ob = smem_u32(ring + (size_t)rs.slot * OB);
         for (int j = 0; j < NJ; ++j) {
+          // all of this tile's raw chunks first (the stores below are volatile
+          // asm: loads issued after them would serialise)
           uint4 vv[RC];
 #pragma unroll
-          for (int k = 0; k < RC; ++k) {
-            const int w = ct + VQ_CONV * 32 * k;
-            const int row = w / RCR, q = w % RCR;
-            vv[k] = lds128(smem_u32(slot + row * p.row_bytes + j * 16 * BITS + 16 * q));
-          }
-          uint8_t* st = ob + j * VQ_STAGE;
+          for (int k = 0; k < RC; ++k) vv[k] = lds128(slot + src_off[k] + j * 16 * BITS);
+          const uint32_t st = ob + j * VQ_STAGE;
 #pragma unroll
           for (int k = 0; k < RC; ++k) {
-            const int w = ct + VQ_CONV * 32 * k;
-            const int row = w / RCR, q = w % RCR;
             const uint4 v = vv[k];
-            const uint32_t rowa = smem_u32(st + row * 128);
-            const int sw = row & 7;
             if constexpr (BITS == 8) {
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + ((q ^ sw) << 4)),
+              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(st + dst_off[k][0]),
                            "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                            : "memory");
-            } else if constexpr (BITS == 4) {
-              constexpr uint32_t M = 0x0F0F0F0Fu;
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rowa + (((2 * q) ^ sw) << 4)),
-                           "r"(v.x & M), "r"(v.y & M), "r"(v.z & M), "r"(v.w & M)
-                           : "memory");
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                               rowa + (((2 * q + 1) ^ sw) << 4)),
-                           "r"((v.x >> 4) & M), "r"((v.y >> 4) & M), "r"((v.z >> 4) & M),
-                           "r"((v.w >> 4) & M)
-                           : "memory");
-            } else {  // BITS == 2
-              constexpr uint32_t M = 0x03030303u;
+            } else {
+              // nibbles / crumbs -> bytes: chunk e holds bits [BITS e, BITS e + BITS) of every byte
+              constexpr uint32_t M = BITS == 4 ? 0x0F0F0F0Fu : 0x03030303u;
 #pragma unroll
-              for (int e = 0; e < 4; ++e)
-                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(
-                                 rowa + (((4 * q + e) ^ sw) << 4)),
-                             "r"((v.x >> (2 * e)) & M), "r"((v.y >> (2 * e)) & M),
-                             "r"((v.z >> (2 * e)) & M), "r"((v.w >> (2 * e)) & M)
+              for (int e = 0; e < OC; ++e)
+                asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(st + dst_off[k][e]),
+                             "r"((v.x >> (BITS * e)) & M), "r"((v.y >> (BITS * e)) & M),
+                             "r"((v.z >> (BITS * e)) & M), "r"((v.w >> (BITS * e)) & M)
                              : "memory");
             }
           }
@@ -379,6 +418,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         rr.next(p.raw_slots);
         rs.next(p.stages);
       }
+    }
     }
   } else if (warp == VQ_MMA) {
     // ---------------- MMA issuer ----------------
@@ -395,12 +435,26 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
           if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
           fence_after();
           mark(152 + min(sb, 15));
-          const uint32_t pb = smem_u32(pbuf + buf * VQ_PBUF);
+          const uint32_t pb = smem_u32(pbuf + buf * PBUF);
           const int b1 = min(nblk, b0 + VQ_NB);
-          for (int blk = b0; blk < b1; ++blk, rs.next(p.stages)) {
+          for (int blk = b0; BITS == 16 && blk < b1; ++blk)
+            for (int j = 0; j < NJ; ++j, rs.next(p.stages)) {
+              mbar_wait(&full[rs.slot], rs.phase);
+              fence_after();
+              const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
+              const uint32_t a0 = smem_u32(ring + rs.slot * OB);
+              if ((p.diag & 1) == 0)
+#pragma unroll
+                for (int kk = 0; kk < TILE_M / 16; ++kk)  // K = 16 tokens: 2 KB of A (2 slabs)
+                  umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, VQ_BSTAGE / 2, 1024),
+                               sdesc(pb + (blk - b0) * PBLK + (kk >> 2) * 2048 + (kk & 3) * 32), IDESC_QB,
+                               (blk != b0) || (kk != 0));
+              umma_commit(&empty[rs.slot]);
+            }
+          for (int blk = b0; BITS != 16 && blk < b1; ++blk, rs.next(p.stages)) {
             mbar_wait(&full[rs.slot], rs.phase);
             fence_after();
-            const uint64_t db = sdesc(pb + (blk - b0) * 2048);
+            const uint64_t db = sdesc(pb + (blk - b0) * PBLK);
             for (int j = 0; j < NJ; ++j) {
               const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
               const uint64_t da = sdesc_mn(smem_u32(ring + rs.slot * OB + j * VQ_STAGE), VQ_STAGE, 1024);
@@ -449,9 +503,9 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
           if (h < p.s && t < nt) v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
           dst[h] = v;
         }
-        sd = make_float2(0.f, 0.f);
+        sd = make_float2(1.f, 1.f);
         zd = make_float2(0.f, 0.f);
-        if (t < nt) {
+        if (BITS != 16 && t < nt) {
           sd.x = __ldg(sc + t);
           zd.x = __ldg(zp + t);
           if (t + 1 < nt) {
@@ -501,38 +555,61 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         if (ta == 0) mark(216 + min(sb, 15));
         // (2) p = exp(x - m), u = p s / max s in [0, 1]; digits w = 254 hi + lo
         const float inv = m[V_HP] > 0.f ? 127.f / m[V_HP] : 0.f;
-        uint8_t* pb = pbuf + buf * VQ_PBUF;
+        uint8_t* pb = pbuf + buf * PBUF;
         const int tl = 2 * ta;
         const bool live = s0 + tl < ntok;
         const int blk = tl >> 7, tk = tl & 127;
-        uint8_t* rb = pb + blk * 2048 + (tk & 15);
-        const int z0 = (int)zv.x, z1 = (int)zv.y;  // zero points (integers)
+        uint8_t* rb = pb + blk * PBLK + (tk & 15);
         float l[V_HP];
-        long long zw[V_HP];
+        float zw[V_HP];
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
           l[h] = 0.f;
-          zw[h] = 0;
-          int w0 = 0, w1 = 0;
-          if (h < p.s && live) {
+          zw[h] = 0.f;
+          float w0 = 0.f, w1 = 0.f;
+          if constexpr (BITS == 16) {
+            // bf16 digit pair of p (rows h, h + 4; K-major SW128 atoms of 64
+            // tokens, 16-byte chunk ((tk % 64) / 8) ^ row)
+            uint8_t* ab = pb + blk * PBLK + (tk >> 6) * 2048 + (tk & 7) * 2;
+            const int w8 = (tk & 63) >> 3;
+            uint32_t hv = 0u, lv = 0u;
+            if (h < p.s && live) {
+              const float p0 = __expf(x[h].x - m[h]), p1 = __expf(x[h].y - m[h]);
+              l[h] = p0 + p1;
+              const __nv_bfloat162 hi = __floats2bfloat162_rn(p0, p1);
+              const float2 hf = __bfloat1622float2(hi);
+              const __nv_bfloat162 lo = __floats2bfloat162_rn(p0 - hf.x, p1 - hf.y);
+              hv = *reinterpret_cast<const uint32_t*>(&hi);
+              lv = *reinterpret_cast<const uint32_t*>(&lo);
+            }
+            if (live) {
+              *reinterpret_cast<uint32_t*>(ab + h * 128 + (((w8 ^ h) & 7) << 4)) = hv;
+              *reinterpret_cast<uint32_t*>(ab + (h + 4) * 128 + (((w8 ^ (h + 4)) & 7) << 4)) = lv;
+            }
+          } else if (h < p.s && live) {
+            // round-to-nearest integers via the 1.5 * 2^23 magic constant: the
+            // low byte of the float's bits is the two's-complement digit, so no
+            // F2I / rint is needed; |lo| <= 127 since |v - hi| <= 0.5
+            constexpr float MAGIC = 12582912.f;
             const float p0 = __expf(x[h].x - m[h]), p1 = __expf(x[h].y - m[h]);
             l[h] = p0 + p1;
             const float v0 = p0 * sv.x * inv, v1 = p1 * sv.y * inv;
-            const float h0 = rintf(v0), h1 = rintf(v1);
-            const int l0 = (int)fminf(fmaxf(rintf((v0 - h0) * 254.f), -127.f), 127.f);
-            const int l1 = (int)fminf(fmaxf(rintf((v1 - h1) * 254.f), -127.f), 127.f);
-            w0 = 254 * (int)h0 + l0;
-            w1 = 254 * (int)h1 + l1;
+            const float th0 = v0 + MAGIC, th1 = v1 + MAGIC;
+            const float h0 = th0 - MAGIC, h1 = th1 - MAGIC;
+            const float tl0 = fmaf(v0 - h0, 254.f, MAGIC), tl1 = fmaf(v1 - h1, 254.f, MAGIC);
+            w0 = fmaf(254.f, h0, tl0 - MAGIC);  // exact integers < 2^15
+            w1 = fmaf(254.f, h1, tl1 - MAGIC);
             // K-major SW128: row r, token tk -> 16-byte chunk (tk / 16) ^ (r & 7)
             *reinterpret_cast<uint16_t*>(rb + h * 128 + ((((tk >> 4) ^ h) & 7) << 4)) =
-                (uint16_t)((uint32_t)(int)h0 | ((uint32_t)(int)h1 << 8));
+                (uint16_t)__byte_perm(__float_as_uint(th0), __float_as_uint(th1), 0x0040);
             *reinterpret_cast<uint16_t*>(rb + (h + 4) * 128 + ((((tk >> 4) ^ (h + 4)) & 7) << 4)) =
-                (uint16_t)((uint32_t)(uint8_t)(int8_t)l0 | ((uint32_t)(uint8_t)(int8_t)l1 << 8));
+                (uint16_t)__byte_perm(__float_as_uint(tl0), __float_as_uint(tl1), 0x0040);
           } else if (live) {
             *reinterpret_cast<uint16_t*>(rb + h * 128 + ((((tk >> 4) ^ h) & 7) << 4)) = 0;
             *reinterpret_cast<uint16_t*>(rb + (h + 4) * 128 + ((((tk >> 4) ^ (h + 4)) & 7) << 4)) = 0;
           }
-          zw[h] = -((long long)w0 * z0 + (long long)w1 * z1);  // - sum w z (exact)
+          // - sum w z in fp32: relative to the digit sums it carries ~1e-7
+          if (BITS != 16) zw[h] = -fmaf(w0, zv.x, w1 * zv.y);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         if (ta == 0) mark(332 + min(sb, 15));
@@ -540,8 +617,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
           l[h] = warp_reduce(l[h], [](float a, float c) { return a + c; });
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) zw[h] += __shfl_xor_sync(0xffffffffu, zw[h], o);
+          zw[h] = warp_reduce(zw[h], [](float a, float c) { return a + c; });
         }
         if (lane == 0) {
 #pragma unroll

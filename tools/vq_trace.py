@@ -52,6 +52,9 @@ def main():
     starts = (tr[:, 0] - t0) / 1e3
     print(f"CTAs {n}: start spread {starts.min():.1f}..{starts.max():.1f} us, "
           f"end spread {ends.min():.1f}..{ends.max():.1f} us")
+    busy = ends[tr[:, 3] > 2000000]
+    print("  CTA end us p10/p50/p90/max", np.percentile(busy, [10, 50, 90, 100]).round(1),
+          " even-SM CTAs median", np.median(ends[0::2]).round(1), "odd", np.median(ends[1::2]).round(1))
 
     GHZ = 1.9  # slots >= 3 hold SM clock64 values; slot 2 = clock64 at entry
 
