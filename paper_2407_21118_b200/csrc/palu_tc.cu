@@ -2166,7 +2166,9 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
 // converter-to-bf16 kernel (A/B timing).
 static bool value_q_enabled(int bits) {
   const char* e = getenv("PALU_VALUE_KERNEL");
-  if (bits == 16) return !(e && strcmp(e, "tc_bf16_role") == 0);  // earlier bf16 value role
+  // raw bf16 values: the value role (value_tc_kernel) measured faster than
+  // value_q_kernel<16> (74 vs 86 us at r 256); PALU_VALUE_KERNEL=tc_bf16_q for A/B
+  if (bits == 16) return e && strcmp(e, "tc_bf16_q") == 0;
   return !(e && strcmp(e, "tc_quant_bf16") == 0);
 }
 
