@@ -50,8 +50,11 @@ def parse():
                     help="multi-GPU: head-group shards with one NCCL all-reduce of the layer "
                          "output per layer (strong scaling; the default for N > 1, SURVEY 8(e)) "
                          "or batch replicas (weak scaling)")
-    ap.add_argument("--rope-base", type=float, default=10000.0,
-                    help="1e6 for the Mistral-7B-shaped config (32 q-heads / 8 KV groups, SURVEY 8(d) C4)")
+    ap.add_argument("--rope-base", type=float, default=None,
+                    help="RoPE base (default 1e4; 1e6 with --kv-heads, Mistral-7B v0.2)")
+    ap.add_argument("--kv-heads", type=int, default=0,
+                    help="GQA (BASELINE configs[3], Mistral-7B: 8): one G-LRD group per KV head, "
+                         "replicated B (MHA-equivalent); ranks default to 64 = 50%% of a KV head")
     ap.add_argument("--rope", default="on", choices=["on", "off"],
                     help="off: palu_decode_step_norope path (attention.py:365-389)")
     ap.add_argument("--score-kernel", default="auto")
@@ -59,6 +62,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-baseline", action="store_true", help="skip the uncompressed comparators")
     a = ap.parse_args()
+    if a.rope_base is None:
+        a.rope_base = 1e6 if a.kv_heads else 10000.0
+    if a.kv_heads and a.rank_k == RANK and a.rank_v == RANK:
+        a.rank_k = a.rank_v = DH // 2
     b = [int(x) for x in str(a.bits).split(",")]
     a.bits = b[0] if len(b) == 1 else (b[0], b[1])
     return a
@@ -185,7 +192,9 @@ def cpu_baseline(args):
 
 def workload_config(args, world: int, heads: bool) -> dict:
     """The `config` of the bench line (shared by both arms)."""
-    return {"workload": (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
+    model = (f"mistral-7b-gqa{args.kv_heads}-32L-palu50-kvgroup" if args.kv_heads
+             else "llama2-7b-32L-palu50-gs4")
+    return {"workload": (f"{model}-rk{args.rank_k}-rv{args.rank_v}-"
                          + ("rope" if args.rope == "on" else "norope")),
             "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
             "batch_per_gpu": args.batch,
@@ -257,12 +266,14 @@ def uncompressed_baseline(args, palu_ms):
     out = {}
     T, B, Lyr = args.context, args.batch, args.layers
     d, n, dh = D, NH, DH
+    nkv = args.kv_heads or n  # GQA: the uncompressed cache holds the KV heads only
     cfg = AttentionConfig(D, NH, DH, layers=Lyr, rope=True, rope_base=args.rope_base)
     cap = T + 64
     g = torch.Generator(device="cuda")
     g.manual_seed(7)
     sc = 1.0 / math.sqrt(D)
-    wqkv = [((torch.rand(3 * D, D, device="cuda", generator=g) * 2 - 1) * sc).bfloat16() for _ in range(Lyr)]
+    wqkv = [((torch.rand(D + 2 * nkv * DH, D, device="cuda", generator=g) * 2 - 1) * sc).bfloat16()
+            for _ in range(Lyr)]
     wo = [((torch.rand(D, D, device="cuda", generator=g) * 2 - 1) * sc).bfloat16() for _ in range(Lyr)]
     K = max(5, args.steps // 2)
 
@@ -291,14 +302,14 @@ def uncompressed_baseline(args, palu_ms):
         del gr
         return e0.elapsed_time(e1) / K
 
-    kv_bytes = 2 * (T + 1) * D * 2 * B
+    kv_bytes = 2 * (T + 1) * nkv * dh * 2 * B
     # ---- flashinfer trtllm-gen step (graph) ----------------------------
     try:
         import flashinfer
 
         page = 64
         pps = (cap + page - 1) // page
-        kv = [torch.empty(pps * B, 2, n, page, dh, device="cuda", dtype=torch.bfloat16)
+        kv = [torch.empty(pps * B, 2, nkv, page, dh, device="cuda", dtype=torch.bfloat16)
               for _ in range(Lyr)]
         for t_ in kv:
             t_.normal_(0.0, 0.3)
@@ -308,7 +319,8 @@ def uncompressed_baseline(args, palu_ms):
         theta = torch.from_numpy(__import__("numpy").array(
             [args.rope_base ** (-2.0 * i / dh) for i in range(dh // 2)])).cuda()
         x = torch.randn(B, d, device="cuda") * 0.5
-        qkv = torch.zeros(B, 3 * d, device="cuda")
+        nqkv = d + 2 * nkv * dh
+        qkv = torch.zeros(B, nqkv, device="cuda")
         qb = torch.zeros(B, n, dh, device="cuda", dtype=torch.bfloat16)
         ob = torch.zeros(B, n, dh, device="cuda", dtype=torch.bfloat16)
         attn = torch.zeros(B, d, device="cuda")
@@ -319,8 +331,8 @@ def uncompressed_baseline(args, palu_ms):
             st_ = _stream()
             torch.add(t_dev, 1, out=seq)  # every sequence holds t + 1 rows after the append
             for li in range(Lyr):
-                _lib.call("palu_gemv", code, _ptr(wqkv[li]), 3 * d, d, _ptr(x), B, d, _ptr(qkv), 3 * d, 0, st_)
-                _lib.call("palu_dense_append_paged", _ptr(qkv), B, n, dh, _ptr(kv[li]), page, pps,
+                _lib.call("palu_gemv", code, _ptr(wqkv[li]), nqkv, d, _ptr(x), B, d, _ptr(qkv), nqkv, 0, st_)
+                _lib.call("palu_dense_append_paged", _ptr(qkv), B, n, nkv, dh, _ptr(kv[li]), page, pps,
                           _ptr(theta), _ptr(t_dev), _ptr(qb), st_)
                 flashinfer.decode.trtllm_batch_decode_with_kv_cache(
                     qb, kv[li], ws, bt, seq, cap, bmm1_scale=1.0 / math.sqrt(dh), bmm2_scale=1.0,
@@ -352,8 +364,10 @@ def uncompressed_baseline(args, palu_ms):
     except Exception as exc:  # comparator only; never the product path
         out["flashinfer_error"] = f"{type(exc).__name__}: {str(exc)[:200]}"
     torch.cuda.empty_cache()
-    # ---- own simple K0 (reference only) -----------------------------------
+    # ---- own simple K0 (reference only; MHA) --------------------------------
     try:
+        if nkv != n:
+            raise RuntimeError("own K0 implements MHA only")
         m = DenseModel(cfg, [w.float() for w in wqkv], [w.float() for w in wo], dtype="bfloat16",
                        batch=B, capacity=cap)
         m.kc.normal_(0.0, 0.3)
@@ -363,8 +377,8 @@ def uncompressed_baseline(args, palu_ms):
         m.x.normal_(0.0, 0.5)
         out["own_k0_us_per_step"] = time_graph(m.launch_step) * 1e3
         del m
-    except torch.OutOfMemoryError as exc:
-        out["own_k0_error"] = f"OutOfMemoryError: {str(exc)[:120]}"
+    except (torch.OutOfMemoryError, RuntimeError) as exc:
+        out["own_k0_error"] = f"{type(exc).__name__}: {str(exc)[:120]}"
     del wqkv, wo
     torch.cuda.empty_cache()
     return out
@@ -437,7 +451,8 @@ def main():
                                              context=args.context, extra=extra, bits=args.bits,
                                              dtype=args.dtype, seed=1234 + (0 if heads else rank),
                                              rank_k=args.rank_k, rank_v=args.rank_v,
-                                             rope=args.rope == "on", rope_base=args.rope_base)
+                                             rope=args.rope == "on", rope_base=args.rope_base,
+                                             kv_heads=args.kv_heads)
     if heads:
         # this rank keeps its head groups; one all-reduce per layer
         from paper_2407_21118_b200.sharding import attach_allreduce, shard_engine
@@ -539,8 +554,7 @@ def main():
                          "frac_of_sustained": achieved_tf / tf_sus}
     # measured DRAM traffic of the dominant kernel, from a committed ncu capture
     # of the same workload (profiles/*_traffic.json), else null
-    workload = (f"llama2-7b-32L-palu50-gs4-rk{args.rank_k}-rv{args.rank_v}-"
-                + ("rope" if args.rope == "on" else "norope"))
+    workload = workload_config(args, 1, False)["workload"]
     for tf_name in ("r02_traffic.json", "r01_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf_name)) as fh:

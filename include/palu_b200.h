@@ -266,12 +266,13 @@ size_t palu_dense_workspace(int B, int n_heads, int head_dim, int n_chunks);
 /*
  * Comparator support for the uncompressed step with flashinfer's trtllm-gen
  * decode kernel (bench.py): RoPE + append of row t into an HND paged bf16
- * K/V cache [page][2][n][page_size][d_h] (page = b * pages_per_seq + t /
- * page_size; same semantics as palu_dense_decode's append), rotated q as
- * bf16 [B][n][d_h]; and a bf16 -> fp32 cast of the attention output.
+ * K/V cache [page][2][n_kv][page_size][d_h] (page = b * pages_per_seq + t /
+ * page_size; same semantics as palu_dense_decode's append; qkv fp32
+ * [B][n d_h + 2 n_kv d_h], n_kv < n for GQA), rotated q as bf16
+ * [B][n][d_h]; and a bf16 -> fp32 cast of the attention output.
  */
-int palu_dense_append_paged(const float* qkv, int B, int n_heads, int head_dim, void* kv_pages,
-                            int page_size, int pages_per_seq, const double* theta,
+int palu_dense_append_paged(const float* qkv, int B, int n_heads, int n_kv, int head_dim,
+                            void* kv_pages, int page_size, int pages_per_seq, const double* theta,
                             const int* t_dev, void* q_out, void* stream);
 int palu_cast_bf16_f32(const void* src, float* dst, int n, void* stream);
 

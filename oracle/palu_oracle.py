@@ -489,3 +489,54 @@ def synth_layer(d: int, n_heads: int, head_dim: int, s_k: int, ranks_k, s_v: int
     wk = random_matrix(d, d, seed + 1) * sq if with_kv else None
     wv = random_matrix(d, d, seed + 2) * sq if with_kv else None
     return OracleLayer(wq=wq, wo=wo, ak=ak, bk=bk, av=av, bv=bv, s_k=s_k, s_v=s_v, wk=wk, wv=wv)
+
+
+# --------------------------------------------------------------------------
+# GQA (BASELINE configs[3], Mistral-7B: 32 query heads, 8 KV heads).  The
+# reference has no GQA (AttentionConfig forces d = n d_h, attention.py:44-47);
+# the MHA-equivalent layer replicates each KV head's factors across the
+# query heads that share it, so the unchanged reference
+# computes exact GQA semantics.  gqa_decode_step_rope is an independent
+# KV-head restatement used to check that equivalence.
+# --------------------------------------------------------------------------
+def synth_gqa_layer(d: int, n_q: int, n_kv: int, head_dim: int, rank_k: int, rank_v: int,
+                    seed: int, hadamard_fused: bool = False) -> OracleLayer:
+    """Replicated-B layer: group j = the n_q / n_kv query heads of KV head j,
+    A_j = U(d x r)/sqrt(d), B_j = [B_kv B_kv ...] with B_kv = U(r x d_h)/sqrt(r)."""
+    s = n_q // n_kv
+    sq = 1.0 / math.sqrt(d)
+    wq = random_matrix(d, d, seed) * sq
+    wo = random_matrix(d, d, seed + 3) * sq
+    ak, bk, av, bv = [], [], [], []
+    for g in range(n_kv):
+        for r, dst_a, dst_b, off in ((rank_k, ak, bk, 1000), (rank_v, av, bv, 2000)):
+            a = random_matrix(d, r, seed + off + 2 * g) * sq
+            b = np.tile(random_matrix(r, head_dim, seed + off + 1 + 2 * g) / math.sqrt(r), (1, s))
+            if hadamard_fused:
+                a, b = fuse_hadamard(a, b)
+            dst_a.append(a)
+            dst_b.append(b)
+    return OracleLayer(wq=wq, wo=wo, ak=ak, bk=bk, av=av, bv=bv, s_k=s, s_v=s)
+
+
+def gqa_decode_step_rope(layer: OracleLayer, hk: np.ndarray, hv: np.ndarray, x_t, n_q: int,
+                         n_kv: int, head_dim: int, rope_base: float, t: int) -> np.ndarray:
+    """One GQA decode step over KV heads (not via the MHA-equivalent path):
+    keys of KV head j = rope(H_k,j B_kv,j), query head i attends to KV head
+    i // (n_q / n_kv); H_k / H_v hold rows 0..t (the newest token's included)."""
+    s, dh = n_q // n_kv, head_dim
+    x = np.asarray(x_t, dtype=np.float64)
+    off_k = np.concatenate([[0], np.cumsum([a.shape[1] for a in layer.ak])])
+    off_v = np.concatenate([[0], np.cumsum([a.shape[1] for a in layer.av])])
+    pos = np.arange(t + 1, dtype=np.float64)
+    out = np.zeros(n_q * dh)
+    for j in range(n_kv):
+        keys = rope_rows(hk[:, off_k[j]:off_k[j + 1]] @ layer.bk[j][:, :dh], pos, rope_base)
+        vals = hv[:, off_v[j]:off_v[j + 1]] @ layer.bv[j][:, :dh]
+        for i in range(j * s, (j + 1) * s):
+            q = rope_rows((x @ layer.wq[:, i * dh:(i + 1) * dh])[None, :], np.array([float(t)]),
+                          rope_base)[0]
+            p = softmax(keys @ q / math.sqrt(dh))
+            out += (p @ vals) @ layer.wo[i * dh:(i + 1) * dh, :]
+    return out
+

@@ -61,7 +61,7 @@ SIGNATURES = {
     "palu_advance": (i32, [p, p]),
     "palu_dense_decode": (i32, [i32, p, i32, i32, i32, p, p, i32, p, p, i32, p, p, p]),
     "palu_dense_workspace": (sz, [i32, i32, i32, i32]),
-    "palu_dense_append_paged": (i32, [p, i32, i32, i32, p, i32, i32, p, p, p, p]),
+    "palu_dense_append_paged": (i32, [p, i32, i32, i32, i32, p, i32, i32, p, p, p, p]),
     "palu_cast_bf16_f32": (i32, [p, p, i32, p]),
 }
 

@@ -1039,31 +1039,39 @@ __global__ void advance_kernel(int* t_dev) { pdl_enter(); *t_dev += 1; }
 // step graph): RoPE + append row t into an HND paged bf16 cache
 // [page][2][n][P][d_h] (page = b * pages_per_seq + t / P), rotated q as bf16
 // [B][n][d_h] for the attention kernel.
-__global__ void dense_append_paged_kernel(const float* __restrict__ qkv, int n_heads, int dh,
+// qkv: fp32 [B][n dh + 2 n_kv dh] (q | k | v; GQA: n_kv < n KV heads); block
+// (i, b) rotates query head i and, for i < n_kv, appends KV head i.
+__global__ void dense_append_paged_kernel(const float* __restrict__ qkv, int n_heads, int n_kv, int dh,
                                           bf16* __restrict__ kv, int P, int pages_per_seq,
                                           const double* __restrict__ theta,
                                           const int* __restrict__ t_dev, bf16* __restrict__ qout) {
   pdl_enter();
   const int i = blockIdx.x, b = blockIdx.y;
-  const int d = n_heads * dh, half = dh / 2;
+  const int d = n_heads * dh, dkv = n_kv * dh, half = dh / 2;
   const int t = *t_dev;
-  const float* q = qkv + (size_t)b * 3 * d + (size_t)i * dh;
-  const float* k = q + d;
-  const float* v = q + 2 * d;
+  const float* row = qkv + (size_t)b * (d + 2 * dkv);
+  const float* q = row + (size_t)i * dh;
+  const float* k = row + d + (size_t)i * dh;
+  const float* v = row + d + dkv + (size_t)i * dh;
+  const bool kv_head = i < n_kv;
   const size_t page = (size_t)b * pages_per_seq + t / P;
-  bf16* krow = kv + (((page * 2 + 0) * n_heads + i) * P + t % P) * dh;
-  bf16* vrow = kv + (((page * 2 + 1) * n_heads + i) * P + t % P) * dh;
+  bf16* krow = kv + (((page * 2 + 0) * n_kv + i) * P + t % P) * dh;
+  bf16* vrow = kv + (((page * 2 + 1) * n_kv + i) * P + t % P) * dh;
   bf16* qo = qout + ((size_t)b * n_heads + i) * dh;
   for (int j = threadIdx.x; j < half; j += blockDim.x) {
     double sn, cs;
     sincos_big((double)t * theta[j], &sn, &cs);
-    const double klo = k[j], khi = k[j + half], qlo = q[j], qhi = q[j + half];
-    krow[j] = __float2bfloat16_rn((float)(klo * cs - khi * sn));
-    krow[j + half] = __float2bfloat16_rn((float)(klo * sn + khi * cs));
+    const double qlo = q[j], qhi = q[j + half];
     qo[j] = __float2bfloat16_rn((float)(qlo * cs - qhi * sn));
     qo[j + half] = __float2bfloat16_rn((float)(qlo * sn + qhi * cs));
+    if (kv_head) {
+      const double klo = k[j], khi = k[j + half];
+      krow[j] = __float2bfloat16_rn((float)(klo * cs - khi * sn));
+      krow[j + half] = __float2bfloat16_rn((float)(klo * sn + khi * cs));
+    }
   }
-  for (int j = threadIdx.x; j < dh; j += blockDim.x) vrow[j] = __float2bfloat16_rn(v[j]);
+  if (kv_head)
+    for (int j = threadIdx.x; j < dh; j += blockDim.x) vrow[j] = __float2bfloat16_rn(v[j]);
 }
 
 __global__ void cast_bf16_f32_kernel(const bf16* __restrict__ src, float* __restrict__ dst, int n) {
@@ -1554,12 +1562,13 @@ int palu_advance(int* t_dev, void* stream) {
   return PALU_OK;
 }
 
-int palu_dense_append_paged(const float* qkv, int B, int n_heads, int head_dim, void* kv_pages,
+int palu_dense_append_paged(const float* qkv, int B, int n_heads, int n_kv, int head_dim, void* kv_pages,
                             int page_size, int pages_per_seq, const double* theta, const int* t_dev,
                             void* q_out, void* stream) {
-  PALU_REQUIRE(head_dim % 2 == 0, "palu_dense_append_paged: head_dim %d", head_dim);
+  PALU_REQUIRE(head_dim % 2 == 0 && n_kv >= 1 && n_kv <= n_heads && n_heads % n_kv == 0,
+               "palu_dense_append_paged: head_dim %d, %d query / %d KV heads", head_dim, n_heads, n_kv);
   PALU_CK(launch_k(dense_append_paged_kernel, dim3(n_heads, B), dim3(64), 0, S(stream), qkv, n_heads,
-                   head_dim, (bf16*)kv_pages, page_size, pages_per_seq, theta, t_dev, (bf16*)q_out));
+                   n_kv, head_dim, (bf16*)kv_pages, page_size, pages_per_seq, theta, t_dev, (bf16*)q_out));
   PALU_LAUNCHED();
   return PALU_OK;
 }

@@ -172,12 +172,17 @@ def _shape_only(rows: int, cols: int):
 
 def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=256, layers=32,
                      batch=1, context=65536, extra=64, bits=16, dtype="bfloat16", seed=0,
-                     rope_base=10000.0, rope=True):
+                     rope_base=10000.0, rope=True, kv_heads=0):
     """Return (weights, fused, cache) for a Llama-2-7B-shaped Palu model.
 
     Random-init weights of that architecture (uniform, scaled as SURVEY
-    8(d)); the cache holds ``context`` tokens per sequence.
+    8(d)); the cache holds ``context`` tokens per sequence.  kv_heads > 0:
+    GQA (Mistral-7B: 8 KV heads) as the MHA-equivalent layer -- one group per
+    KV head (s = n_heads / kv_heads), its B_k / B_v columns replicated across
+    the group's query heads.
     """
+    if kv_heads:
+        s = n_heads // kv_heads
     import torch as _t
     from .attention import FusedWeights, LayerFused, _dt, _head_offsets, _rank_pad, _round_up, theta_table
 
@@ -206,7 +211,10 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
         n1 = qdim + G * (rank_k + rank_v)
         w1 = U(n1, d, scale=1.0 / math.sqrt(d)).to(tdt)
         bk = torch.zeros(G, rk_pad, s * head_dim, device=dev, dtype=tdt)
-        bk[:, :rank_k] = U(G, rank_k, s * head_dim, scale=1.0 / math.sqrt(rank_k)).to(tdt)
+        if kv_heads:  # one KV head's B columns replicated over its query heads
+            bk[:, :rank_k] = U(G, rank_k, head_dim, scale=1.0 / math.sqrt(rank_k)).repeat(1, 1, s).to(tdt)
+        else:
+            bk[:, :rank_k] = U(G, rank_k, s * head_dim, scale=1.0 / math.sqrt(rank_k)).to(tdt)
         # wo_fused rows: (B_v block @ W_o block); entries ~ scale of a product
         woT = torch.zeros(d, ko_pad, device=dev, dtype=tdt)
         woT[:, :ko] = U(d, ko, scale=1.0 / math.sqrt(3.0 * d)).to(tdt)

@@ -309,7 +309,58 @@ def gen_c1():
     _save("c1_step.npz", **out)
 
 
+GQA_CASES = [
+    # name, d, n_q, n_kv, dh, rank_k, rank_v, T, bits, hadamard, base
+    ("gqa_q8_kv2_r64", 1024, 8, 2, 128, 64, 64, 300, 16, False, 1e6),
+    ("gqa_q8_kv2_r64_k16v4_had", 1024, 8, 2, 128, 64, 64, 260, (16, 4), True, 1e6),
+    ("gqa_q8_kv2_r32_b4_had", 1024, 8, 2, 128, 32, 64, 200, 4, True, 1e6),
+]
+
+
+def gen_gqa():
+    """BASELINE configs[3] semantics (Mistral-7B GQA), scaled down: the
+    MHA-equivalent replicated-B layer decoded by the
+    UNMODIFIED reference, checked against an independent KV-head restatement
+    (oracle.gqa_decode_step_rope) before it is stored."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from oracle import palu_oracle as po
+    out, names = {}, []
+    for ci, (name, d, nq, nkv, dh, rk, rv, T, bits, had, base) in enumerate(GQA_CASES):
+        seed = 8100 + 100 * ci
+        L = po.synth_gqa_layer(d, nq, nkv, dh, rk, rv, seed, hadamard_fused=had)
+        s = nq // nkv
+        config = AttentionConfig(d, nq, dh, layers=1, rope=True, rope_base=base)
+        z = Matrix(np.zeros((d, d)))
+        lw = LayerWeights(wq=Matrix(L.wq), wk=z, wv=z, wo=Matrix(L.wo))
+        gran = Granularity.group_head(s)
+        key = DecomposedLayer(gran, tuple(GroupFactors(Matrix(a), Matrix(b), a.shape[1])
+                                          for a, b in zip(L.ak, L.bk)), d, dh, nq)
+        value = DecomposedLayer(gran, tuple(GroupFactors(Matrix(a), Matrix(b), a.shape[1])
+                                            for a, b in zip(L.av, L.bv)), d, dh, nq)
+        kv = LayerKV(key=key, value=value)
+        weights = ModelWeights(layers=(lw,))
+        fused = build_fused(weights, [kv], config)
+        cache = LatentKVCache([kv], config, bits=bits)
+        x_rows = random_matrix(T, d, seed=seed + 77).data
+        _direct_fill(cache, kv, 0, x_rows)
+        cache.t = T
+        x_t = random_matrix(1, d, seed=seed + 78).data[0]
+        y = palu_decode_step_rope(weights, fused, cache, x_t)
+        indep = po.gqa_decode_step_rope(L, cache.hk(0), cache.hv(0), x_t, nq, nkv, dh, base, T)
+        err = float(np.linalg.norm(indep - y) / np.linalg.norm(y))
+        assert err < 1e-12, (name, err)
+        p = f"c{ci}_"
+        names.append(name)
+        out[p + "meta"] = np.array([d, nq, nkv, dh, rk, rv, T, had, base, seed], dtype=np.float64)
+        out[p + "bits"] = np.array(bits if isinstance(bits, tuple) else (bits, bits))
+        out[p + "out1"] = y
+        out[p + "indep_rel_err"] = np.array([err])
+        print(f"gqa {name}: reference vs independent GQA restatement rel-L2 {err:.2e}")
+    out["names"] = np.array(names)
+    _save("gqa_step.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "quant", "small", "medium", "c1"]
+    which = sys.argv[1:] or ["rng", "quant", "small", "medium", "c1", "gqa"]
     for w in which:
         globals()[f"gen_{w}"]()

@@ -72,3 +72,17 @@ def oracle_step_from_fill(case, steps=1):
         x = po.decode_step_rope([L], wo_f, cache, x, case["n"], case["dh"], case["base"])
         outs.append(x)
     return outs, cache
+
+
+def gqa_case(g, ci):
+    """GQA_CASES[ci] (make_golden.py): the replicated-B layer from its seed."""
+    p = f"c{ci}_"
+    d, nq, nkv, dh, rk, rv, T, had, base, seed = g[p + "meta"]
+    d, nq, nkv, dh, rk, rv, T, seed = (int(v) for v in (d, nq, nkv, dh, rk, rv, T, seed))
+    L = po.synth_gqa_layer(d, nq, nkv, dh, rk, rv, seed, hadamard_fused=bool(had))
+    x_rows = po.random_matrix(T, d, seed + 77)
+    x_t = po.random_matrix(1, d, seed + 78)[0]
+    bits = tuple(int(b) for b in g[p + "bits"])
+    return dict(layer=L, x_rows=x_rows, x_t=x_t, bits=bits, base=float(base), n=nq, n_kv=nkv,
+                dh=dh, d=d, T=T, out1=g[p + "out1"])
+

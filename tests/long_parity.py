@@ -32,9 +32,14 @@ def log_result(rec: dict) -> None:
             f.write(json.dumps(rec) + "\n")
 
 
-def make_layers(n_layers, d=4096, n=32, dh=128, s=4, rk=256, rv=256, hadamard=False, seed=500):
-    """OracleLayer list with po.synth_layer's seeds/scales, via the GPU generator."""
+def make_layers(n_layers, d=4096, n=32, dh=128, s=4, rk=256, rv=256, hadamard=False, seed=500,
+                gqa_kv=0):
+    """OracleLayer list with po.synth_layer's seeds/scales, via the GPU generator.
+    gqa_kv > 0: po.synth_gqa_layer's replicated-B layers (n_kv = gqa_kv)."""
     from paper_2407_21118_b200.harness import random_matrix_gpu
+    if gqa_kv:
+        return [po.synth_gqa_layer(d, n, gqa_kv, dh, rk, rv, seed + 101 * li, hadamard_fused=hadamard)
+                for li in range(n_layers)]
 
     def rm(r, c, sd):
         return random_matrix_gpu(r, c, sd).cpu().numpy()
@@ -117,11 +122,11 @@ def fill_both(cache, oc, layers, T, seed=900, chunk=8192):
 
 
 def run_case(P, *, T, n_layers=2, rk=256, rv=256, bits=16, hadamard=False, rope=True,
-             base=10000.0, seed=500, steps=1, name=""):
+             base=10000.0, seed=500, steps=1, name="", gqa_kv=0):
     """One (or more) GPU decode steps vs the oracle; returns a record dict."""
     from paper_2407_21118_b200.harness import set_cache_t
     n, dh, s = 32, 128, 4
-    layers = make_layers(n_layers, rk=rk, rv=rv, hadamard=hadamard, seed=seed)
+    layers = make_layers(n_layers, rk=rk, rv=rv, hadamard=hadamard, seed=seed, gqa_kv=gqa_kv)
     w, dec, cfg = to_package(layers, n, dh, rope, base)
     fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
     cache = P.LatentKVCache(dec, cfg, bits, dtype="bfloat16", capacity=T + 8 * steps)
@@ -147,7 +152,7 @@ def run_case(P, *, T, n_layers=2, rk=256, rv=256, bits=16, hadamard=False, rope=
         errs.append(float(np.linalg.norm(yg - yo) / np.linalg.norm(yo)))
         xg, xo = yg, yo
     sess = cache._session
-    rec = dict(case=name, T=T, layers=n_layers, rank_k=rk, rank_v=rv,
+    rec = dict(case=name, T=T, layers=n_layers, rank_k=rk, rank_v=rv, kv_heads=gqa_kv or None,
                bits=list(bits) if isinstance(bits, tuple) else bits, hadamard=hadamard, rope=rope,
                rope_base=base, rel_l2=errs, code_mismatches=mism,
                score_kernel=("tcgen05" if any(sess.tc_layers) else

@@ -34,6 +34,13 @@ CASES = [
     ("norope_r256_int4had_64k", 65536, 1, 256, 256, 4, True, False, 10000.0),
 ]
 
+# BASELINE configs[3]: Mistral-7B GQA (32 query heads, 8 KV heads, d_h 128),
+# 50 % rank of a KV head (64), RoPE base 1e6, 32K context, replicated-B layers
+GQA_CASES = [
+    ("mistral_gqa8_r64_bf16_32k", 32768, 2, 64, 64, 16, False),
+    ("mistral_gqa8_r64_k16v4had_32k", 32768, 1, 64, 64, (16, 4), True),
+]
+
 
 @pytest.fixture(scope="module")
 def P():
@@ -54,3 +61,17 @@ def test_long_context_step_matches_oracle(P, case):
     torch.cuda.empty_cache()
     assert rec["code_mismatches"] == 0, rec
     assert max(rec["rel_l2"]) < TOL, rec
+
+
+@pytest.mark.parametrize("case", GQA_CASES, ids=[c[0] for c in GQA_CASES])
+def test_gqa_long_context_step_matches_oracle(P, case):
+    import torch
+    name, T, nl, rk, rv, bits, had = case
+    rec = run_case(P, T=T, n_layers=nl, rk=rk, rv=rv, bits=bits, hadamard=had, rope=True, base=1e6,
+                   name=name, gqa_kv=8)
+    rec["tol"] = TOL
+    log_result(rec)
+    torch.cuda.empty_cache()
+    assert rec["code_mismatches"] == 0, rec
+    assert max(rec["rel_l2"]) < TOL, rec
+

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from conftest import rel_err
-from golden_cases import c1_case, medium_case, oracle_step_from_fill, small_case
+from golden_cases import c1_case, gqa_case, medium_case, oracle_step_from_fill, small_case
 from oracle import palu_oracle as po
 
 pytestmark = pytest.mark.gpu
@@ -468,3 +468,25 @@ def test_append_kv_equals_two_appends(P, bits_k, bits_v):
             assert torch.equal(a[key].view(torch.uint8) if a[key].dtype == torch.bfloat16 else a[key],
                                b[key].view(torch.uint8) if b[key].dtype == torch.bfloat16 else b[key]), key
         assert a["rows"].abs().sum() > 0 if a["rows"].dtype != torch.uint8 else a["rows"].any()
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_gqa_replicated_b_matches_reference(P, golden, dtype):
+    """BASELINE configs[3] (Mistral-7B GQA) semantics: the replicated-B layers
+    of tests/golden/gqa_step.npz (decoded by the unmodified reference, checked
+    there against an independent KV-head restatement) through the GPU step."""
+    from paper_2407_21118_b200.harness import fill_cache_direct, set_cache_t
+    g = golden("gqa_step.npz")
+    for ci, name in enumerate(g["names"]):
+        case = gqa_case(g, ci)
+        w, dec, cfg = _to_types(P, [case["layer"]], case["n"], case["dh"], True, case["base"])
+        fused = P.build_fused(w, dec, cfg, dtype=dtype)
+        bits = case["bits"] if case["bits"][0] != case["bits"][1] else case["bits"][0]
+        cache = P.LatentKVCache(dec, cfg, bits, dtype=dtype, capacity=case["T"] + 8)
+        fill_cache_direct(cache, 0, case["x_rows"])
+        set_cache_t(cache, case["T"])
+        y = P.palu_decode_step_rope(w, fused, cache, case["x_t"])
+        tol = TOL[dtype] if min(case["bits"]) == 16 else max(TOL[dtype], 1e-2)
+        e = rel_err(y, case["out1"])
+        assert e < tol, (name, dtype, e)
+
