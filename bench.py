@@ -52,6 +52,9 @@ def parse():
                          "or batch replicas (weak scaling)")
     ap.add_argument("--rope-base", type=float, default=None,
                     help="RoPE base (default 1e4; 1e6 with --kv-heads, Mistral-7B v0.2)")
+    ap.add_argument("--rank-plan", default="", choices=["", "kv25-75"],
+                    help="SURVEY 8(f)4: per-layer, per-group (r_k, r_v) from rank_plan.allocate "
+                         "(ranks.py:131-219) on synthetic Fisher scores, K budget 25%%, V 75%%")
     ap.add_argument("--kv-heads", type=int, default=0,
                     help="GQA (BASELINE configs[3], Mistral-7B: 8): one G-LRD group per KV head, "
                          "replicated B (MHA-equivalent); ranks default to 64 = 50%% of a KV head")
@@ -66,6 +69,14 @@ def parse():
         a.rope_base = 1e6 if a.kv_heads else 10000.0
     if a.kv_heads and a.rank_k == RANK and a.rank_v == RANK:
         a.rank_k = a.rank_v = DH // 2
+    a.plan = None
+    if a.rank_plan:
+        from paper_2407_21118_b200 import rank_plan as RP
+        rk, rv, _, _ = RP.kv_plan(a.layers, NH // GS, GS * DH, D, 0.25, 0.75, min_rank=8)
+        a.plan = (rk, rv)
+        # accounting (bytes, FLOPs) uses the mean group rank
+        a.rank_k = round(sum(map(sum, rk)) / (a.layers * (NH // GS)))
+        a.rank_v = round(sum(map(sum, rv)) / (a.layers * (NH // GS)))
     b = [int(x) for x in str(a.bits).split(",")]
     a.bits = b[0] if len(b) == 1 else (b[0], b[1])
     return a
@@ -193,7 +204,7 @@ def cpu_baseline(args):
 def workload_config(args, world: int, heads: bool) -> dict:
     """The `config` of the bench line (shared by both arms)."""
     model = (f"mistral-7b-gqa{args.kv_heads}-32L-palu50-kvgroup" if args.kv_heads
-             else "llama2-7b-32L-palu50-gs4")
+             else "llama2-7b-32L-palu50-gs4" + ("-plan" if args.plan else ""))
     return {"workload": (f"{model}-rk{args.rank_k}-rv{args.rank_v}-"
                          + ("rope" if args.rope == "on" else "norope")),
             "context": args.context, "rank_k": args.rank_k, "rank_v": args.rank_v,
@@ -450,7 +461,8 @@ def main():
     weights, fused, cache = synthetic_engine(layers=args.layers, batch=args.batch,
                                              context=args.context, extra=extra, bits=args.bits,
                                              dtype=args.dtype, seed=1234 + (0 if heads else rank),
-                                             rank_k=args.rank_k, rank_v=args.rank_v,
+                                             rank_k=args.plan[0] if args.plan else args.rank_k,
+                                             rank_v=args.plan[1] if args.plan else args.rank_v,
                                              rope=args.rope == "on", rope_base=args.rope_base,
                                              kv_heads=args.kv_heads)
     if heads:

@@ -192,29 +192,36 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
     g = torch.Generator(device=dev)
     g.manual_seed(seed)
     G = n_heads // s
-    rk, rv = (rank_k,) * G, (rank_v,) * G
-    rk_pad, rv_pad = _round_up(rank_k, 128), _round_up(rank_v, 128)
-    ko = n_heads * rank_v
-    ko_pad = _round_up(ko, 8)
+
+    def per_layer(r):
+        # int (uniform) | per-layer tuples of per-group ranks (rank_plan.kv_plan)
+        return [tuple([r] * G)] * layers if isinstance(r, int) else [tuple(int(x) for x in t) for t in r]
+
+    ranks_k_l, ranks_v_l = per_layer(rank_k), per_layer(rank_v)
 
     def U(*shape, scale):
         return ((torch.rand(*shape, generator=g, device=dev, dtype=torch.float32) * 2 - 1) * scale)
 
     i32 = lambda v: torch.tensor(list(v), dtype=torch.int32, device=dev)
-    lat_k = [i * rank_k for i in range(G)]
-    lat_v = [i * rank_v for i in range(G)]
     fl, wl, dl = [], [], []
     gran = Granularity.group_head(s) if 1 < s < n_heads else (
         Granularity.multi_head() if s == 1 else Granularity.joint_head(n_heads))
-    qdim = d if rope else n_heads * rank_k  # rope off: w1 starts with wq_fused^T
     for li in range(layers):
-        n1 = qdim + G * (rank_k + rank_v)
+        rk, rv = ranks_k_l[li], ranks_v_l[li]
+        rk_pad, rv_pad = _round_up(max(rk), 128), _round_up(max(rv), 128)
+        ko = s * sum(rv)
+        ko_pad = _round_up(ko, 8)
+        lat_k = [sum(rk[:i]) for i in range(G)]
+        lat_v = [sum(rv[:i]) for i in range(G)]
+        qdim = d if rope else s * sum(rk)  # rope off: w1 starts with wq_fused^T
+        n1 = qdim + sum(rk) + sum(rv)
         w1 = U(n1, d, scale=1.0 / math.sqrt(d)).to(tdt)
         bk = torch.zeros(G, rk_pad, s * head_dim, device=dev, dtype=tdt)
-        if kv_heads:  # one KV head's B columns replicated over its query heads
-            bk[:, :rank_k] = U(G, rank_k, head_dim, scale=1.0 / math.sqrt(rank_k)).repeat(1, 1, s).to(tdt)
-        else:
-            bk[:, :rank_k] = U(G, rank_k, s * head_dim, scale=1.0 / math.sqrt(rank_k)).to(tdt)
+        for gg, r in enumerate(rk):
+            if kv_heads:  # one KV head's B columns replicated over its query heads
+                bk[gg, :r] = U(r, head_dim, scale=1.0 / math.sqrt(r)).repeat(1, s).to(tdt)
+            else:
+                bk[gg, :r] = U(r, s * head_dim, scale=1.0 / math.sqrt(r)).to(tdt)
         # wo_fused rows: (B_v block @ W_o block); entries ~ scale of a product
         woT = torch.zeros(d, ko_pad, device=dev, dtype=tdt)
         woT[:, :ko] = U(d, ko, scale=1.0 / math.sqrt(3.0 * d)).to(tdt)
@@ -228,10 +235,8 @@ def synthetic_engine(d=4096, n_heads=32, head_dim=128, s=4, rank_k=256, rank_v=2
                              q_off_dev=i32(_head_offsets(rk, s, n_heads))))
         sh = _shape_only(d, d)
         wl.append(LayerWeights(sh, sh, sh, sh))
-        kg = tuple(GroupFactors(_shape_only(d, rank_k), _shape_only(rank_k, s * head_dim), rank_k)
-                   for _ in range(G))
-        vg = tuple(GroupFactors(_shape_only(d, rank_v), _shape_only(rank_v, s * head_dim), rank_v)
-                   for _ in range(G))
+        kg = tuple(GroupFactors(_shape_only(d, r), _shape_only(r, s * head_dim), r) for r in rk)
+        vg = tuple(GroupFactors(_shape_only(d, r), _shape_only(r, s * head_dim), r) for r in rv)
         dl.append(LayerKV(DecomposedLayer(gran, kg, d, head_dim, n_heads),
                           DecomposedLayer(gran, vg, d, head_dim, n_heads)))
     config = AttentionConfig(d, n_heads, head_dim, layers=layers, rope=rope, rope_base=rope_base)

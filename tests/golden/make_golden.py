@@ -360,7 +360,46 @@ def gen_gqa():
     _save("gqa_step.npz", **out)
 
 
+def gen_plan():
+    """a layer- and group-varying (r_k, r_v) plan from the
+    reference's own ranks.allocate (K budget 25 %, V 75 %: the paper's
+    K-light / V-heavy split) on deterministic synthetic Fisher scores, and a
+    two-layer Llama-2-7B-shaped decode step of the unmodified reference with
+    those ranks."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2407_21118_b200 import rank_plan as RP
+    from palu.ranks import FisherScore, allocate
+    d, n, dh, s, layers, T, G = 4096, 32, 128, 4, 2, 1024, 8
+    out = {}
+    plans = {}
+    for side, rate in (("k", 0.25), ("v", 0.75)):
+        mine = RP.synthetic_fisher_scores(layers, G, side)
+        ref = allocate([FisherScore(x.target_id, x.score) for x in mine], [s * dh] * layers * G, d, rate,
+                       min_rank=8)
+        plans[side] = [[ref.rank_for(RP.target_id(li, side, g)) for g in range(G)] for li in range(layers)]
+        out[f"scores_{side}"] = np.array([x.score for x in mine])
+        out[f"ranks_{side}"] = np.array(plans[side])
+    config = AttentionConfig(d, n, dh, layers=layers, rope=True, rope_base=10000.0)
+    lws, kvs = [], []
+    for li in range(layers):
+        lw, kv = _synth_ref_layer(d, n, dh, s, plans["k"][li], s, plans["v"][li], 9100 + 101 * li)
+        lws.append(lw)
+        kvs.append(kv)
+    weights = ModelWeights(layers=tuple(lws))
+    fused = build_fused(weights, kvs, config)
+    cache = LatentKVCache(kvs, config, bits=16)
+    for li in range(layers):
+        _direct_fill(cache, kvs[li], li, random_matrix(T, d, seed=9100 + 101 * li + 77).data)
+    cache.t = T
+    x_t = random_matrix(1, d, seed=9178).data[0]
+    t0 = time.time()
+    out["out1"] = palu_decode_step_rope(weights, fused, cache, x_t)
+    out["meta"] = np.array([d, n, dh, s, layers, T, 9100], dtype=np.float64)
+    print(f"plan: K ranks {plans['k']} V ranks {plans['v']} ({time.time() - t0:.1f}s)")
+    _save("plan_step.npz", **out)
+
+
 if __name__ == "__main__":
-    which = sys.argv[1:] or ["rng", "quant", "small", "medium", "c1", "gqa"]
+    which = sys.argv[1:] or ["rng", "quant", "small", "medium", "c1", "gqa", "plan"]
     for w in which:
         globals()[f"gen_{w}"]()

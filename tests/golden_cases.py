@@ -86,3 +86,15 @@ def gqa_case(g, ci):
     return dict(layer=L, x_rows=x_rows, x_t=x_t, bits=bits, base=float(base), n=nq, n_kv=nkv,
                 dh=dh, d=d, T=T, out1=g[p + "out1"])
 
+
+def plan_case(g):
+    """gen_plan (make_golden.py): two layers with the reference plan's ranks."""
+    d, n, dh, s, layers, T, seed = (int(v) for v in g["meta"])
+    rk, rv = g["ranks_k"], g["ranks_v"]
+    Ls = [po.synth_layer(d, n, dh, s, [int(r) for r in rk[li]], s, [int(r) for r in rv[li]],
+                         seed + 101 * li) for li in range(layers)]
+    x_rows = [po.random_matrix(T, d, seed + 101 * li + 77) for li in range(layers)]
+    x_t = po.random_matrix(1, d, 9178)[0]
+    return dict(layers=Ls, x_rows=x_rows, x_t=x_t, n=n, dh=dh, d=d, T=T, out1=g["out1"],
+                ranks_k=rk, ranks_v=rv)
+

@@ -12,7 +12,7 @@ import numpy as np
 import pytest
 
 from conftest import rel_err
-from golden_cases import c1_case, gqa_case, medium_case, oracle_step_from_fill, small_case
+from golden_cases import c1_case, gqa_case, plan_case, medium_case, oracle_step_from_fill, small_case
 from oracle import palu_oracle as po
 
 pytestmark = pytest.mark.gpu
@@ -489,4 +489,24 @@ def test_gqa_replicated_b_matches_reference(P, golden, dtype):
         tol = TOL[dtype] if min(case["bits"]) == 16 else max(TOL[dtype], 1e-2)
         e = rel_err(y, case["out1"])
         assert e < tol, (name, dtype, e)
+
+
+def test_rank_plan_two_layers_bf16(P, golden):
+    """layer- and group-varying (r_k, r_v) from the reference's
+    ranks.allocate (K 25 %, V 75 %; K ranks 55..227, V ranks 193..512), two
+    chained Llama-2-7B-shaped layers on the bf16 GPU path against the
+    reference's output."""
+    from paper_2407_21118_b200.harness import fill_cache_direct, set_cache_t
+    case = plan_case(golden("plan_step.npz"))
+    w, dec, cfg = _to_types(P, case["layers"], case["n"], case["dh"], True)
+    fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
+    cache = P.LatentKVCache(dec, cfg, 16, dtype="bfloat16", capacity=case["T"] + 8)
+    for li in range(len(case["layers"])):
+        fill_cache_direct(cache, li, case["x_rows"][li])
+    set_cache_t(cache, case["T"])
+    y = P.palu_decode_step_rope(w, fused, cache, case["x_t"])
+    sess = cache._session
+    assert all(sess.tc_layers) and all(sess.value_tc_layers)
+    e = rel_err(y, case["out1"])
+    assert e < TOL["bfloat16"], e
 
