@@ -20,7 +20,8 @@ from .attention import (
     palu_prefill,
     rope_apply,
 )
-from . import container
+from . import container, offline, rank_plan
+from .offline import decompose_gpu, fuse_hadamard_gpu
 from .container import export_latents
 from .dense import DecodeResult, DenseModel, reference_decode
 from .errors import GoldenMismatchError, NumericalError, PaluError, ValidationError

@@ -155,13 +155,17 @@ def _rank_pad(r: int, dtype: str, bits: int = 16) -> int:
     return _round_up(max(r, 1), m)
 
 
-def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=None) -> FusedWeights:
+def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=None,
+                prep: str = "host") -> FusedWeights:
     """attention.py:194-232, then upload in the kernels' layouts.
 
     Per head i of value group g: wo block = B_v[g][:, i-in-g] @ W_o[rows i];
     the key-side fusion into W_q only exists without rotary embedding.
-    Offline prep runs once in fp64 on the host (as in the reference).
+    Offline prep runs once in fp64: on the host (prep="host", as the
+    reference) or as batched fp64 GEMMs on the GPU (prep="gpu", offline.py).
     """
+    if prep not in ("host", "gpu"):
+        raise ValidationError(f"prep must be 'host' or 'gpu', got {prep!r}")
     torch = _torch()
     code, tdt = _dt(dtype)
     validate_weights(weights, config)
@@ -183,13 +187,19 @@ def build_fused(weights, decomposed, config, *, dtype: str = "float32", device=N
         av = [as_array(g.a) for g in kv.value.groups]
         bv = [as_array(g.b) for g in kv.value.groups]
         o_blocks, q_blocks = [], []
-        for i in range(n):
-            gk, pk = divmod(i, s_k)
-            gv, pv = divmod(i, s_v)
+        if prep == "gpu":
+            from .offline import fused_blocks_gpu
+            wo_fused, wq_gpu = fused_blocks_gpu(wq, wo, bk, bv, n, dh, s_k, s_v, config.rope, device=dev)
             if not config.rope:
-                q_blocks.append(wq[:, i * dh:(i + 1) * dh] @ bk[gk][:, pk * dh:(pk + 1) * dh].T)
-            o_blocks.append(bv[gv][:, pv * dh:(pv + 1) * dh] @ wo[i * dh:(i + 1) * dh, :])
-        wo_fused = np.concatenate(o_blocks, axis=0)
+                q_blocks = [wq_gpu]
+        else:
+            for i in range(n):
+                gk, pk = divmod(i, s_k)
+                gv, pv = divmod(i, s_v)
+                if not config.rope:
+                    q_blocks.append(wq[:, i * dh:(i + 1) * dh] @ bk[gk][:, pk * dh:(pk + 1) * dh].T)
+                o_blocks.append(bv[gv][:, pv * dh:(pv + 1) * dh] @ wo[i * dh:(i + 1) * dh, :])
+            wo_fused = np.concatenate(o_blocks, axis=0)
         key_ranks = tuple(g.rank for g in kv.key.groups)
         value_ranks = tuple(g.rank for g in kv.value.groups)
         rk_pad = _round_up(max(key_ranks), 128)  # covers every store width below
