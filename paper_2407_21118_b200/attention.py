@@ -826,11 +826,20 @@ def palu_decode_step_quantized(weights, fused, cache, x_t, tile_len=None) -> np.
 
 
 def palu_prefill(weights, decomposed, config, prompt, bits=FP_BITS, fused=None, tile_len=None,
-                 *, dtype: str = "float32") -> LatentKVCache:
-    """attention.py:469-494: token-by-token steps, keeping only the cache."""
+                 *, dtype: str = "float32", batched: bool = True) -> LatentKVCache:
+    """attention.py:469-494: the cache after feeding the prompt.
+
+    batched=True (rope on): one causal attention pass per layer over the
+    whole prompt (prefill.py); batched=False: token-by-token decode steps,
+    the reference's own schedule."""
     tokens = np.asarray(prompt, dtype=np.float64)
     if tokens.ndim != 2 or tokens.shape[1] != config.d_model:
         raise ValidationError(f"prompt must be (T, {config.d_model})")
+    if tile_len is not None and tile_len < 1:
+        raise ValidationError(f"tile_len must be >= 1, got {tile_len}")
+    if batched and config.rope:
+        from .prefill import palu_prefill_batched
+        return palu_prefill_batched(weights, decomposed, config, tokens, bits, fused, tile_len, dtype=dtype)
     if fused is None:
         fused = build_fused(weights, decomposed, config, dtype=dtype)
     cache = LatentKVCache(decomposed, config, bits, dtype=fused.dtype,

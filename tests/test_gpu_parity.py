@@ -571,3 +571,72 @@ def test_build_fused_gpu_prep_equals_host(P, golden, rope):
     import torch
     assert torch.equal(host.layers[0].woT, gpu.layers[0].woT) or \
         torch.allclose(host.layers[0].woT, gpu.layers[0].woT, rtol=1e-6, atol=1e-7)
+
+
+def test_batched_prefill_matches_stepwise(P, golden):
+    """palu_prefill as one causal attention pass per layer
+    (prefill.py) leaves the cache the reference's token-by-token prefill
+    leaves: the reference's own stored latents (small_decode fixtures, fp32
+    path) and the GPU stepwise prefill; then one decode step from each."""
+    from paper_2407_21118_b200.attention import palu_prefill
+    g = golden("small_decode.npz")
+    done = 0
+    for ci, name in enumerate(g["names"]):
+        case = small_case(g, ci)
+        if not case["rope"]:
+            continue
+        w, dec, cfg = _to_types(P, case["layers"], case["n"], case["dh"], True, case["base"])
+        bits = case["bits"] if case["bits"][0] != case["bits"][1] else case["bits"][0]
+        toks = case["tokens"]
+        fast = palu_prefill(w, dec, cfg, toks, bits=bits, batched=True)
+        slow = palu_prefill(w, dec, cfg, toks, bits=bits, batched=False)
+        assert fast.t == slow.t == case["T"]
+        for li in range(len(case["layers"])):
+            if fast.k_bits == 16:
+                ref = g[f"c{ci}_L{li}_hk"]
+                assert rel_err(fast.hk(li), ref) < 1e-5, (name, li)
+                assert rel_err(fast.hk(li), slow.hk(li)) < 1e-5, (name, li)
+            else:
+                qf = fast.layers[li].k_groups[0].quantized_latent()
+                qs = slow.layers[li].k_groups[0].quantized_latent()
+                assert np.mean(qf.codes == qs.codes) > 0.95, name
+                assert np.max(np.abs(qf.codes.astype(int) - qs.codes.astype(int))) <= 1, name
+        x = toks[-1]
+        fused = P.build_fused(w, dec, cfg)
+        ya = P.palu_decode_step_rope(w, fused, fast, x)
+        yb = P.palu_decode_step_rope(w, fused, slow, x)
+        tol = 1e-5 if min(case["bits"]) == 16 else 2e-2
+        assert rel_err(ya, yb) < tol, (name, rel_err(ya, yb))
+        done += 1
+    assert done >= 8
+
+
+def test_batched_prefill_llama_shape_bf16(P):
+    """The batched prefill at the Llama-2-7B layer shape (bf16, 2 layers,
+    1K-token prompt) against token-by-token prefill: same cache, same next
+    step; and it is the faster of the two."""
+    import time
+    from oracle import palu_oracle as po
+    from paper_2407_21118_b200.attention import palu_prefill
+    from long_parity import make_layers, to_package
+    layers = make_layers(2, rk=128, rv=256, seed=700)
+    w, dec, cfg = to_package(layers, 32, 128, True, 10000.0)
+    fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
+    toks = po.random_matrix(1024, 4096, 701) * 0.5
+    import torch
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    fast = palu_prefill(w, dec, cfg, toks, fused=fused, batched=True)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    slow = palu_prefill(w, dec, cfg, toks, fused=fused, batched=False)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    for li in range(2):
+        assert rel_err(fast.hk(li), slow.hk(li)) < 2e-2, li  # bf16 rows; a rounding may differ
+    x = toks[-1]
+    ya = P.palu_decode_step_rope(w, fused, fast, x)
+    yb = P.palu_decode_step_rope(w, fused, slow, x)
+    assert rel_err(ya, yb) < 5e-3
+    print(f"prefill 1024 tokens x 2 layers: batched {t1 - t0:.3f} s, stepwise {t2 - t1:.3f} s")
+    assert t1 - t0 < t2 - t1
