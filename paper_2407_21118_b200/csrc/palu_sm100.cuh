@@ -12,7 +12,8 @@ constexpr int TILE_M = 128;    // tokens per tile = TMEM lanes
 constexpr int N_CTA = 256;     // accumulator columns: 2 heads x (64 u + 64 w)
 constexpr int KB = 64;         // bf16 per 128-byte swizzled row
 constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + EPI_WARPS * 32 + 64;  // + 2 converter warps (quantised keys)
+constexpr int THREADS = 64 + EPI_WARPS * 32 + 64;    // score kernel: + 2 converter warps
+constexpr int THREADS_Q = 64 + EPI_WARPS * 32 + 128;  // packed keys: + 4 converter warps
 constexpr int H_STAGE_BYTES = TILE_M * 128;  // 16 KB per (tile, k-block)
 constexpr int UW_KB_BYTES = N_CTA * 128;     // 32 KB per k-block
 constexpr int SMEM_LIMIT = 232448;           // 227 KB opt-in

@@ -72,7 +72,10 @@ __device__ __forceinline__ unsigned smid_u32() {
   return r;
 }
 
-constexpr int CONV_WARPS = 2;    // quantised keys: code -> bf16 converter warps per SM
+constexpr int CONV_WARPS = 2;    // rope-off latent score: code -> bf16 converter warps per SM
+// rope-on score: 4 converter warps (one token row per lane).  2 warps (two
+// rows per lane) left the int4-key score at 173 us vs 99 us for bf16 keys;
+// 12 warps per CTA still fit the 168-register budget (3 per scheduler quadrant)
 constexpr int CODE_BIAS = 128;   // bits <= 4: bf16(128 + c) has bit pattern 0x4300 | c
 
 // Unpack this SM's 128-token tile of packed key codes into the SW128 K-major
@@ -110,18 +113,18 @@ struct ItemPos {
 };
 
 
-template <int BITS, class PP>
+template <int BITS, int RPL, class PP>
 __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t* full,
                                              uint64_t* empty, int bg, int tile, int T_rows,
                                              int kblocks, int cl, Ring& rg) {
   constexpr int NW = BITS;  // 8-byte words per row per 64-code k-block
   const int lane = threadIdx.x & 31;
-  const uint8_t* rowp[2];
-  bool ok[2];
-  float zr[2];
+  const uint8_t* rowp[RPL];
+  bool ok[RPL];
+  float zr[RPL];
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int t = tile * TILE_M + cl + 64 * rr;
+  for (int rr = 0; rr < RPL; ++rr) {
+    const int t = tile * TILE_M + cl + (TILE_M / RPL) * rr;
     ok[rr] = t < T_rows;
     const size_t tok = (size_t)bg * p.T_cap + (ok[rr] ? t : 0);
     rowp[rr] = p.codes + tok * p.code_row_bytes;
@@ -134,10 +137,10 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     // shift and a LOP3: 0x43004300 | ((w >> BITS k) & mask)
     constexpr uint32_t MASK = BITS == 4 ? 0x000F000Fu : 0x00030003u;
     constexpr int NV = 2 * BITS / 4;  // uint4 loads per row per k-block (32 B int4, 16 B int2)
-    uint4 nx[2][2], cu[2][2];
+    uint4 nx[RPL][2], cu[RPL][2];
     auto load4 = [&](int kb) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
+      for (int rr = 0; rr < RPL; ++rr)
 #pragma unroll
         for (int q = 0; q < NV; ++q)
           nx[rr][q] = ok[rr] ? __ldg(reinterpret_cast<const uint4*>(rowp[rr] + kb * 8 * BITS) + q)
@@ -146,7 +149,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     load4(0);
     for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr)
+      for (int rr = 0; rr < RPL; ++rr)
 #pragma unroll
         for (int q = 0; q < NV; ++q) cu[rr][q] = nx[rr][q];
       if (kb + 1 < kblocks) load4(kb + 1);
@@ -154,8 +157,8 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
       mbar_wait(&empty[stage], rg.phase ^ 1);
       uint8_t* sb = s_h + stage * H_STAGE_BYTES;
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int row = cl + 64 * rr;
+      for (int rr = 0; rr < RPL; ++rr) {
+        const int row = cl + (TILE_M / RPL) * rr;
         const uint32_t words[8] = {cu[rr][0].x, cu[rr][0].y, cu[rr][0].z, cu[rr][0].w,
                                    cu[rr][1].x, cu[rr][1].y, cu[rr][1].z, cu[rr][1].w};
         // c - z: one bf16x2 subtract of (128 + z) from (128 + c), exact when
@@ -195,10 +198,10 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     }
     return;
   }
-  unsigned long long nxt[2][NW], cur[2][NW];
+  unsigned long long nxt[RPL][NW], cur[RPL][NW];
   auto load = [&](int kb) {
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+    for (int rr = 0; rr < RPL; ++rr)
 #pragma unroll
       for (int q = 0; q < NW; ++q)
         nxt[rr][q] = ok[rr] ? __ldg(reinterpret_cast<const unsigned long long*>(rowp[rr] + kb * 8 * BITS) + q)
@@ -207,7 +210,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
   load(0);
   for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr)
+    for (int rr = 0; rr < RPL; ++rr)
 #pragma unroll
       for (int q = 0; q < NW; ++q) cur[rr][q] = nxt[rr][q];
     if (kb + 1 < kblocks) load(kb + 1);
@@ -215,8 +218,8 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     mbar_wait(&empty[stage], rg.phase ^ 1);
     uint8_t* sb = s_h + stage * H_STAGE_BYTES;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
-      const int row = cl + 64 * rr;
+    for (int rr = 0; rr < RPL; ++rr) {
+      const int row = cl + (TILE_M / RPL) * rr;
 #pragma unroll
       for (int ch = 0; ch < 8; ++ch) {  // 8 codes -> one 16-byte swizzled chunk
         uint32_t wv[4];
@@ -265,7 +268,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
 // short ranks (r <= 128: 8 MMAs per unit) the accumulator must be quad-
 // buffered to cover the ~1 us from a unit's last MMA issue to its epilogue
 // (tools/score_trace.py: 2 slots left the tensor pipe ~45 % idle at r 128).
-template <int UH>
+template <int UH, int NCONV>
 __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUtensorMap& map_uw,
                                            const Params& p, uint8_t* smem) {
   constexpr int NSLOT = UH == 2 ? 2 : 4;
@@ -305,7 +308,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     prefetch_map(&map_uw);
     for (int s = 0; s < p.stages; ++s) {
       // raw bf16: the leader's expect_tx; quantised: both SMs' converter warps
-      mbar_init(&full[s], p.bits == 16 ? 1 : 2 * CONV_WARPS);
+      mbar_init(&full[s], p.bits == 16 ? 1 : 2 * NCONV);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NSLOT; ++a) {
@@ -469,17 +472,17 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       // the newest token's codes and zero point come from this step's latent
       // append: wait for the predecessor chain before the first code load
       pdl_wait();
-      const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // rows cl, cl + 64 of the SM's tile
+      const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // the SM tile's row(s) of this lane
       Ring rg;
       ItemPos ip_(i0, n_super, p.G);
       for (int i = i0; i < i1; ++i, ip_.next(n_super, p.G)) {
         const int bg = ip_.bg, st = ip_.st;
         const int tile = 2 * st + (int)rank;
         switch (p.bits) {
-          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 2: convert_tile<2, TILE_M / (NCONV * 32)>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 3: convert_tile<3, TILE_M / (NCONV * 32)>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 4: convert_tile<4, TILE_M / (NCONV * 32)>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          default: convert_tile<8, TILE_M / (NCONV * 32)>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
         }
       }
     }
@@ -613,8 +616,11 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   }
 }
 
-template <int UH>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// NCONV converter warps: 2 for raw bf16 keys (idle; 10 warps keep 168
+// registers), 4 for packed keys (2 left the int4-key score at 173 us vs 156
+// with 4; the 12-warp build gets 128 registers)
+template <int UH, int NCONV>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + EPI_WARPS * 32 + NCONV * 32, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
   // setup overlaps the query absorb; only the UW loads read its output
@@ -627,7 +633,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  score_role<UH>(map_h, map_uw, p, smem);
+  score_role<UH, NCONV>(map_h, map_uw, p, smem);
 }
 
 // ===========================================================================
@@ -1400,7 +1406,7 @@ rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
   }
   if ((int)(blockIdx.x >> 1) < p.score_pairs) {
-    score_role<2>(map_h, map_uw, p, smem);
+    score_role<2, 2>(map_h, map_uw, p, smem);
   } else {
     const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
     value_role(map_v, p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
@@ -1656,10 +1662,10 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile, tile = i - bg * ntile;
         switch (p.bits) {
-          case 2: convert_tile<2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          case 3: convert_tile<3>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          case 4: convert_tile<4>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
-          default: convert_tile<8>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 2: convert_tile<2, 2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 3: convert_tile<3, 2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          case 4: convert_tile<4, 2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
+          default: convert_tile<8, 2>(p, s_h, full, empty, bg, tile, T_rows, kblocks, cl, rg); break;
         }
       }
     }
@@ -1902,9 +1908,11 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   const size_t smem = (size_t)fixed + (size_t)stages * H_STAGE_BYTES;
   static bool attr = false;
   if (!attr) {
-    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_LIMIT));
-    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_LIMIT));
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_LIMIT));
     attr = true;
   }
@@ -1945,10 +1953,13 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
     g_trace_ctas = sms & ~1;
   }
   if (uh == 1)
-    PALU_CK(launch_k(rope_score_tc_kernel<1>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+    PALU_CK(launch_k(rope_score_tc_kernel<1, 2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
                      map_h, map_uw, prm));
+  else if (bits != 16)
+    PALU_CK(launch_k(rope_score_tc_kernel<2, 4>, dim3(sms & ~1), dim3(THREADS_Q), smem,
+                     (cudaStream_t)stream, map_h, map_uw, prm));
   else
-    PALU_CK(launch_k(rope_score_tc_kernel<2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+    PALU_CK(launch_k(rope_score_tc_kernel<2, 2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
                      map_h, map_uw, prm));
   PALU_LAUNCHED();
   return PALU_OK;

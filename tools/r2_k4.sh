@@ -1,0 +1,6 @@
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "quantized_keys or fused or medium or c1 or tcgen05_score" 2>&1 | tail -2
+for v in "default:" "int4:--bits 4" "k16v4:--rank-k 128 --rank-v 384 --bits 16,4" "k4v4p:--rank-k 128 --rank-v 384 --bits 4"; do
+  name=${v%%:*}; args=${v#*:}
+  timeout 200 python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-baseline $args > gpurun_out/r2_bench_k4_$name.log 2>&1
+  tail -1 gpurun_out/r2_bench_k4_$name.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$name', round(d['value'],1), {k: round(v*1e3,1) for k,v in d['roofline']['per_kernel_ms'].items()})" 2>/dev/null || echo "$name failed"
+done
