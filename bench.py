@@ -567,12 +567,15 @@ def main():
     # measured DRAM traffic of the dominant kernel, from a committed ncu capture
     # of the same workload (profiles/*_traffic.json), else null
     workload = workload_config(args, 1, False)["workload"]
+    bits_key = list(args.bits) if isinstance(args.bits, tuple) else args.bits
     for tf_name in ("r02_traffic.json", "r01_traffic.json"):
         try:
             with open(os.path.join(ROOT, "profiles", tf_name)) as fh:
-                tr = json.load(fh).get(score_name)
-            if (tr and tr["workload"] == workload and tr["context"] == args.context
-                    and tr["batch"] == args.batch and tr.get("bits", 16) == args.bits):
+                entries = json.load(fh).get(score_name) or []
+            entries = entries if isinstance(entries, list) else [entries]
+            tr = next((e for e in entries if e["workload"] == workload and e["context"] == args.context
+                       and e["batch"] == args.batch and e.get("bits", 16) == bits_key), None)
+            if tr:
                 roofline_head["traffic"] = tr["bytes"]
                 roofline_head["traffic_source"] = "profiles/" + tr["capture"]
                 break
