@@ -37,30 +37,46 @@ def needs_build() -> bool:
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not needs_build():
+def build(force: bool = False, verbose: bool = False, defines=(), out_dir: str = "") -> str:
+    """Compile every CUDA source (in parallel) and link libpalu_b200.so.
+
+    ``defines`` / ``out_dir`` build a variant library elsewhere (e.g. the
+    diagnostic build with -DPALU_DIAG -DPALU_TRACE under abtmp/diag/, loaded
+    through PALU_LIB_PATH for A/B timing); the product build uses neither."""
+    lib = os.path.join(out_dir, "libpalu_b200.so") if out_dir else LIB
+    if not out_dir and not defines and not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+
     nvcc = _nvcc()
-    objs = []
-    tmp = os.path.join(HERE, "build")
+    tmp = os.path.join(out_dir or HERE, "build")
     os.makedirs(tmp, exist_ok=True)
+    jobs = []
     for src in SOURCES:
         path = os.path.join(CSRC, src)
         if not os.path.exists(path):
             continue
         obj = os.path.join(tmp, src.replace(".cu", ".o"))
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr", "-c", path, "-o", obj]
+               "-I", INCLUDE, "-I", CSRC, "--expt-relaxed-constexpr", *defines, "-c", path, "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
             print(" ".join(cmd), flush=True)
-        subprocess.run(cmd, check=True)
-        objs.append(obj)
-    out = LIB + ".tmp"
-    subprocess.run([nvcc, *ARCH, "-shared", "-o", out, *objs, "-lcuda"], check=True)
-    os.replace(out, LIB)
-    return LIB
+        jobs.append((cmd, obj))
+    with ThreadPoolExecutor(max_workers=len(jobs) or 1) as ex:
+        for f in [ex.submit(subprocess.run, cmd, check=True) for cmd, _ in jobs]:
+            f.result()
+    out = lib + ".tmp"
+    subprocess.run([nvcc, *ARCH, "-shared", "-o", out, *[o for _, o in jobs], "-lcuda"], check=True)
+    os.replace(out, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    out_dir = ""
+    if "--out" in args:
+        out_dir = args[args.index("--out") + 1]
+        os.makedirs(out_dir, exist_ok=True)
+    print(build(force="--force" in args, verbose="-v" in args,
+                defines=[a for a in args if a.startswith("-D")], out_dir=out_dir))

@@ -53,9 +53,25 @@ struct Params {
 };
 
 constexpr int TRACE_STRIDE = 512;
+constexpr int SU = 8;  // score trace marks per accumulator unit
+// score epilogue shared memory: the cross-warp reduction buffer, then per
+// epilogue warp two (cos/sin base half-row 256 B, lane scales 128 B) buffers
+constexpr int EPI_RED_BYTES = 4 * 2 * 128 * 4;
+constexpr int EPI_STAGE_BYTES = 2 * 256 + 2 * 128;
+constexpr int SCORE_FIXED_BYTES = 512 + EPI_RED_BYTES + EPI_WARPS * EPI_STAGE_BYTES;
 
 // Profiling modes that skip MMAs or barrier waits (results invalid) exist only
 // in diagnostic builds (-DPALU_DIAG); the product library ignores the knobs.
+#ifdef PALU_TRACE
+constexpr bool kTrace = true;   // per-CTA timelines (tools/score_trace.py, fused_trace.py)
+#else
+constexpr bool kTrace = false;
+#endif
+#ifdef PALU_DIAG
+constexpr bool kDiag = true;
+#else
+constexpr bool kDiag = false;
+#endif
 #ifdef PALU_DIAG
 static int diag_env(const char* name) { return getenv(name) ? atoi(getenv(name)) : 0; }
 #else
@@ -112,6 +128,16 @@ struct ItemPos {
   }
 };
 
+
+// A converter warp hands its operand rows over with a CTA-local arrive on its
+// own SM's full[stage] (release.cta: no memory barrier).  A cluster-scope
+// release from the converter itself compiles to MEMBAR.GPU, which waits for
+// the warp's in-flight code prefetch loads: it made the prefetch synchronous
+// and cost ~30 % of the packed-key score kernel (int4 r 256: 154 -> 110 us).
+// On the peer SM, warp 1 (idle: only the leader issues MMAs) relays each
+// completed stage to the leader with the cluster-scope release; the leader's
+// MMA issuer acquires at cluster scope.
+__device__ __forceinline__ void conv_arrive(uint64_t* bar) { mbar_arrive(bar); }
 
 template <int BITS, int RPL, class PP>
 __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t* full,
@@ -192,9 +218,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
       if (lane == 0)
-        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                         smem_u32(&full[stage]) & PEER_MASK)
-                     : "memory");
+        conv_arrive(&full[stage]);
     }
     return;
   }
@@ -247,9 +271,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncwarp();
     if (lane == 0)
-      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
-                       smem_u32(&full[stage]) & PEER_MASK)
-                   : "memory");
+      conv_arrive(&full[stage]);
   }
 }
 
@@ -291,6 +313,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   float* red = reinterpret_cast<float*>(tmem_slot + 4);  // [NSLOT][UH heads][128]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int mode = kDiag ? p.mode : 0;  // profiling modes exist in diagnostic builds only
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int pair_id = blockIdx.x >> 1, n_pairs = p.score_pairs;
@@ -300,7 +323,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   const int per = (total + n_pairs - 1) / n_pairs;
   const int i0 = min(total, pair_id * per);
   const int i1 = min(total, i0 + per);
-  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0)
+  if (kTrace && p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0)
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 0] = gtimer();
 
   if (warp == 0 && lane == 0) {
@@ -308,7 +331,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     prefetch_map(&map_uw);
     for (int s = 0; s < p.stages; ++s) {
       // raw bf16: the leader's expect_tx; quantised: both SMs' converter warps
-      mbar_init(&full[s], p.bits == 16 ? 1 : 2 * NCONV);
+      mbar_init(&full[s], p.bits == 16 ? 1 : NCONV + (leader ? 1 : 0));  // + the peer's relay
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < NSLOT; ++a) {
@@ -331,7 +354,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
-  if (p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0) {
+  if (kTrace && p.trace != nullptr && p.ready == nullptr && threadIdx.x == 0) {
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = gtimer();
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 511] = clock64();  // per-unit marks are SM clocks
   }
@@ -420,10 +443,10 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         }
         for (int h = 0; h < units; ++h, ++unit) {
           const int slot = unit & (NSLOT - 1);
-          if ((p.mode & 4) == 0) mbar_wait(&tempty[slot], ((unit / NSLOT) & 1) ^ 1);
+          if ((mode & 4) == 0) mbar_wait(&tempty[slot], ((unit / NSLOT) & 1) ^ 1);
           fence_after();
-          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE && lane == 0)
-            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + 4 * unit] = clock64();
+          if (kTrace && p.trace != nullptr && p.ready == nullptr && SU * unit + 11 < TRACE_STRIDE && lane == 0)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + SU * unit] = clock64();
           const uint32_t d_tmem = tmem_base + slot * SLOT_COLS;
           for (int kb = 0; kb < kblocks; ++kb) {
             int stage = st0 + kb, par = ph0;
@@ -431,13 +454,16 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
               stage -= p.stages;
               par ^= 1;
             }
-            if (h == 0 && (p.mode & 2) == 0) {
-              mbar_wait(&full[stage], par);
+            if (h == 0 && (mode & 2) == 0) {
+              if (p.bits == 16)
+                mbar_wait(&full[stage], par);
+              else
+                mbar_wait_cluster(&full[stage], par);  // the peer's stages: a cluster-scope release
               fence_after();
             }
             // profile modes 8 / 16 (diagnostics): pin the A / B operand tile
-            const uint32_t a0 = h_addr + ((p.mode & 8) ? 0 : stage) * H_STAGE_BYTES;
-            const uint32_t b0 = uw_addr + ((p.mode & 16) ? 0 : (kb * units + h)) * UWB;
+            const uint32_t a0 = h_addr + ((mode & 8) ? 0 : stage) * H_STAGE_BYTES;
+            const uint32_t b0 = uw_addr + ((mode & 16) ? 0 : (kb * units + h)) * UWB;
             // K16 steps are 32 B apart: +2 in the descriptor's address field
             // (smem addresses < 256 KB, so the 14-bit field cannot carry)
             const uint64_t da = sdesc(a0), db = sdesc(b0);
@@ -451,8 +477,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           }
           if (elect_one()) umma2_commit_both(&tfull[slot]);
           __syncwarp();
-          if (p.trace != nullptr && p.ready == nullptr && 4 * unit + 7 < TRACE_STRIDE && lane == 0)
-            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + 4 * unit] = clock64();
+          if (kTrace && p.trace != nullptr && p.ready == nullptr && SU * unit + 11 < TRACE_STRIDE && lane == 0)
+            p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 5 + SU * unit] = clock64();
         }
         st0 += kblocks;
         if (st0 >= p.stages) {
@@ -460,11 +486,21 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           ph0 ^= 1;
         }
       }
-      if (p.trace != nullptr && p.ready == nullptr && lane == 0) {  // SM clocks vs wall time of the issue loop
+      if (kTrace && p.trace != nullptr && p.ready == nullptr && lane == 0) {  // SM clocks vs wall time of the issue loop
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 508] = clock64() - c_start;
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 509] = gtimer() - g_start;
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 510] = (unsigned long long)unit * kblocks * (KB / 16);
       }
+    } else if (p.bits != 16 && lane == 0) {
+      // ---------------- peer SM, packed keys: stage relay (see conv_arrive) ----------------
+      Ring rg;
+      for (int i = i0; i < i1; ++i)
+        for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
+          mbar_wait(&full[rg.slot], rg.phase);
+          asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(
+                           smem_u32(&full[rg.slot]) & PEER_MASK)
+                       : "memory");
+        }
     }
   } else if (warp >= 2 + EPI_WARPS) {
     // ---------------- quantised keys: converter warps (both SMs) ----------------
@@ -491,6 +527,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     const int q = warp & 3;          // TMEM lane quarter
     const int jh = (warp - 2) >> 2;  // which 32 of the 64 frequencies
     const int delta = q * 32 + lane; // token row inside this SM's tile
+    constexpr int CH = 8;            // frequencies per epilogue chunk (TMEM loads of 8 columns)
     float2 cd2[16], sd2[16];         // cos/sin(delta th_j) for j pairs (2i, 2i + 1)
     {
       const float4* off =
@@ -503,70 +540,98 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       }
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
+    // Per item the epilogue needs the tile's cos/sin base half-row and (packed
+    // keys) its token scales.  Loaded at the item boundary they cost ~1 us per
+    // item (L2 latency under the HBM stream; tools/score_trace.py at r_k 128:
+    // the tensor pipe idled behind it), so this warp stages them into shared
+    // memory with cp.async one item ahead.
+    uint8_t* eb = reinterpret_cast<uint8_t*>(red) + EPI_RED_BYTES + (warp - 2) * EPI_STAGE_BYTES;
+    auto stage_item = [&](int buf, int tile_, int bg_) {
+      if (lane < 16)
+        cp_async16(eb + buf * 256 + lane * 16,
+                   reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile_ * 64 + jh * 32) + lane);
+      if (p.bits != 16) {
+        const int tq = tile_ * TILE_M + delta;
+        if (tq < T_rows) cp_async4(eb + 512 + buf * 128 + lane * 4, p.scales + (size_t)bg_ * p.T_cap + tq);
+      }
+      cp_async_commit();
+    };
     // quantised keys: the newest token's scale comes from this step's append
     pdl_wait();
     int unit = 0, it = 0;
-    ItemPos ip_(i0, n_super, p.G);
+    ItemPos ip_(i0, n_super, p.G), nx(i0, n_super, p.G);
+    if (i0 < i1) stage_item(0, 2 * nx.st + (int)rank, nx.bg);
+    nx.next(n_super, p.G);
     for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
       const int bg = ip_.bg, st = ip_.st;
       const int b = ip_.b, g = ip_.g;
       const int tile = 2 * st + (int)rank;
-      // this tile's cos/sin base row (fp64-reduced, L2-resident table): issued
-      // before the accumulator wait, so its latency hides behind the MMAs
-      float4 bv4[16];
-      {
-        const float4* base = reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile * 64 + jh * 32);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) bv4[k] = __ldg(base + k);
-      }
+      if (kTrace && p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 && SU * unit + 11 < TRACE_STRIDE)
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 10 + SU * unit] = clock64();
+      cp_async_wait_all();
+      __syncwarp();
+      if (kTrace && p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 && SU * unit + 11 < TRACE_STRIDE)
+        p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 11 + SU * unit] = clock64();
+      const uint32_t base_addr = smem_u32(eb) + (uint32_t)(it & 1) * 256u;
       // quantised keys: the converter wrote c - z, so logit = s_t x (epilogue sum)
       float sq = 1.f;
-      if (p.bits != 16) {
-        const int tq = tile * TILE_M + delta;
-        if (tq < T_rows) sq = __ldg(p.scales + (size_t)bg * p.T_cap + tq);
-      }
-      // cos/sin((t0 + delta) th_j) = base (x) offset, for this thread's 32 frequencies
-      float2 c2[16], s2[16];
-      {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) {
-          const float4 bv = bv4[k];
-          const float2 bc = make_float2(bv.x, bv.z), bsn = make_float2(bv.y, bv.w);
-          const float2 t = fmul2(bsn, sd2[k]);
-          c2[k] = ffma2(bc, cd2[k], make_float2(-t.x, -t.y));
-          s2[k] = ffma2(bsn, cd2[k], fmul2(bc, sd2[k]));
-        }
+      if (p.bits != 16 && tile * TILE_M + delta < T_rows)
+        sq = *reinterpret_cast<const float*>(eb + 512 + (it & 1) * 128 + lane * 4);
+      if (i + 1 < i1) {  // the other buffer was consumed an item ago
+        stage_item((it + 1) & 1, 2 * nx.st + (int)rank, nx.bg);
+        nx.next(n_super, p.G);
       }
       for (int h = 0; h < units; ++h, ++unit) {
         const int slot = unit & (NSLOT - 1);
+        const bool tr = kTrace && p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 &&
+                        SU * unit + 11 < TRACE_STRIDE;
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 9 + SU * unit] = clock64();
         mbar_wait(&tfull[slot], (unit / NSLOT) & 1);
         fence_after();
-        const bool tr = p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 &&
-                        4 * unit + 7 < TRACE_STRIDE;
-        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + 4 * unit] = clock64();
-        float v[2] = {0.f, 0.f};
-        if ((p.mode & 1) == 0)
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + SU * unit] = clock64();
+        float2 acc2[UH];
 #pragma unroll
-        for (int hp = 0; hp < UH; ++hp) {
-          float2 acc2 = make_float2(0.f, 0.f);
+        for (int hp = 0; hp < UH; ++hp) acc2[hp] = make_float2(0.f, 0.f);
+        if ((mode & 1) == 0)
 #pragma unroll
-          for (int jc = 0; jc < 2; ++jc) {
-            float u[16], w[16];
-            const uint32_t col = slot * SLOT_COLS + hp * 128 + jh * 32 + jc * 16;
-            tmem_ld16(lane_base + col, u);
-            tmem_ld16(lane_base + col + 64, w);
-            tmem_wait_ld();
+        for (int jc = 0; jc < 32 / CH; ++jc) {
+          // this chunk's accumulator columns (u_j at col, w_j at col + 64) for
+          // every head of the unit, then cos/sin((t0 + delta) th_j) = base (x)
+          // offset for its CH frequencies while the loads are in flight
+          // (recomputed per unit: persistent per-item copies do not fit in
+          // registers beside the offsets, and spilled values cost an L2 round
+          // trip per use)
+          float u[UH][CH], w[UH][CH];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              acc2 = ffma2(c2[jc * 8 + k], make_float2(u[2 * k], u[2 * k + 1]), acc2);
-              acc2 = ffma2(s2[jc * 8 + k], make_float2(w[2 * k], w[2 * k + 1]), acc2);
-            }
+          for (int hp = 0; hp < UH; ++hp) {
+            const uint32_t col = slot * SLOT_COLS + hp * 128 + jh * 32 + jc * CH;
+            tmem_ld8(lane_base + col, u[hp]);
+            tmem_ld8(lane_base + col + 64, w[hp]);
           }
-          v[hp] = acc2.x + acc2.y;
+          float2 c2[CH / 2], s2[CH / 2];
+#pragma unroll
+          for (int k = 0; k < CH / 2; ++k) {
+            const float4 bv = lds128f(base_addr + (uint32_t)(jc * (CH / 2) + k) * 16u);
+            const float2 bc = make_float2(bv.x, bv.z), bsn = make_float2(bv.y, bv.w);
+            const float2 t = fmul2(bsn, sd2[jc * (CH / 2) + k]);
+            c2[k] = ffma2(bc, cd2[jc * (CH / 2) + k], make_float2(-t.x, -t.y));
+            s2[k] = ffma2(bsn, cd2[jc * (CH / 2) + k], fmul2(bc, sd2[jc * (CH / 2) + k]));
+          }
+          tmem_wait_ld();
+#pragma unroll
+          for (int hp = 0; hp < UH; ++hp)
+#pragma unroll
+            for (int k = 0; k < CH / 2; ++k) {
+              acc2[hp] = ffma2(c2[k], make_float2(u[hp][2 * k], u[hp][2 * k + 1]), acc2[hp]);
+              acc2[hp] = ffma2(s2[k], make_float2(w[hp][2 * k], w[hp][2 * k + 1]), acc2[hp]);
+            }
         }
+        float v[2] = {0.f, 0.f};
+#pragma unroll
+        for (int hp = 0; hp < UH; ++hp) v[hp] = acc2[hp].x + acc2[hp].y;
         // (staging the whole unit in registers to release the slot earlier
         // needs 128 more registers than the 168 this kernel gets: it spilled)
-        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + 4 * unit] = clock64();
+        if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + SU * unit] = clock64();
         float* r = red + slot * UH * TILE_M;
         if (jh == 1) {
           r[delta] = v[0];
@@ -577,6 +642,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           named_bar_arrive(1 + slot, EPI_WARPS * 32);
         } else {
           named_bar_sync(1 + slot, EPI_WARPS * 32);
+          if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 8 + SU * unit] = clock64();
           const float v0 = v[0] + r[delta], v1 = UH == 2 ? v[1] + r[TILE_M + delta] : 0.f;
           fence_before();
           __syncwarp();
@@ -590,7 +656,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             lg[0] = v0 * sq;
             if (UH == 2) lg[p.ld_logits] = v1 * sq;
           }
-          if (p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == units - 1 &&
+          if (kTrace && p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == units - 1 &&
               it < TRACE_STRIDE - 8)
             p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 4 + it] = gtimer();
           if (p.ready != nullptr && h == units - 1) {
@@ -610,7 +676,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
   }
-  if (p.trace != nullptr && threadIdx.x == 0) {
+  if (kTrace && p.trace != nullptr && threadIdx.x == 0) {
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 1] = gtimer();
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 3] = i1 - i0;
   }
@@ -1900,8 +1966,7 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   PALU_REQUIRE(uh == 1 || uh == 2, "PALU_SCORE_UH must be 1 or 2");
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, uh == 2 ? TILE_M : 64);
   if (rc) return rc;
-  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + 512 +
-                    4 * 2 * TILE_M * 4;
+  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + SCORE_FIXED_BYTES;
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
   PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
@@ -2077,8 +2142,7 @@ int palu_rope_attend_tc(const void* hk, const void* hv, int B, int n_heads, int 
   rc = make_map_2d(&map_uw, uw, Rk_pad, (uint64_t)B * G * s * 128, KB, TILE_M);
   if (rc) return rc;
   const int kblocks = Rk_pad / KB;
-  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + 512 +
-                    4 * 2 * TILE_M * 4;
+  const int fixed = 1024 + kblocks * (s / 2) * HEAD_BYTES + SCORE_FIXED_BYTES;
   const int dyn_limit = SMEM_LIMIT - 2048;  // the value role has ~1 KB of static smem
   int stages = (dyn_limit - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;

@@ -17,6 +17,9 @@ sys.path.insert(0, ROOT)
 os.environ.setdefault("PALU_SCORE_TRACE", "1")
 
 
+SU = 8  # trace marks per unit (palu_tc.cu)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--context", type=int, default=65536)
@@ -61,9 +64,9 @@ def main():
     rows = []
     for cta in range(0, n, 2):  # leaders
         u = 0
-        while 4 + 4 * u + 3 < 512 and tr[cta, 4 + 4 * u] > 0:
-            ms, me, ew, er = tr[cta, 4 + 4 * u:8 + 4 * u]
-            rows.append((cta, u, ms, me, ew, er))
+        while 4 + SU * u + 7 < 508 and tr[cta, 4 + SU * u] > 0:
+            ms, me, ew, er, ex, eb, ia, ib = tr[cta, 4 + SU * u:12 + SU * u]
+            rows.append((cta, u, ms, me, ew, er, ex, eb, ia, ib))
             u += 1
     r = np.array(rows, dtype=np.int64)
     if not len(r):
@@ -84,12 +87,17 @@ def main():
     print(f"units {len(r)}: MMA issue span us p10/50/90 {pct(mma_issue)}")
     print(f"  commit->epilogue wake {pct(epi_lat)}; epilogue on slot {pct(epi_dur)}")
     print(f"  MMA idle between units {pct(np.array(gaps))}")
+    xch = (r[:, 6] - r[:, 5]) / ghz / 1e3        # math end -> cross-warp exchange done (jh 0 warp)
+    ready = (r[:, 4] - r[:, 7]) / ghz / 1e3      # epilogue ready for the unit -> accumulator complete
+    print(f"  exchange wait {pct(xch)}; epilogue waiting for the accumulator {pct(ready)}")
     cta = r[0, 0]
     c0 = tr[cta, 511]
     rr = r[r[:, 0] == cta][:12]
     us = lambda v: round((v - c0) / ghz / 1e3, 2)
     for x in rr:
-        print("  unit", x[1], "mma", us(x[2]), "->", us(x[3]), "epi", us(x[4]), "->", us(x[5]))
+        print("  unit", x[1], "mma", us(x[2]), "->", us(x[3]), "epi ready", us(x[7]), "wake", us(x[4]),
+              "math end", us(x[5]), "exchanged", us(x[6]),
+              *(("item start", us(x[8]), "staged", us(x[9])) if x[8] else ()))
 
 
 if __name__ == "__main__":
