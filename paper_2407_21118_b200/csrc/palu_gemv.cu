@@ -16,20 +16,32 @@
 // shared-memory x traffic; the cross-warp sum is a fixed-order reduction
 // (deterministic, no atomics).
 #include "palu_sm100.cuh"
+#include "palu_tmap.cuh"
 
 namespace palu {
 namespace tc {
 
-constexpr int GS_WARPS = 8;
+// ring geometry (overridable at build time for A/B builds)
+#ifndef PALU_GS_WARPS
+#define PALU_GS_WARPS 8
+#endif
+#ifndef PALU_GS_CHUNK
+#define PALU_GS_CHUNK 32768
+#endif
+#ifndef PALU_GS_SLOTS
+#define PALU_GS_SLOTS 5
+#endif
+constexpr int GS_WARPS = PALU_GS_WARPS;
 constexpr int GS_THREADS = (GS_WARPS + 1) * 32;
-constexpr int GS_CHUNK = 32768;
-constexpr int GS_SLOTS = 5;
+constexpr int GS_CHUNK = PALU_GS_CHUNK;
+constexpr int GS_SLOTS = PALU_GS_SLOTS;
 
 // KR8: 16-byte weight loads per lane per row (= K / 2048); NB: batch rows
 template <int KR8, int NB>
 __global__ void __launch_bounds__(GS_THREADS, 1)
-gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __restrict__ x, int ldx,
-                   float* __restrict__ y, int ldy, int accumulate, int rpc) {
+gemv_stream_kernel(const __grid_constant__ CUtensorMap map_w, const bf16* __restrict__ W, int N, int K,
+                   const float* __restrict__ x, int ldx,
+                   float* __restrict__ y, int ldy, int accumulate, int rpc, int diag) {
   pdl_launch();
   extern __shared__ __align__(128) uint8_t gs_smem[];
   uint8_t* ring = gs_smem;                                            // GS_SLOTS x GS_CHUNK
@@ -42,6 +54,7 @@ gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __rest
   const int nchunks = (r1 - r0 + rpc - 1) / rpc;
   const size_t row_bytes = (size_t)K * 2;
   if (threadIdx.x == 0) {
+    prefetch_map(&map_w);
     for (int s = 0; s < GS_SLOTS; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], GS_WARPS);
@@ -58,8 +71,10 @@ gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __rest
         const int nr = min(rpc, r1 - row);
         mbar_wait(&empty[rg.slot], rg.phase ^ 1);
         mbar_expect_tx(&full[rg.slot], (uint32_t)(nr * row_bytes));
-        bulk_load(ring + rg.slot * GS_CHUNK, W + (size_t)row * K, (uint32_t)(nr * row_bytes),
-                  &full[rg.slot]);
+        // one 2-D tensor box per weight row (W viewed as 256-byte rows)
+        for (int r = 0; r < nr; ++r)
+          tma_load_2d(&map_w, &full[rg.slot], ring + rg.slot * GS_CHUNK + r * row_bytes, 0,
+                      (int)((size_t)(row + r) * (row_bytes / 256)));
       }
     }
     return;  // the producer takes no part in the reductions below
@@ -78,6 +93,7 @@ gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __rest
       xr[b][i][4] = c.x; xr[b][i][5] = c.y; xr[b][i][6] = c.z; xr[b][i][7] = c.w;
     }
   const uint32_t lane_off = (uint32_t)(warp * kw + 8 * lane) * 2;
+  constexpr int MAXR = GS_CHUNK / (2048 * 2 * KR8) > 0 ? GS_CHUNK / (2048 * 2 * KR8) : 1;  // = rpc
   Ring rg;
   for (int c = 0; c < nchunks; ++c, rg.next(GS_SLOTS)) {
     const int row = r0 + c * rpc;
@@ -85,28 +101,42 @@ gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __rest
     mbar_wait(&full[rg.slot], rg.phase);
     const uint32_t base = smem_u32(ring + rg.slot * GS_CHUNK) + lane_off;
     float* rb = red + (size_t)(c & 1) * GS_WARPS * rpc * NB;
-    for (int r = 0; r < nr; ++r) {
-      float acc[NB];
+    // all rows of the chunk at once: independent FMA and shuffle-reduction
+    // chains per row (a row at a time left each warp waiting on one 5-step
+    // shuffle chain after another)
+    float acc[MAXR][NB];
 #pragma unroll
-      for (int b = 0; b < NB; ++b) acc[b] = 0.f;
-      uint4 wv[KR8];
+    for (int r = 0; r < MAXR; ++r) {
 #pragma unroll
-      for (int i = 0; i < KR8; ++i) wv[i] = lds128(base + (uint32_t)(r * row_bytes) + 512u * i);
+      for (int b = 0; b < NB; ++b) acc[r][b] = 0.f;
+      if (r < nr && !(diag & 1)) {  // diag 1 (diagnostic builds): stream without the math
+        uint4 wv[KR8];
 #pragma unroll
-      for (int i = 0; i < KR8; ++i) {
-        float wf[8];
-        Vec16<bf16>::unpack(wv[i], wf);
+        for (int i = 0; i < KR8; ++i) wv[i] = lds128(base + (uint32_t)(r * row_bytes) + 512u * i);
 #pragma unroll
-        for (int b = 0; b < NB; ++b)
+        for (int i = 0; i < KR8; ++i) {
+          float wf[8];
+          Vec16<bf16>::unpack(wv[i], wf);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) acc[b] = fmaf(wf[e], xr[b][i][e], acc[b]);
-      }
+          for (int b = 0; b < NB; ++b)
 #pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const float v = warp_reduce(acc[b], [](float a, float d) { return a + d; });
-        if (lane == 0) rb[(warp * rpc + r) * NB + b] = v;
+            for (int e = 0; e < 8; ++e) acc[r][b] = fmaf(wf[e], xr[b][i][e], acc[r][b]);
+        }
       }
     }
+#pragma unroll
+    for (int r = 0; r < MAXR; ++r)
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[r][b] += __shfl_xor_sync(0xffffffffu, acc[r][b], o);
+      }
+    if (lane == 0)
+#pragma unroll
+      for (int r = 0; r < MAXR; ++r)
+        if (r < nr)
+#pragma unroll
+          for (int b = 0; b < NB; ++b) rb[(warp * rpc + r) * NB + b] = acc[r][b];
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[rg.slot]);  // all lanes' smem reads of the slot are done
     named_bar_sync(1, GS_WARPS * 32);
@@ -119,6 +149,14 @@ gemv_stream_kernel(const bf16* __restrict__ W, int N, int K, const float* __rest
       *dst = accumulate ? *dst + v : v;
     }
   }
+}
+
+static int gemv_diag() {
+#ifdef PALU_DIAG
+  return getenv("PALU_GEMV_DIAG") ? atoi(getenv("PALU_GEMV_DIAG")) : 0;
+#else
+  return 0;
+#endif
 }
 
 template <int KR8, int NB>
@@ -136,8 +174,14 @@ static int launch_stream(const bf16* W, int N, int K, const float* x, int ldx, f
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = N < sms ? N : sms;
-  PALU_CK(launch_k(gemv_stream_kernel<KR8, NB>, dim3(grid), dim3(GS_THREADS), smem, st, W, N, K, x,
-                   ldx, y, ldy, acc, rpc));
+  CUtensorMap map_w;
+  const CUresult mr = make_map_stream(&map_w, W, (uint64_t)N * K * 2, (uint32_t)(K * 2));
+  if (mr != CUDA_SUCCESS) {
+    set_error("gemv: cuTensorMapEncodeTiled failed (%d)", (int)mr);
+    return PALU_ECUDA;
+  }
+  PALU_CK(launch_k(gemv_stream_kernel<KR8, NB>, dim3(grid), dim3(GS_THREADS), smem, st, map_w, W, N, K, x,
+                   ldx, y, ldy, acc, rpc, gemv_diag()));
   PALU_LAUNCHED();
   return PALU_OK;
 }

@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include "palu_sm100.cuh"
+#include "palu_tmap.cuh"
 
 namespace palu {
 namespace tc {
@@ -746,6 +747,7 @@ constexpr uint32_t IDESC_LS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(1
 constexpr int V_TMEM_COLS = 128;
 constexpr int V_PF = 0;     // L2 prefetch distance of the value stream (128-token blocks)
 constexpr int V_SUB = 512;  // tokens per P sub-block (double-buffered)
+constexpr int V_HEAD_START = 2;  // H_v stages issued before the first logits have arrived
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   uint32_t v;
@@ -1021,6 +1023,9 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   uint64_t* dfull = pfull + 2;    // [2] sub-block accumulator complete (P consumed)
   uint64_t* dempty = dfull + 2;   // [2] sub-block accumulator read back
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  // group A holds the first sub-block's logits (the bf16 producer waits for
+  // this after its first V_HEAD_START stages)
+  uint64_t* lgready = reinterpret_cast<uint64_t*>(tslot + 2);
   // packed V, standalone kernel: TMA ring of code tiles (+ 128 zero points each)
   const int nslots = vp.raw_slots;
   uint64_t* rfull = reinterpret_cast<uint64_t*>(tslot + 4);  // [nslots]
@@ -1040,6 +1045,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       mbar_init(&dfull[a], 1);
       mbar_init(&dempty[a], 1);
     }
+    mbar_init(lgready, 1);
     for (int a = 0; a < nslots; ++a) {
       mbar_init(&rfull[a], 1);
       mbar_init(&rempty[a], (int)(blockDim.x >> 5) - 10);
@@ -1172,6 +1178,11 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
               tma_prefetch_l2(&map_v, j * 128, rowp);
               tma_prefetch_l2(&map_v, j * 128 + 64, rowp);
             }
+            // start-up: every SM's first ring fill (~28 MB chip-wide) queues
+            // ahead of group A's logits reads (written by the score kernel,
+            // no longer in L2), which held the first P back ~8 us; issue
+            // V_HEAD_START stages, then let the logits through first
+            if (vp.no_wait && ctr == V_HEAD_START) mbar_wait(lgready, 0);
             mbar_wait(&empty[st], rg.phase ^ 1);
             if (vtr != nullptr && ctr == 0) vtr[496] = gtimer();  // first TMA issue
             mbar_expect_tx(&full[st], V_STAGE);
@@ -1317,6 +1328,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
         // has been read back
         if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
         named_bar_sync(3, 128);
+        if (sb == 0 && ta == 0) mbar_arrive(lgready);  // every group-A thread holds its logits
         trace(2);
 #pragma unroll
         for (int h = 0; h < V_HP; ++h)
@@ -1849,25 +1861,6 @@ __global__ void rope_table_kernel(const double* __restrict__ theta, int half, in
   }
 }
 
-// ---- host: tensor maps through the driver entry point (no -lcuda needed) ----
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-static EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  if (!fn) {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  }
-  return fn;
-}
-
 // packed key codes: uint8 rows, one box = the whole row x 128 rows (L2 prefetch only)
 static int make_map_u8(CUtensorMap* m, const void* base, uint64_t row_bytes, uint64_t rows) {
   EncodeTiledFn fn = encode_fn();
@@ -2303,7 +2296,7 @@ static int launch_value_q(int bits, const void* hv, const float* scales, const f
   const int OB = bits == 16 ? VQ_BSTAGE : NJ * VQ_STAGE;
   const int RS = RB;  // raw slot: the block's codes
   const int pbuf = VQ_NB * (bits == 16 ? 4096 : 2048);
-  const int misc = 1024 + 2 * pbuf + (2 * (V_HP + 1) + 2) * 4 + 2 * VQ_A * V_HP * (4 + 4) + 6 * 8 + 16;
+  const int misc = 1024 + 2 * pbuf + (2 * (V_HP + 1) + 2) * 4 + 2 * VQ_A * V_HP * (4 + 4) + 6 * 8 + 16 + 8;
   if (bits == 16) {
     p.raw_slots = 0;
     p.stages = (dyn_limit - misc) / (OB + 16);

@@ -234,6 +234,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
   uint64_t* dfull = pfull + 2;             // [2] sub-block accumulators complete
   uint64_t* dempty = dfull + 2;            // [2] sub-block accumulators read back
   uint32_t* tslot = reinterpret_cast<uint32_t*>(dempty + 2);
+  uint64_t* lgready = reinterpret_cast<uint64_t*>(tslot + 2);  // group A holds its first logits
   __shared__ float red_m[2][VQ_A][V_HP + 1];  // per-warp max logit per head + max scale
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
@@ -257,6 +258,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       mbar_init(&dfull[a], 1);
       mbar_init(&dempty[a], 1);
     }
+    mbar_init(lgready, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // digit rows 8..15 of every block stay zero (N = 16 > 4 heads x 2 digits)
@@ -310,14 +312,29 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         bulk_prefetch_l2(p.codes + ((size_t)pbg * p.T_cap + pc) * p.row_bytes, RB);
         pc += TILE_M;
       };
-      for (int k = 0; k < VQ_PF; ++k) prefetch_next();
+      // start-up: every SM's first loads (~30 MB chip-wide with the L2
+      // prefetches) queue ahead of group A's logits reads (the score kernel's
+      // output, no longer in L2), holding the first digits back by several
+      // us; after V_HEAD_START blocks the producer lets the logits through
+      int nblk_issued = 0;
+      bool released = false;
+      auto gate = [&]() {
+        if (released) {
+          prefetch_next();
+        } else if (nblk_issued == V_HEAD_START) {
+          mbar_wait(lgready, 0);
+          released = true;
+          for (int k = 0; k < VQ_PF; ++k) prefetch_next();
+        }
+        ++nblk_issued;
+      };
       if constexpr (BITS == 16) prefetch_map(&map_c);
       while (BITS == 16 && it.next(bg, s0u, s1u)) {
         // raw bf16: per block and 128-column tile two {64 col, 128 token} SW128
         // boxes straight into the MN-major operand stage
         const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
         for (int t0 = c0; t0 < c1; t0 += TILE_M) {
-          prefetch_next();
+          gate();
           if (!waited && t0 + TILE_M >= T_rows) {
             pdl_wait();
             waited = true;
@@ -335,7 +352,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       while (BITS != 16 && it.next(bg, s0u, s1u)) {
         const int c0 = s0u * SUPER, c1 = min(T_rows, s1u * SUPER);
         for (int t0 = c0; t0 < c1; t0 += TILE_M) {
-          prefetch_next();
+          gate();
           // the newest token (row T_rows - 1) comes from this step's append
           if (!waited && t0 + TILE_M >= T_rows) {
             pdl_wait();
@@ -541,6 +558,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
         }
         if (ta == 0) mark(300 + min(sb, 15));
         named_bar_sync(3, NT);
+        if (sb == 0 && ta == 0) mbar_arrive(lgready);  // every group-A thread holds its logits
         if (ta == 0) mark(316 + min(sb, 15));
 #pragma unroll
         for (int h = 0; h <= V_HP; ++h) {
