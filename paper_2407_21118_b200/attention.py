@@ -688,6 +688,10 @@ class _Session:
 
         _lib.call = timed
         try:
+            # keep the device busy while the host enqueues the step, so each
+            # event pair brackets the kernel alone rather than the host's
+            # launch latency (which dominated the short kernels' numbers)
+            torch.cuda._sleep(20_000_000)
             self.launch_step()
         finally:
             _lib.call = orig
