@@ -536,8 +536,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float4 v = off[i];
-        cd2[i] = make_float2(v.x, v.z);
-        sd2[i] = make_float2(v.y, v.w);
+        cd2[i] = make_float2(v.x, v.y);
+        sd2[i] = make_float2(v.z, v.w);
       }
     }
     const uint32_t lane_base = tmem_base + ((uint32_t)(q * 32) << 16);
@@ -577,7 +577,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       // quantised keys: the converter wrote c - z, so logit = s_t x (epilogue sum)
       float sq = 1.f;
       if (p.bits != 16 && tile * TILE_M + delta < T_rows)
-        sq = *reinterpret_cast<const float*>(eb + 512 + (it & 1) * 128 + lane * 4);
+        sq = lds32f(smem_u32(eb) + 512u + (uint32_t)(it & 1) * 128u + (uint32_t)lane * 4u);
       if (i + 1 < i1) {  // the other buffer was consumed an item ago
         stage_item((it + 1) & 1, 2 * nx.st + (int)rank, nx.bg);
         nx.next(n_super, p.G);
@@ -613,7 +613,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 #pragma unroll
           for (int k = 0; k < CH / 2; ++k) {
             const float4 bv = lds128f(base_addr + (uint32_t)(jc * (CH / 2) + k) * 16u);
-            const float2 bc = make_float2(bv.x, bv.z), bsn = make_float2(bv.y, bv.w);
+            const float2 bc = make_float2(bv.x, bv.y), bsn = make_float2(bv.z, bv.w);
             const float2 t = fmul2(bsn, sd2[jc * (CH / 2) + k]);
             c2[k] = ffma2(bc, cd2[jc * (CH / 2) + k], make_float2(-t.x, -t.y));
             s2[k] = ffma2(bsn, cd2[jc * (CH / 2) + k], fmul2(bc, sd2[jc * (CH / 2) + k]));
@@ -644,7 +644,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         } else {
           named_bar_sync(1 + slot, EPI_WARPS * 32);
           if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 8 + SU * unit] = clock64();
-          const float v0 = v[0] + r[delta], v1 = UH == 2 ? v[1] + r[TILE_M + delta] : 0.f;
+          const uint32_t ra = smem_u32(r + delta);
+          const float v0 = v[0] + lds32f(ra), v1 = UH == 2 ? v[1] + lds32f(ra + TILE_M * 4) : 0.f;
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty[slot]);
@@ -1849,15 +1850,19 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
 // ---------------------------------------------------------------------------
 // tile bases: cos/sin(t0 * th_j), t0 = 128 * row (fp64 angle reduction);
 // offsets: cos/sin(delta * th_j), delta in [0, 128).
+// Row layout per frequency pair (2p, 2p + 1): {cos 2p, cos 2p+1, sin 2p, sin 2p+1}
+// -- the float2 halves the epilogue's FFMA2s take without register moves.
 __global__ void rope_table_kernel(const double* __restrict__ theta, int half, int n_tiles,
-                                  float2* __restrict__ tab) {
+                                  float* __restrict__ tab) {
   const int total = (n_tiles + 128) * half;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int row = i / half, j = i - row * half;
     const double pos = row < n_tiles ? 128.0 * row : (double)(row - n_tiles);
     double sn, cs;
     sincos_big(pos * theta[j], &sn, &cs);
-    tab[i] = make_float2((float)cs, (float)sn);
+    float* e = tab + (size_t)row * 2 * half + 4 * (j >> 1) + (j & 1);
+    e[0] = (float)cs;
+    e[2] = (float)sn;
   }
 }
 
@@ -1914,8 +1919,7 @@ size_t palu_rope_table_floats(int half, int T_cap) {
 int palu_rope_table(const double* theta, int half, int T_cap, float* rope_tab, void* stream) {
   PALU_REQUIRE(half > 0 && T_cap > 0, "palu_rope_table: bad sizes");
   const int n_tiles = (T_cap + 127) / 128 + 1;
-  tc::rope_table_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(theta, half, n_tiles,
-                                                               reinterpret_cast<float2*>(rope_tab));
+  tc::rope_table_kernel<<<256, 256, 0, (cudaStream_t)stream>>>(theta, half, n_tiles, rope_tab);
   PALU_LAUNCHED();
   return PALU_OK;
 }
