@@ -619,6 +619,13 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             s2[k] = ffma2(bsn, cd2[jc * (CH / 2) + k], fmul2(bc, sd2[jc * (CH / 2) + k]));
           }
           tmem_wait_ld();
+          if (jc == 32 / CH - 1) {
+            // every accumulator column this warp reads is in registers: hand
+            // the slot back before the last FMAs and the cross-warp exchange
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_leader(&tempty[slot]);
+          }
 #pragma unroll
           for (int hp = 0; hp < UH; ++hp)
 #pragma unroll
@@ -627,28 +634,30 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
               acc2[hp] = ffma2(s2[k], make_float2(w[hp][2 * k], w[hp][2 * k + 1]), acc2[hp]);
             }
         }
+        if (mode & 1) {  // diagnostics: no math, release the slot at once
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_leader(&tempty[slot]);
+        }
         float v[2] = {0.f, 0.f};
 #pragma unroll
         for (int hp = 0; hp < UH; ++hp) v[hp] = acc2[hp].x + acc2[hp].y;
-        // (staging the whole unit in registers to release the slot earlier
-        // needs 128 more registers than the 168 this kernel gets: it spilled)
         if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + SU * unit] = clock64();
-        float* r = red + slot * UH * TILE_M;
+        // exchange buffer and named barrier rotate over 4 units: a warp hands
+        // the slot back before this exchange, so unit u + 2 may already be
+        // in flight, and reuse at u + 4 waits (through the MMA) for every
+        // warp's release of u + 2, issued after its reads of u
+        const int xb = unit & 3;
+        float* r = red + xb * UH * TILE_M;
         if (jh == 1) {
           r[delta] = v[0];
           if (UH == 2) r[TILE_M + delta] = v[1];
-          fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_leader(&tempty[slot]);
-          named_bar_arrive(1 + slot, EPI_WARPS * 32);
+          named_bar_arrive(1 + xb, EPI_WARPS * 32);
         } else {
-          named_bar_sync(1 + slot, EPI_WARPS * 32);
+          named_bar_sync(1 + xb, EPI_WARPS * 32);
           if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 8 + SU * unit] = clock64();
           const uint32_t ra = smem_u32(r + delta);
           const float v0 = v[0] + lds32f(ra), v1 = UH == 2 ? v[1] + lds32f(ra + TILE_M * 4) : 0.f;
-          fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           const int t = tile * TILE_M + delta;
           if (t < T_rows) {
             // UH 2: D columns 0..127 = head 2h (leader's UW rows), 128..255 =
