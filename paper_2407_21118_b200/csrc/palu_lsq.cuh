@@ -1,0 +1,314 @@
+// Rope-off latent score for packed keys on the int8 tensor pipe (sm_100a
+// tcgen05.mma.kind::i8).  Included by palu_tc.cu after palu_vq.cuh
+// (namespace palu::tc; uses umma_i8 and vq_column).
+//
+// Restates attention.py:380-388 (logits = H_k q_lat / sqrt(d_h), with
+// wq_fused) for quantised key latents, dequantised as quant.py:106-107
+// x = (c - z) s, without materialising x:
+//
+//   logit_t,h = s_t * sum_k (c_tk - z_t) q_hk = s_t * qs_h * (sum_k c_tk w_hk - z_t W_h)
+//
+// q_h (scaled by 1/sqrt(d_h)) is split per head into two signed 8-bit digits,
+// w = 254 hi + lo = round(q / qs_h), qs_h = max_k |q_hk| / 32258 (|q - w qs|
+// <= qs / 2), and W_h = sum_k w_hk.  The tensor pipe accumulates EXACT s32
+// sums D = sum_k c_tk {hi, lo}_hk over the group rank (A = the codes as u8,
+// K-major SW128, one row per token; B = the digits, K-major, N = 16: 4 heads
+// x {hi, lo} + 8 zero rows); the epilogue forms 254 D_hi + D_lo - z_t W_h in
+// int64 (zero points are integers, quant.py:96) and scales once.  Only the
+// digit rounding of q enters the result.
+//
+// Warps: 0 producer (one 1-D bulk copy per 128-token tile of codes, L2
+// prefetch ahead), 1 MMA issuer + TMEM owner, 2-5 epilogue and digit builder
+// (TMEM lane quarter = warp & 3), 6-13 converters (packed -> u8 operand:
+// nibbles / crumbs to bytes in the vq_column order the digits follow).
+
+constexpr int LQ_CV0 = 6, LQ_CONV = 8;
+constexpr int LQ_THREADS = (LQ_CV0 + LQ_CONV) * 32;
+constexpr int LQ_PF = 6;  // L2 prefetch distance (tiles)
+// D s32, A u8 (K-major), B s8 (K-major), M 128, N 16
+constexpr uint32_t IDESC_LQ = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) |
+                              ((uint32_t)(TILE_M >> 4) << 24);
+
+struct LQParams {
+  int B, n_heads, s, G, R_pad, T_cap, ld_logits, ld_y, row_bytes, stages, raw_slots;
+  float scale;
+  const float* y;  // [B][ld_y] fp32, q_lat of head i at q_off[i]
+  const int* q_off;
+  const int* ranks;
+  const int* t_dev;
+  float* logits;
+  const uint8_t* codes;  // [B][G][T_cap][row_bytes] packed LE codes (quant.py:156-169)
+  const float* scales;
+  const float* zps;
+};
+
+template <int BITS>
+__global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQParams p) {
+  pdl_enter();  // T_rows, the newest token's codes / scale / zero point, and q come from predecessors
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  constexpr int OC = 8 / BITS;      // operand chunks (16 codes) per raw 16-byte chunk
+  constexpr int GC = 16 * OC;       // codes per raw chunk
+  const int kblocks = p.R_pad / 128;  // 128-byte K-blocks of u8 codes
+  const int OB = kblocks * 16384;     // operand stage: 128 tokens x R_pad bytes
+  const int DB = kblocks * 2048;      // digits: 16 rows x R_pad bytes
+  const int RB = TILE_M * p.row_bytes;
+  uint8_t* ring = smem;
+  uint8_t* dig = ring + (size_t)p.stages * OB;
+  uint8_t* raw = dig + 2 * DB;
+  float* qs_sh = reinterpret_cast<float*>(raw + (size_t)p.raw_slots * RB);  // [2][4]
+  int* w_sh = reinterpret_cast<int*>(qs_sh + 8);                           // [2][4]
+  float* red = reinterpret_cast<float*>(w_sh + 8);                          // [4 warps][4 heads]
+  int* redw = reinterpret_cast<int*>(red + 16);                             // [4][4]
+  uint64_t* full = reinterpret_cast<uint64_t*>(redw + 16);
+  uint64_t* empty = full + p.stages;
+  uint64_t* rfull = empty + p.stages;
+  uint64_t* rempty = rfull + p.raw_slots;
+  uint64_t* dfull = rempty + p.raw_slots;  // [2]
+  uint64_t* dempty = dfull + 2;            // [2]
+  uint64_t* qfull = dempty + 2;            // [2]
+  uint64_t* qempty = qfull + 2;            // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(qempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int T_rows = *p.t_dev + 1;
+  const int ntile = (T_rows + TILE_M - 1) / TILE_M;
+  const int total = p.B * p.G * ntile;
+  const int per = (total + (int)gridDim.x - 1) / (int)gridDim.x;
+  const int i0 = min(total, (int)blockIdx.x * per), i1 = min(total, i0 + per);
+  if (tid == 0) {
+    for (int st = 0; st < p.stages; ++st) {
+      mbar_init(&full[st], LQ_CONV);
+      mbar_init(&empty[st], 1);
+    }
+    for (int r = 0; r < p.raw_slots; ++r) {
+      mbar_init(&rfull[r], 1);
+      mbar_init(&rempty[r], LQ_CONV);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&dfull[a], 1);
+      mbar_init(&dempty[a], 4);
+      mbar_init(&qfull[a], 1);
+      mbar_init(&qempty[a], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // digit rows 8..15 stay zero (N = 16 > 4 heads x 2 digits)
+  for (int i = tid; i < 2 * kblocks * 64; i += LQ_THREADS)
+    reinterpret_cast<uint4*>(dig + (i >> 6) * 2048 + 1024)[i & 63] = make_uint4(0u, 0u, 0u, 0u);
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ---------------- producer: a tile of one (sequence, group) is one contiguous range ----------------
+    if (lane == 0) {
+      int pf = i0;
+      auto prefetch = [&](int upto) {
+        for (; pf < min(i1, upto); ++pf) {
+          const int bg = pf / ntile, tile = pf - bg * ntile;
+          bulk_prefetch_l2(p.codes + ((size_t)bg * p.T_cap + tile * TILE_M) * p.row_bytes, (uint32_t)RB);
+        }
+      };
+      prefetch(i0 + LQ_PF);
+      Ring rg;
+      for (int i = i0; i < i1; ++i, rg.next(p.raw_slots)) {
+        prefetch(i + 1 + LQ_PF);
+        const int bg = i / ntile, tile = i - bg * ntile;
+        mbar_wait(&rempty[rg.slot], rg.phase ^ 1);
+        mbar_expect_tx(&rfull[rg.slot], (uint32_t)RB);
+        bulk_load(raw + (size_t)rg.slot * RB, p.codes + ((size_t)bg * p.T_cap + tile * TILE_M) * p.row_bytes,
+                  (uint32_t)RB, &rfull[rg.slot]);
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer: D[slot] = codes (u8) x digits^T (s8) ----------------
+    if (lane == 0) {
+      int seg = -1, cur = -1;
+      Ring rs;
+      for (int i = i0; i < i1; ++i, rs.next(p.stages)) {
+        const int bg = i / ntile;
+        if (bg != cur) {
+          if (seg >= 0) umma_commit(&qempty[seg & 1]);
+          ++seg;
+          cur = bg;
+          mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
+        }
+        const int k = i - i0, slot = k & 1;
+        if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
+        mbar_wait(&full[rs.slot], rs.phase);
+        fence_after();
+        const uint32_t a0 = smem_u32(ring + (size_t)rs.slot * OB);
+        const uint32_t b0 = smem_u32(dig + (seg & 1) * DB);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          const uint64_t da = sdesc(a0 + kb * 16384), db = sdesc(b0 + kb * 2048);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)  // K = 32 codes = 32 bytes: +2 in the address field
+            umma_i8(tmem + slot * 16, da + 2 * kk, db + 2 * kk, IDESC_LQ, (kb | kk) != 0);
+        }
+        umma_commit(&empty[rs.slot]);
+        umma_commit(&dfull[slot]);
+      }
+      if (seg >= 0) umma_commit(&qempty[seg & 1]);
+    }
+  } else if (warp >= LQ_CV0) {
+    // ---------------- converters: packed tile -> u8 K-major SW128 operand ----------------
+    // item = (row, raw 16-byte chunk q); chunk q holds codes [q GC, (q + 1) GC)
+    // and becomes OC operand chunks: chunk e = codes e + OC j (j = 0..15),
+    // i.e. K positions [q GC + 16 e, + 16) in vq_column order
+    const int ct = tid - LQ_CV0 * 32;
+    const int cpr = p.row_bytes / 16;  // raw chunks per row
+    const int items = TILE_M * cpr;
+    Ring rr, rs;
+    for (int i = i0; i < i1; ++i, rr.next(p.raw_slots), rs.next(p.stages)) {
+      mbar_wait(&rfull[rr.slot], rr.phase);
+      mbar_wait(&empty[rs.slot], rs.phase ^ 1);
+      const uint32_t src = smem_u32(raw + (size_t)rr.slot * RB);
+      const uint32_t dst = smem_u32(ring + (size_t)rs.slot * OB);
+      for (int w0 = 0; w0 < items; w0 += LQ_CONV * 32 * 4) {
+        uint4 v[4];
+        int row[4], q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {  // loads first: the stores below are volatile asm
+          const int w = w0 + ct + LQ_CONV * 32 * u;
+          row[u] = w / cpr;
+          q[u] = w - row[u] * cpr;
+          v[u] = w < items ? lds128(src + (uint32_t)w * 16u) : make_uint4(0u, 0u, 0u, 0u);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (w0 + ct + LQ_CONV * 32 * u >= items) continue;
+          const uint32_t rbase = dst + (uint32_t)(row[u] >> 3) * 1024u + (uint32_t)(row[u] & 7) * 128u;
+#pragma unroll
+          for (int e = 0; e < OC; ++e) {
+            const int kpos = q[u] * GC + 16 * e;
+            const uint32_t a = rbase + (uint32_t)(kpos >> 7) * 16384u +
+                               (uint32_t)((((kpos >> 4) & 7) ^ (row[u] & 7)) << 4);
+            if constexpr (BITS == 8) {
+              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[u].x), "r"(v[u].y),
+                           "r"(v[u].z), "r"(v[u].w)
+                           : "memory");
+            } else {
+              constexpr uint32_t M = BITS == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                           "r"((v[u].x >> (BITS * e)) & M), "r"((v[u].y >> (BITS * e)) & M),
+                           "r"((v[u].z >> (BITS * e)) & M), "r"((v[u].w >> (BITS * e)) & M)
+                           : "memory");
+            }
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&full[rs.slot]);
+        mbar_arrive(&rempty[rr.slot]);
+      }
+    }
+  } else {
+    // ---------------- epilogue + digit builder (warps 2-5) ----------------
+    const int q4 = warp & 3, te = tid - 64;  // TMEM lane quarter; 0..127
+    int seg = -1, cur = -1;
+    for (int i = i0; i < i1; ++i) {
+      const int bg = i / ntile, tile = i - bg * ntile;
+      const int b = bg / p.G, g = bg - b * p.G;
+      const int t = tile * TILE_M + q4 * 32 + lane;
+      // the token's scale and zero point: in flight while the MMAs run
+      float st_ = 0.f, zt = 0.f;
+      if (t < T_rows) {
+        st_ = __ldg(p.scales + (size_t)bg * p.T_cap + t);
+        zt = __ldg(p.zps + (size_t)bg * p.T_cap + t);
+      }
+      if (bg != cur) {
+        ++seg;
+        cur = bg;
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&qempty[buf], ((seg >> 1) - 1) & 1);
+        // digits of every head of the group: w = round(q / qs), qs = max|q| / 32258
+        const int r = p.ranks[g];
+        float amax[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int m = te; m < p.R_pad; m += 128) {
+          const int k = vq_column<BITS>(m);
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            if (h < p.s && k < r)
+              amax[h] = fmaxf(amax[h], fabsf(p.y[(size_t)b * p.ld_y + p.q_off[g * p.s + h] + k] * p.scale));
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          amax[h] = warp_reduce(amax[h], [](float x, float y) { return fmaxf(x, y); });
+          if (lane == 0) red[q4 * 4 + h] = amax[h];
+        }
+        named_bar_sync(1, 128);
+        float qs[4];
+        int wsum[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          qs[h] = fmaxf(fmaxf(red[h], red[4 + h]), fmaxf(red[8 + h], red[12 + h])) * (1.f / 32258.f);
+        uint8_t* db = dig + buf * DB;
+        for (int m = te; m < p.R_pad; m += 128) {
+          const int k = vq_column<BITS>(m);
+          const uint32_t kbo = (uint32_t)(m >> 7) * 2048u + (uint32_t)(m & 15);
+          const int c = (m >> 4) & 7;
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            int w = 0;
+            if (h < p.s && k < r && qs[h] > 0.f)
+              w = __float2int_rn(p.y[(size_t)b * p.ld_y + p.q_off[g * p.s + h] + k] * p.scale / qs[h]);
+            const int hi = __float2int_rn((float)w * (1.f / 254.f));
+            const int lo = w - 254 * hi;
+            wsum[h] += w;
+            // rows h (hi) and h + 4 (lo) of the first 8-row group (K-major SW128:
+            // row pitch 128 B, 16-byte chunk index ^= row)
+            db[kbo + (uint32_t)h * 128u + (uint32_t)((c ^ h) << 4)] = (uint8_t)(int8_t)hi;
+            db[kbo + (uint32_t)(h + 4) * 128u + (uint32_t)((c ^ (h + 4)) << 4)] = (uint8_t)(int8_t)lo;
+          }
+        }
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          wsum[h] = warp_reduce(wsum[h], [](int x, int y) { return x + y; });
+          if (lane == 0) redw[q4 * 4 + h] = wsum[h];
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        named_bar_sync(1, 128);
+        if (te < 4) {
+          qs_sh[buf * 4 + te] = qs[te];
+          w_sh[buf * 4 + te] = redw[te] + redw[4 + te] + redw[8 + te] + redw[12 + te];
+        }
+        named_bar_sync(1, 128);
+        if (te == 0) mbar_arrive(&qfull[buf]);
+      }
+      const int k = i - i0, slot = k & 1, buf = seg & 1;
+      mbar_wait(&dfull[slot], (k >> 1) & 1);
+      fence_after();
+      float v[16];
+      tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + slot * 16, v);
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&dempty[slot]);
+      if (t < T_rows) {
+        const long long z = (long long)zt;  // integer-valued zero point (quant.py:96)
+#pragma unroll
+        for (int h = 0; h < 4; ++h)
+          if (h < p.s) {
+            const long long d = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + 4]) - z * w_sh[buf * 4 + h];
+            p.logits[((size_t)b * p.n_heads + g * p.s + h) * p.ld_logits + t] = st_ * qs_sh[buf * 4 + h] * (float)d;
+          }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+  }
+}

@@ -1912,6 +1912,7 @@ static int make_map_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t
 }
 
 #include "palu_vq.cuh"
+#include "palu_lsq.cuh"
 
 }  // namespace tc
 }  // namespace palu
@@ -2462,6 +2463,59 @@ int palu_value_tc(int bits, const void* hv, const float* scales, const float* zp
 
 
 // Rope-off score on tcgen05 (bf16 latents, s <= 16, R_pad % 64 == 0, <= 256).
+// Rope-off packed keys on the int8 tensor pipe (palu_lsq.cuh).
+static int launch_latent_score_q(int bits, const void* hk, const float* scales, const float* zps, int B,
+                                 int n_heads, int s, int G, int R_pad, int T_cap, const float* y, int ld_y,
+                                 const int* q_off, const int* ranks, float scale, const int* t_dev,
+                                 float* logits, int ld_logits, cudaStream_t st) {
+  using namespace palu::tc;
+  LQParams p = {};
+  p.B = B;
+  p.n_heads = n_heads;
+  p.s = s;
+  p.G = G;
+  p.R_pad = R_pad;
+  p.T_cap = T_cap;
+  p.ld_logits = ld_logits;
+  p.ld_y = ld_y;
+  p.row_bytes = R_pad * bits / 8;
+  p.scale = scale;
+  p.y = y;
+  p.q_off = q_off;
+  p.ranks = ranks;
+  p.t_dev = t_dev;
+  p.logits = logits;
+  p.codes = reinterpret_cast<const uint8_t*>(hk);
+  p.scales = scales;
+  p.zps = zps;
+  const int OB = R_pad / 128 * 16384, DB = R_pad / 128 * 2048, RB = TILE_M * p.row_bytes;
+  const int limit = SMEM_LIMIT - 2048;
+  const int misc = 1024 + 2 * DB + 256 + 16 * 8 + 64;  // align, digits, scalars, barriers, TMEM slot
+  p.stages = 3;
+  p.raw_slots = (limit - misc - p.stages * (OB + 16)) / (RB + 16);
+  if (p.raw_slots > 6) p.raw_slots = 6;
+  PALU_REQUIRE(p.raw_slots >= 2, "palu_latent_score_tc (int8 pipe): shared memory too small (%d)", p.raw_slots);
+  const size_t smem = (size_t)misc + (size_t)p.stages * (OB + 16) + (size_t)p.raw_slots * (RB + 16);
+  static bool attr = false;
+  if (!attr) {
+    PALU_CK(cudaFuncSetAttribute(latent_score_q_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+    PALU_CK(cudaFuncSetAttribute(latent_score_q_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+    PALU_CK(cudaFuncSetAttribute(latent_score_q_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, limit));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (bits == 2)
+    PALU_CK(launch_k(latent_score_q_kernel<2>, dim3(sms), dim3(LQ_THREADS), smem, st, p));
+  else if (bits == 4)
+    PALU_CK(launch_k(latent_score_q_kernel<4>, dim3(sms), dim3(LQ_THREADS), smem, st, p));
+  else
+    PALU_CK(launch_k(latent_score_q_kernel<8>, dim3(sms), dim3(LQ_THREADS), smem, st, p));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
 int palu_latent_score_tc(int bits, const void* hk, const float* scales, const float* zps, int B,
                          int n_heads, int s, int G, int R_pad, int T_cap, const float* y, int ld_y,
                          const int* q_off, const int* ranks, float scale, const int* t_dev,
@@ -2475,6 +2529,10 @@ int palu_latent_score_tc(int bits, const void* hk, const float* scales, const fl
     return PALU_EUNSUPPORTED;
   }
   PALU_REQUIRE(((uintptr_t)hk & 15) == 0, "palu_latent_score_tc: unaligned latents");
+  static const bool lq_off = getenv("PALU_LS_KERNEL") && strcmp(getenv("PALU_LS_KERNEL"), "bf16") == 0;
+  if ((bits == 2 || bits == 4 || bits == 8) && R_pad % 128 == 0 && T_cap % TILE_M == 0 && s <= 4 && !lq_off)
+    return launch_latent_score_q(bits, hk, scales, zps, B, n_heads, s, G, R_pad, T_cap, y, ld_y, q_off,
+                                 ranks, scale, t_dev, logits, ld_logits, (cudaStream_t)stream);
   CUtensorMap map_h = {};
   if (bits == 16) {
     int rc = make_map_2d(&map_h, hk, R_pad, (uint64_t)B * G * T_cap, KB, TILE_M);
