@@ -24,7 +24,14 @@
 
 constexpr int LQ_CV0 = 6, LQ_CONV = 8;
 constexpr int LQ_THREADS = (LQ_CV0 + LQ_CONV) * 32;
-constexpr int LQ_PF = 6;  // L2 prefetch distance (tiles)
+#ifndef PALU_LQ_PF
+#define PALU_LQ_PF 6
+#endif
+constexpr int LQ_PF = PALU_LQ_PF;  // L2 prefetch distance (tiles)
+#ifndef PALU_LQ_DS
+#define PALU_LQ_DS 4
+#endif
+constexpr int LQ_DS = PALU_LQ_DS;  // accumulator slots (16 TMEM columns each): MMA / epilogue hand-off depth
 // D s32, A u8 (K-major), B s8 (K-major), M 128, N 16
 constexpr uint32_t IDESC_LQ = (2u << 4) | (0u << 7) | (1u << 10) | ((uint32_t)(16 >> 3) << 17) |
                               ((uint32_t)(TILE_M >> 4) << 24);
@@ -40,11 +47,14 @@ struct LQParams {
   const uint8_t* codes;  // [B][G][T_cap][row_bytes] packed LE codes (quant.py:156-169)
   const float* scales;
   const float* zps;
+  unsigned long long* trace;  // diagnostic builds (PALU_TRACE + PALU_FUSED_TRACE): per-CTA clock64 marks
 };
 
 template <int BITS>
 __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQParams p) {
+  const unsigned long long t_entry = kTrace && p.trace ? gtimer() : 0ull;
   pdl_enter();  // T_rows, the newest token's codes / scale / zero point, and q come from predecessors
+  const unsigned long long t_dep = kTrace && p.trace ? gtimer() : 0ull;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -65,9 +75,9 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
   uint64_t* empty = full + p.stages;
   uint64_t* rfull = empty + p.stages;
   uint64_t* rempty = rfull + p.raw_slots;
-  uint64_t* dfull = rempty + p.raw_slots;  // [2]
-  uint64_t* dempty = dfull + 2;            // [2]
-  uint64_t* qfull = dempty + 2;            // [2]
+  uint64_t* dfull = rempty + p.raw_slots;  // [LQ_DS]
+  uint64_t* dempty = dfull + LQ_DS;        // [LQ_DS]
+  uint64_t* qfull = dempty + LQ_DS;        // [2]
   uint64_t* qempty = qfull + 2;            // [2]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(qempty + 2);
 
@@ -86,9 +96,11 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
       mbar_init(&rfull[r], 1);
       mbar_init(&rempty[r], LQ_CONV);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < LQ_DS; ++a) {
       mbar_init(&dfull[a], 1);
       mbar_init(&dempty[a], 4);
+    }
+    for (int a = 0; a < 2; ++a) {
       mbar_init(&qfull[a], 1);
       mbar_init(&qempty[a], 1);
     }
@@ -98,7 +110,8 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
   for (int i = tid; i < 2 * kblocks * 64; i += LQ_THREADS)
     reinterpret_cast<uint4*>(dig + (i >> 6) * 2048 + 1024)[i & 63] = make_uint4(0u, 0u, 0u, 0u);
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(smem_u32(tslot)));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                 "r"(LQ_DS * 16 < 32 ? 32 : LQ_DS * 16));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -106,6 +119,19 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
+  // trace slots: 2 entry clock; per tile k < 60: 8 + k producer issue, 68 + k
+  // converter start, 128 + k converter done, 188 + k MMA issue, 248 + k MMA
+  // done (epilogue wake), 308 + k epilogue done
+  unsigned long long* tr = kTrace && p.trace ? p.trace + (size_t)blockIdx.x * TRACE_STRIDE : nullptr;
+  auto mark = [&](int base, int k) {
+    if (tr != nullptr && k < 60) tr[base + k] = (unsigned long long)clock64();
+  };
+  if (tr != nullptr && tid == 0) {
+    tr[0] = gtimer();
+    tr[2] = (unsigned long long)clock64();
+    tr[4] = t_entry;
+    tr[5] = t_dep;
+  }
 
   if (warp == 0) {
     // ---------------- producer: a tile of one (sequence, group) is one contiguous range ----------------
@@ -123,6 +149,7 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         prefetch(i + 1 + LQ_PF);
         const int bg = i / ntile, tile = i - bg * ntile;
         mbar_wait(&rempty[rg.slot], rg.phase ^ 1);
+        mark(8, i - i0);
         mbar_expect_tx(&rfull[rg.slot], (uint32_t)RB);
         bulk_load(raw + (size_t)rg.slot * RB, p.codes + ((size_t)bg * p.T_cap + tile * TILE_M) * p.row_bytes,
                   (uint32_t)RB, &rfull[rg.slot]);
@@ -130,23 +157,27 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
     }
   } else if (warp == 1) {
     // ---------------- MMA issuer: D[slot] = codes (u8) x digits^T (s8) ----------------
-    if (lane == 0) {
-      int seg = -1, cur = -1;
-      Ring rs;
-      for (int i = i0; i < i1; ++i, rs.next(p.stages)) {
-        const int bg = i / ntile;
-        if (bg != cur) {
-          if (seg >= 0) umma_commit(&qempty[seg & 1]);
-          ++seg;
-          cur = bg;
-          mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
-        }
-        const int k = i - i0, slot = k & 1;
-        if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
-        mbar_wait(&full[rs.slot], rs.phase);
-        fence_after();
-        const uint32_t a0 = smem_u32(ring + (size_t)rs.slot * OB);
-        const uint32_t b0 = smem_u32(dig + (seg & 1) * DB);
+    // the whole warp runs the loop (descriptors stay warp-uniform); one
+    // elected lane issues the tcgen05 instructions
+    int seg = -1, cur = -1;
+    Ring rs;
+    for (int i = i0; i < i1; ++i, rs.next(p.stages)) {
+      const int bg = i / ntile;
+      if (bg != cur) {
+        if (seg >= 0 && elect_one()) umma_commit(&qempty[seg & 1]);
+        __syncwarp();
+        ++seg;
+        cur = bg;
+        mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
+      }
+      const int k = i - i0, slot = k % LQ_DS;
+      if (k >= LQ_DS) mbar_wait(&dempty[slot], ((k / LQ_DS) - 1) & 1);
+      mbar_wait(&full[rs.slot], rs.phase);
+      fence_after();
+      if (lane == 0) mark(188, k);
+      const uint32_t a0 = smem_u32(ring + (size_t)rs.slot * OB);
+      const uint32_t b0 = smem_u32(dig + (seg & 1) * DB);
+      if (elect_one()) {
         for (int kb = 0; kb < kblocks; ++kb) {
           const uint64_t da = sdesc(a0 + kb * 16384), db = sdesc(b0 + kb * 2048);
 #pragma unroll
@@ -156,52 +187,67 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         umma_commit(&empty[rs.slot]);
         umma_commit(&dfull[slot]);
       }
-      if (seg >= 0) umma_commit(&qempty[seg & 1]);
+      __syncwarp();
     }
+    if (seg >= 0 && elect_one()) umma_commit(&qempty[seg & 1]);
+    __syncwarp();
   } else if (warp >= LQ_CV0) {
     // ---------------- converters: packed tile -> u8 K-major SW128 operand ----------------
     // item = (row, raw 16-byte chunk q); chunk q holds codes [q GC, (q + 1) GC)
     // and becomes OC operand chunks: chunk e = codes e + OC j (j = 0..15),
     // i.e. K positions [q GC + 16 e, + 16) in vq_column order
     const int ct = tid - LQ_CV0 * 32;
-    const int cpr = p.row_bytes / 16;  // raw chunks per row
-    const int items = TILE_M * cpr;
+    const int cpr = p.row_bytes / 16;  // raw chunks per row (R_pad <= 256: <= 2 BITS)
+    const int items = TILE_M * cpr;    // <= 256 BITS: at most BITS items per thread
+    // item order: each 8-thread phase of a 16-byte store covers QP raw chunks
+    // of one K-block in each of RP rows, so its 8 swizzled chunks land in 8
+    // distinct bank groups (row-major order put two threads on each).  The
+    // geometry is the same for every tile: offsets are computed once.
+    constexpr int QP = 128 / GC, RP = 8 / QP, IT = BITS;
+    const int kbc = cpr / QP;
+    uint32_t src_off[IT], dst_off[IT];
+    int cbase[IT], rsw[IT];
+    bool live[IT];
+#pragma unroll
+    for (int u = 0; u < IT; ++u) {
+      const int w = ct + LQ_CONV * 32 * u;
+      const int ph = w >> 3, l8 = w & 7;
+      const int row = (ph / kbc) * RP + l8 / QP, q = (ph % kbc) * QP + l8 % QP;
+      live[u] = w < items;
+      src_off[u] = (uint32_t)(row * p.row_bytes + 16 * q);
+      // chunk e of the item sits at K position q GC + 16 e: K-block (q GC) / 128,
+      // 16-byte chunk ((q GC) / 16 + e) & 7, XOR-swizzled by the row
+      dst_off[u] = (uint32_t)((q * GC) >> 7) * 16384u + (uint32_t)(row >> 3) * 1024u + (uint32_t)(row & 7) * 128u;
+      cbase[u] = ((q * GC) >> 4) & 7;
+      rsw[u] = row & 7;
+    }
     Ring rr, rs;
     for (int i = i0; i < i1; ++i, rr.next(p.raw_slots), rs.next(p.stages)) {
       mbar_wait(&rfull[rr.slot], rr.phase);
       mbar_wait(&empty[rs.slot], rs.phase ^ 1);
+      if (ct == 0) mark(68, i - i0);
       const uint32_t src = smem_u32(raw + (size_t)rr.slot * RB);
       const uint32_t dst = smem_u32(ring + (size_t)rs.slot * OB);
-      for (int w0 = 0; w0 < items; w0 += LQ_CONV * 32 * 4) {
-        uint4 v[4];
-        int row[4], q[4];
+      uint4 v[IT];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {  // loads first: the stores below are volatile asm
-          const int w = w0 + ct + LQ_CONV * 32 * u;
-          row[u] = w / cpr;
-          q[u] = w - row[u] * cpr;
-          v[u] = w < items ? lds128(src + (uint32_t)w * 16u) : make_uint4(0u, 0u, 0u, 0u);
-        }
+      for (int u = 0; u < IT; ++u)  // loads first: the stores below are volatile asm
+        v[u] = live[u] ? lds128(src + src_off[u]) : make_uint4(0u, 0u, 0u, 0u);
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (w0 + ct + LQ_CONV * 32 * u >= items) continue;
-          const uint32_t rbase = dst + (uint32_t)(row[u] >> 3) * 1024u + (uint32_t)(row[u] & 7) * 128u;
+      for (int u = 0; u < IT; ++u) {
+        if (!live[u]) continue;
 #pragma unroll
-          for (int e = 0; e < OC; ++e) {
-            const int kpos = q[u] * GC + 16 * e;
-            const uint32_t a = rbase + (uint32_t)(kpos >> 7) * 16384u +
-                               (uint32_t)((((kpos >> 4) & 7) ^ (row[u] & 7)) << 4);
-            if constexpr (BITS == 8) {
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[u].x), "r"(v[u].y),
-                           "r"(v[u].z), "r"(v[u].w)
-                           : "memory");
-            } else {
-              constexpr uint32_t M = BITS == 4 ? 0x0F0F0F0Fu : 0x03030303u;
-              asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a),
-                           "r"((v[u].x >> (BITS * e)) & M), "r"((v[u].y >> (BITS * e)) & M),
-                           "r"((v[u].z >> (BITS * e)) & M), "r"((v[u].w >> (BITS * e)) & M)
-                           : "memory");
-            }
+        for (int e = 0; e < OC; ++e) {
+          const uint32_t a = dst + dst_off[u] + (uint32_t)((((cbase[u] + e) & 7) ^ rsw[u]) << 4);
+          if constexpr (BITS == 8) {
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v[u].x), "r"(v[u].y),
+                         "r"(v[u].z), "r"(v[u].w)
+                         : "memory");
+          } else {
+            constexpr uint32_t M = BITS == 4 ? 0x0F0F0F0Fu : 0x03030303u;
+            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a),
+                         "r"((v[u].x >> (BITS * e)) & M), "r"((v[u].y >> (BITS * e)) & M),
+                         "r"((v[u].z >> (BITS * e)) & M), "r"((v[u].w >> (BITS * e)) & M)
+                         : "memory");
           }
         }
       }
@@ -211,36 +257,55 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         mbar_arrive(&full[rs.slot]);
         mbar_arrive(&rempty[rr.slot]);
       }
+      if (ct == 0) mark(128, i - i0);
     }
   } else {
     // ---------------- epilogue + digit builder (warps 2-5) ----------------
     const int q4 = warp & 3, te = tid - 64;  // TMEM lane quarter; 0..127
     int seg = -1, cur = -1;
+    // the token's scale and zero point, loaded one tile ahead (a load issued at
+    // the tile's own start left its latency exposed once per tile)
+    auto load_sz = [&](int i, float& sv, float& zv) {
+      sv = 0.f;
+      zv = 0.f;
+      if (i < i1) {
+        const int bgn = i / ntile, t = (i - bgn * ntile) * TILE_M + q4 * 32 + lane;
+        if (t < T_rows) {
+          sv = __ldg(p.scales + (size_t)bgn * p.T_cap + t);
+          zv = __ldg(p.zps + (size_t)bgn * p.T_cap + t);
+        }
+      }
+    };
+    float sn, zn;
+    load_sz(i0, sn, zn);
     for (int i = i0; i < i1; ++i) {
       const int bg = i / ntile, tile = i - bg * ntile;
       const int b = bg / p.G, g = bg - b * p.G;
       const int t = tile * TILE_M + q4 * 32 + lane;
-      // the token's scale and zero point: in flight while the MMAs run
-      float st_ = 0.f, zt = 0.f;
-      if (t < T_rows) {
-        st_ = __ldg(p.scales + (size_t)bg * p.T_cap + t);
-        zt = __ldg(p.zps + (size_t)bg * p.T_cap + t);
-      }
+      const float st_ = sn, zt = zn;
+      load_sz(i + 1, sn, zn);
       if (bg != cur) {
         ++seg;
         cur = bg;
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&qempty[buf], ((seg >> 1) - 1) & 1);
-        // digits of every head of the group: w = round(q / qs), qs = max|q| / 32258
+        // digits of every head of the group: w = round(q / qs), qs = max|q| / 32258;
+        // each thread owns K positions te and te + 128 (R_pad <= 256): one
+        // round of global loads
         const int r = p.ranks[g];
-        float amax[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int m = te; m < p.R_pad; m += 128) {
+        float qv[2][4];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int m = te + 128 * j;
           const int k = vq_column<BITS>(m);
 #pragma unroll
           for (int h = 0; h < 4; ++h)
-            if (h < p.s && k < r)
-              amax[h] = fmaxf(amax[h], fabsf(p.y[(size_t)b * p.ld_y + p.q_off[g * p.s + h] + k] * p.scale));
+            qv[j][h] = (m < p.R_pad && h < p.s && k < r)
+                           ? p.y[(size_t)b * p.ld_y + p.q_off[g * p.s + h] + k] * p.scale : 0.f;
         }
+        float amax[4];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) amax[h] = fmaxf(fabsf(qv[0][h]), fabsf(qv[1][h]));
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
           amax[h] = warp_reduce(amax[h], [](float x, float y) { return fmaxf(x, y); });
@@ -253,15 +318,15 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         for (int h = 0; h < 4; ++h)
           qs[h] = fmaxf(fmaxf(red[h], red[4 + h]), fmaxf(red[8 + h], red[12 + h])) * (1.f / 32258.f);
         uint8_t* db = dig + buf * DB;
-        for (int m = te; m < p.R_pad; m += 128) {
-          const int k = vq_column<BITS>(m);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int m = te + 128 * j;
+          if (m >= p.R_pad) continue;
           const uint32_t kbo = (uint32_t)(m >> 7) * 2048u + (uint32_t)(m & 15);
           const int c = (m >> 4) & 7;
 #pragma unroll
           for (int h = 0; h < 4; ++h) {
-            int w = 0;
-            if (h < p.s && k < r && qs[h] > 0.f)
-              w = __float2int_rn(p.y[(size_t)b * p.ld_y + p.q_off[g * p.s + h] + k] * p.scale / qs[h]);
+            const int w = qs[h] > 0.f ? __float2int_rn(qv[j][h] / qs[h]) : 0;
             const int hi = __float2int_rn((float)w * (1.f / 254.f));
             const int lo = w - 254 * hi;
             wsum[h] += w;
@@ -285,9 +350,10 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         named_bar_sync(1, 128);
         if (te == 0) mbar_arrive(&qfull[buf]);
       }
-      const int k = i - i0, slot = k & 1, buf = seg & 1;
-      mbar_wait(&dfull[slot], (k >> 1) & 1);
+      const int k = i - i0, slot = k % LQ_DS, buf = seg & 1;
+      mbar_wait(&dfull[slot], (k / LQ_DS) & 1);
       fence_after();
+      if (te == 0) mark(248, k);
       float v[16];
       tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + slot * 16, v);
       tmem_wait_ld();
@@ -295,20 +361,34 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
       __syncwarp();
       if (lane == 0) mbar_arrive(&dempty[slot]);
       if (t < T_rows) {
-        const long long z = (long long)zt;  // integer-valued zero point (quant.py:96)
+        // integer-valued zero point (quant.py:96); int2 / int4 sums fit in 32 bits
+        // (|254 D_hi| <= 254 * 15 * 127 * 256, |z W| <= 15 * 256 * 32258), int8 needs 64
+        const int z = __float2int_rn(zt);
+        float* lrow = p.logits + ((size_t)b * p.n_heads + g * p.s) * p.ld_logits + t;
 #pragma unroll
         for (int h = 0; h < 4; ++h)
           if (h < p.s) {
-            const long long d = 254ll * __float_as_int(v[h]) + __float_as_int(v[h + 4]) - z * w_sh[buf * 4 + h];
-            p.logits[((size_t)b * p.n_heads + g * p.s + h) * p.ld_logits + t] = st_ * qs_sh[buf * 4 + h] * (float)d;
+            float d;
+            if constexpr (BITS == 8)
+              d = (float)(254ll * __float_as_int(v[h]) + __float_as_int(v[h + 4]) -
+                          (long long)z * w_sh[buf * 4 + h]);
+            else
+              d = (float)(254 * __float_as_int(v[h]) + __float_as_int(v[h + 4]) - z * w_sh[buf * 4 + h]);
+            lrow[(size_t)h * p.ld_logits] = st_ * qs_sh[buf * 4 + h] * d;
           }
       }
+      if (te == 0) mark(308, k);
     }
   }
   fence_before();
   __syncthreads();
+  if (tr != nullptr && tid == 0) {
+    tr[1] = gtimer();
+    tr[3] = (unsigned long long)(i1 - i0);
+  }
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"(LQ_DS * 16 < 32 ? 32 : LQ_DS * 16));
   }
 }

@@ -2488,12 +2488,24 @@ static int launch_latent_score_q(int bits, const void* hk, const float* scales, 
   p.codes = reinterpret_cast<const uint8_t*>(hk);
   p.scales = scales;
   p.zps = zps;
+  p.trace = nullptr;
+  if (kTrace && getenv("PALU_LSQ_TRACE")) {  // diagnostics (tools/lsq_trace.py)
+    int sms_ = 148;
+    cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, 0);
+    if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
+    PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, st));
+    p.trace = g_trace;
+    g_trace_ctas = sms_;
+  }
   const int OB = R_pad / 128 * 16384, DB = R_pad / 128 * 2048, RB = TILE_M * p.row_bytes;
   const int limit = SMEM_LIMIT - 2048;
   const int misc = 1024 + 2 * DB + 256 + 16 * 8 + 64;  // align, digits, scalars, barriers, TMEM slot
-  p.stages = 3;
+  // three operand stages (the converter runs ahead of the MMA's ~0.5 us
+  // commit turnaround), the raw ring takes the rest
+  p.stages = getenv("PALU_LQ_STAGES") ? atoi(getenv("PALU_LQ_STAGES")) : 3;
   p.raw_slots = (limit - misc - p.stages * (OB + 16)) / (RB + 16);
-  if (p.raw_slots > 6) p.raw_slots = 6;
+  const int rmax = getenv("PALU_LQ_RAW") ? atoi(getenv("PALU_LQ_RAW")) : 12;
+  if (p.raw_slots > rmax) p.raw_slots = rmax;
   PALU_REQUIRE(p.raw_slots >= 2, "palu_latent_score_tc (int8 pipe): shared memory too small (%d)", p.raw_slots);
   const size_t smem = (size_t)misc + (size_t)p.stages * (OB + 16) + (size_t)p.raw_slots * (RB + 16);
   static bool attr = false;
