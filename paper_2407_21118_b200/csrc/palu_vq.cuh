@@ -439,7 +439,9 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
     }
   } else if (warp == VQ_MMA) {
     // ---------------- MMA issuer ----------------
-    if (lane == 0) {
+    // the whole warp runs the loop (descriptors stay warp-uniform); one
+    // elected lane issues the tcgen05 instructions
+    {
       VQIter it(i0, i1, n_super);
       Ring rs;
       int sb = 0;
@@ -451,7 +453,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
           mbar_wait(&pfull[buf], (sb >> 1) & 1);
           if (sb >= 2) mbar_wait(&dempty[buf], ((sb >> 1) - 1) & 1);
           fence_after();
-          mark(152 + min(sb, 15));
+          if (lane == 0) mark(152 + min(sb, 15));
           const uint32_t pb = smem_u32(pbuf + buf * PBUF);
           const int b1 = min(nblk, b0 + VQ_NB);
           for (int blk = b0; BITS == 16 && blk < b1; ++blk)
@@ -460,31 +462,38 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
               fence_after();
               const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
               const uint32_t a0 = smem_u32(ring + rs.slot * OB);
-              if ((p.diag & 1) == 0)
+              if (elect_one()) {
+                if ((p.diag & 1) == 0)
 #pragma unroll
-                for (int kk = 0; kk < TILE_M / 16; ++kk)  // K = 16 tokens: 2 KB of A (2 slabs)
-                  umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, VQ_BSTAGE / 2, 1024),
-                               sdesc(pb + (blk - b0) * PBLK + (kk >> 2) * 2048 + (kk & 3) * 32), IDESC_QB,
-                               (blk != b0) || (kk != 0));
-              umma_commit(&empty[rs.slot]);
+                  for (int kk = 0; kk < TILE_M / 16; ++kk)  // K = 16 tokens: 2 KB of A (2 slabs)
+                    umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, VQ_BSTAGE / 2, 1024),
+                                 sdesc(pb + (blk - b0) * PBLK + (kk >> 2) * 2048 + (kk & 3) * 32), IDESC_QB,
+                                 (blk != b0) || (kk != 0));
+                umma_commit(&empty[rs.slot]);
+              }
+              __syncwarp();
             }
           for (int blk = b0; BITS != 16 && blk < b1; ++blk, rs.next(p.stages)) {
             mbar_wait(&full[rs.slot], rs.phase);
             fence_after();
             const uint64_t db = sdesc(pb + (blk - b0) * PBLK);
-            for (int j = 0; j < NJ; ++j) {
-              const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
-              const uint64_t da = sdesc_mn(smem_u32(ring + rs.slot * OB + j * VQ_STAGE), VQ_STAGE, 1024);
-              if ((p.diag & 1) == 0)
+            if (elect_one()) {
+              for (int j = 0; j < NJ; ++j) {
+                const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
+                const uint64_t da = sdesc_mn(smem_u32(ring + rs.slot * OB + j * VQ_STAGE), VQ_STAGE, 1024);
+                if ((p.diag & 1) == 0)
 #pragma unroll
-                for (int kk = 0; kk < TILE_M / 32; ++kk)  // K = 32 tokens: 4 KB of A, 32 B of B
-                  umma_i8(d, da + (uint64_t)(kk * 256), db + (uint64_t)(kk * 2), IDESC_Q,
-                          (blk != b0) || (kk != 0));
+                  for (int kk = 0; kk < TILE_M / 32; ++kk)  // K = 32 tokens: 4 KB of A, 32 B of B
+                    umma_i8(d, da + (uint64_t)(kk * 256), db + (uint64_t)(kk * 2), IDESC_Q,
+                            (blk != b0) || (kk != 0));
+              }
+              umma_commit(&empty[rs.slot]);
             }
-            umma_commit(&empty[rs.slot]);
+            __syncwarp();
           }
-          umma_commit(&dfull[buf]);
-          mark(168 + min(sb, 15));
+          if (elect_one()) umma_commit(&dfull[buf]);
+          __syncwarp();
+          if (lane == 0) mark(168 + min(sb, 15));
         }
       }
     }
