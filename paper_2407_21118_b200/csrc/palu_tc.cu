@@ -1206,8 +1206,9 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
   }
   if (warp == 9) {
     // ---------------- MMA issuer: per V_SUB-token sub-block sb (buffer sb & 1)
-    // D[buf][j] = V^T x P^T over the sub-block's 128-token blocks
-    if (lane == 0) {
+    // D[buf][j] = V^T x P^T over the sub-block's 128-token blocks; the whole
+    // warp runs the loop, one elected lane issues the tcgen05 instructions
+    {
       int ctr = 0, sb = 0;
       Ring rg;
       while (it.next(u)) {
@@ -1225,26 +1226,30 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
               const int st = rg.slot;
               mbar_wait(&full[st], rg.phase);
               fence_after();
-              if (vtr != nullptr && ctr == 0) vtr[497] = gtimer();  // first stage landed
-              if (vtr != nullptr && ctr == vs) vtr[498] = gtimer();  // ring wrapped
+              if (vtr != nullptr && lane == 0 && ctr == 0) vtr[497] = gtimer();  // first stage landed
+              if (vtr != nullptr && lane == 0 && ctr == vs) vtr[498] = gtimer();  // ring wrapped
               if (p.mode & 1) {  // diagnostics: release the stage without MMAs
-                mbar_arrive(&empty[st]);
+                if (lane == 0) mbar_arrive(&empty[st]);
                 continue;
               }
               const uint32_t a0 = smem_u32(ring + st * V_STAGE);
               const uint32_t d = tmem + (uint32_t)((buf * NJ + j) * 16);
+              if (elect_one()) {
 #pragma unroll
-              for (int kk = 0; kk < TILE_M / 16; ++kk)
-                umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, V_STAGE / 2, 1024),
-                             sdesc(pb + ((blk - b0) * 2 + kk / 4) * 1024 + (kk % 4) * 32), IDESC_V,
-                             (blk != b0) || (kk != 0));
-              umma_commit(&empty[st]);
+                for (int kk = 0; kk < TILE_M / 16; ++kk)
+                  umma_bf16_id(d, sdesc_mn(a0 + kk * 2048, V_STAGE / 2, 1024),
+                               sdesc(pb + ((blk - b0) * 2 + kk / 4) * 1024 + (kk % 4) * 32), IDESC_V,
+                               (blk != b0) || (kk != 0));
+                umma_commit(&empty[st]);
+              }
+              __syncwarp();
             }
           if (p.mode & 1) {
             if ((p.mode & 2) != 0) mbar_wait(&pfull[buf], (sb >> 1) & 1);
-            mbar_arrive(&dfull[buf]);
+            if (lane == 0) mbar_arrive(&dfull[buf]);
           } else {
-            umma_commit(&dfull[buf]);
+            if (elect_one()) umma_commit(&dfull[buf]);
+            __syncwarp();
           }
         }
       }
