@@ -1763,35 +1763,39 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      int seg = -1, cur = -1;
-      Ring rg;
-      for (int i = i0; i < i1; ++i) {
-        const int bg = i / ntile;
-        if (bg != cur) {
-          if (seg >= 0) umma_commit(&qempty[seg & 1]);
-          ++seg;
-          cur = bg;
-          mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
-          fence_after();
-        }
-        const int k = i - i0, slot = k & 1;
-        if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
+    // MMA issuer: the whole warp runs the loop, one elected lane issues
+    int seg = -1, cur = -1;
+    Ring rg;
+    for (int i = i0; i < i1; ++i) {
+      const int bg = i / ntile;
+      if (bg != cur) {
+        if (seg >= 0 && elect_one()) umma_commit(&qempty[seg & 1]);
+        __syncwarp();
+        ++seg;
+        cur = bg;
+        mbar_wait(&qfull[seg & 1], (seg >> 1) & 1);
         fence_after();
-        const uint32_t q0 = smem_u32(s_q + (seg & 1) * QB);
-        for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
-          const int st = rg.slot;
-          mbar_wait(&full[st], rg.phase);
-          fence_after();
-          const uint32_t a0 = smem_u32(s_h + st * H_STAGE_BYTES);
-          const uint64_t da = sdesc(a0), dq = sdesc(q0 + kb * 2048);  // +2 per K16 step
+      }
+      const int k = i - i0, slot = k & 1;
+      if (k >= 2) mbar_wait(&dempty[slot], ((k >> 1) - 1) & 1);
+      fence_after();
+      const uint32_t q0 = smem_u32(s_q + (seg & 1) * QB);
+      for (int kb = 0; kb < kblocks; ++kb, rg.next(p.stages)) {
+        const int st = rg.slot;
+        mbar_wait(&full[st], rg.phase);
+        fence_after();
+        const uint32_t a0 = smem_u32(s_h + st * H_STAGE_BYTES);
+        const uint64_t da = sdesc(a0), dq = sdesc(q0 + kb * 2048);  // +2 per K16 step
+        if (elect_one()) {
 #pragma unroll
           for (int kk = 0; kk < KB / 16; ++kk)
             umma_bf16_id(tmem + slot * 16, da + 2 * kk, dq + 2 * kk, IDESC_LS, (kb | kk) != 0);
           umma_commit(&empty[st]);
         }
-        umma_commit(&dfull[slot]);
+        __syncwarp();
       }
+      if (elect_one()) umma_commit(&dfull[slot]);
+      __syncwarp();
     }
   } else {
     // ---------------- epilogue / Q builders (warps 2..5) ----------------
