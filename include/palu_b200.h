@@ -130,6 +130,22 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
                       float scale, const int* t_dev, void* uw, int layout, void* stream);
 
 /*
+ * palu_latent_append_kv and palu_query_absorb of one layer in ONE launch
+ * (attention.py:343-347 + :248-255, and :428-431): both read only the GEMV
+ * output row and *t_dev, and the RoPE score needs both, so a single grid
+ * takes the append off the serial launch chain.  Arguments are those of the
+ * two calls (the absorb's R_pad is R_pad_k); results are identical.
+ */
+int palu_append_absorb(int dtype, int bits_k, int bits_v, const float* lat_k, const float* lat_v, int B,
+                       int ld_lat, int G_k, int G_v, const int* ranks_k, const int* lat_off_k,
+                       const int* ranks_v, const int* lat_off_v, void* rows_k, float* scales_k,
+                       float* zps_k, double* scales64_k, int64_t* zps64_k, void* rows_v, float* scales_v,
+                       float* zps_v, double* scales64_v, int64_t* zps64_v, int R_pad_k, int R_pad_v,
+                       int T_cap, const float* q, int ld_q, int n_heads, int head_dim, int s_k,
+                       const void* bk, int bk_rows, const double* theta, float scale, void* uw, int layout,
+                       const int* t_dev, void* stream);
+
+/*
  * RoPE score over the latent key cache (attention.py:433-444):
  *   logits[b][i][t'] = q_rot_i . RoPE_t'( H_k[g(i)][t'] @ B_g[:, head i] ) / sqrt(d_h)
  * for t' in [0, *t_dev], via the absorbed uw (layout 0).  bits 16 reads raw

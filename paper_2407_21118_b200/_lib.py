@@ -38,6 +38,9 @@ SIGNATURES = {
     "palu_quantize_rows": (i32, [p, i32, i32, i32, p, p, p, p]),
     "palu_pack_rows": (i32, [p, i32, i32, i32, p, p]),
     "palu_query_absorb": (i32, [i32, p, i32, i32, i32, i32, i32, p, i32, i32, p, f32, p, p, i32, p]),
+    "palu_append_absorb": (i32, [i32, i32, i32, p, p, i32, i32, i32, i32, p, p, p, p,
+                                 p, p, p, p, p, p, p, p, p, p, i32, i32, i32,
+                                 p, i32, i32, i32, i32, p, i32, p, f32, p, i32, p, p]),
     "palu_rope_score": (i32, [i32, i32, p, p, p, i32, i32, i32, i32, i32, i32, i32, p, p, p, p,
                               i32, p]),
     "palu_rope_score_tc_splits": (i32, [i32, i32]),

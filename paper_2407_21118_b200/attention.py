@@ -33,6 +33,8 @@ from .model import (AttentionConfig, LayerKV, LayerWeights, ModelWeights, as_arr
 
 FP_BITS = 16
 _APPEND_SPLIT = os.environ.get("PALU_APPEND_SPLIT") == "1"  # A/B diagnostics only
+# PALU_APPEND_ABSORB=0: separate append and absorb launches (A/B diagnostics only)
+_APPEND_ABSORB = os.environ.get("PALU_APPEND_ABSORB", "1") != "0"
 SUPPORTED_BITS = (2, 3, 4, 8)
 DTYPES = ("float32", "bfloat16")
 
@@ -586,7 +588,25 @@ class _Session:
         # attention.py:343-347 + _GroupStore.append (:248-255), both sides in one launch
         # (PALU_APPEND_SPLIT=1: one launch per side, for A/B timing)
         assert K.cap == V.cap
-        if _APPEND_SPLIT:
+        # rope on: the query absorption's output buffer and layout (UW K order
+        # matches the converter's code order for int4 / int2 keys)
+        if self.fused_layers[li]:
+            uw_ptr, layout = _ptr(self.uw_bf), 1
+        elif self.tc_layers[li]:
+            uw_ptr, layout = _ptr(self.uw_bf), {4: 2, 2: 3}.get(K.bits, 1)
+        else:
+            uw_ptr, layout = _ptr(self.uw), 0
+        absorbed = self.rope and _APPEND_ABSORB and not _APPEND_SPLIT
+        if absorbed:
+            # append and query absorption in one launch (both read only y and t)
+            _lib.call("palu_append_absorb", code, K.bits, V.bits, yp + 4 * qd,
+                      yp + 4 * (qd + sk_sum), B, self.n1, K.G, V.G, _ptr(L.ranks_k_dev),
+                      _ptr(L.latoff_k_dev), _ptr(L.ranks_v_dev), _ptr(L.latoff_v_dev),
+                      _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), _ptr(K.scales64), _ptr(K.zps64),
+                      _ptr(V.rows), _ptr(V.scales), _ptr(V.zps), _ptr(V.scales64), _ptr(V.zps64),
+                      K.r_pad, V.r_pad, K.cap, yp, self.n1, n, dh, L.s_k, _ptr(L.bk), L.bk.shape[1],
+                      _ptr(f.theta_dev), self.scale, uw_ptr, layout, _ptr(self.t_dev), st)
+        elif _APPEND_SPLIT:
             for S, lat, rk, lo in ((K, yp + 4 * qd, L.ranks_k_dev, L.latoff_k_dev),
                                    (V, yp + 4 * (qd + sk_sum), L.ranks_v_dev, L.latoff_v_dev)):
                 _lib.call("palu_latent_append", code, S.bits, lat, B, self.n1, S.G, _ptr(rk),
@@ -613,10 +633,11 @@ class _Session:
                           _ptr(self.logits), self.ld_logits, st)
             self._value(li, st)
             return
-        if self.fused_layers[li]:
+        if not absorbed:
             _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
                       L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
-                      _ptr(self.uw_bf), 1, st)
+                      uw_ptr, layout, st)
+        if self.fused_layers[li]:
             _lib.call("palu_rope_attend_tc", _ptr(K.rows), _ptr(V.rows), B, n, L.s_k, K.G, K.r_pad,
                       V.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab), _ptr(self.t_dev),
                       _ptr(self.logits), self.ld_logits, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev),
@@ -625,18 +646,10 @@ class _Session:
                       _ptr(x), d, 0, st)
             return
         if self.tc_layers[li]:
-            # UW K order matches the converter's code order for int4 / int2 keys
-            layout = {4: 2, 2: 3}.get(K.bits, 1)
-            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
-                      L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
-                      _ptr(self.uw_bf), layout, st)
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                       n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
         else:
-            _lib.call("palu_query_absorb", code, yp, B, self.n1, n, dh, L.s_k, _ptr(L.bk),
-                      L.bk.shape[1], K.r_pad, _ptr(f.theta_dev), self.scale, _ptr(self.t_dev),
-                      _ptr(self.uw), 0, st)
             _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps),
                       B, n, dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),
                       _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)

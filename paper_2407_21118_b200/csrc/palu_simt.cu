@@ -323,17 +323,15 @@ __global__ void pack_rows_kernel(const uint8_t* __restrict__ codes, int cols, in
 // Query absorption (attention.py:428-431 queries, folded into the key factor).
 // grid (n_heads, B); fp64 RoPE of q at t, then u/w columns per rank row k.
 // ---------------------------------------------------------------------------
+// One CTA: head i, rank rows [32 ky, +32), batch row b.  PDL split form: the
+// fp64 angles (t, theta) and the B_k slice (constant) are prepared before the
+// pdl_wait() for the GEMV that produced q.
 template <typename T>
-__global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n_heads, int dh,
-                                    int s_k, const T* __restrict__ bk, int bk_rows, int R_pad,
-                                    const double* __restrict__ theta, float scale,
-                                    const int* __restrict__ t_dev, void* __restrict__ uw,
-                                    int layout, int split) {
-  // PDL split form: the fp64 angles (t, theta) and the B_k slice (constant)
-  // are prepared before waiting for the GEMV that produced q
-  pdl_launch();
-  if (!split) pdl_wait();
-  // grid (n_heads, ceil(R_pad / 32), B): one head, 32 rank rows per CTA
+__device__ __forceinline__ void query_absorb_body(const float* __restrict__ q, int ld_q, int n_heads, int dh,
+                                                  int s_k, const T* __restrict__ bk, int bk_rows, int R_pad,
+                                                  const double* __restrict__ theta, float scale,
+                                                  const int* __restrict__ t_dev, void* __restrict__ uw,
+                                                  int layout, int i, int ky, int b) {
   // qr[dh], then bs[32][dh + 1] (row pad: the bf16 layouts read one column
   // across 32 rank rows per warp, which an unpadded dh stride maps to one
   // bank), then cos/sin[dh/2] in fp64
@@ -341,7 +339,7 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
   float* qr = qa_sm;
   float* bs = qa_sm + dh;
   const int bstr = dh + 1;
-  const int i = blockIdx.x, k0 = blockIdx.y * 32, b = blockIdx.z;
+  const int k0 = ky * 32;
   const int half = dh / 2;
   double* csn = reinterpret_cast<double*>(qa_sm + dh + 32 * (dh + 1));  // [half] cos, [half] sin
   const int g = i / s_k, p = i - g * s_k;
@@ -427,6 +425,60 @@ __global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n
           __float2bfloat16_rn(scale * (qr[j + half] * b1 - qr[j] * b2));
     }
   }
+}
+
+// grid (n_heads, ceil(R_pad / 32), B)
+template <typename T>
+__global__ void query_absorb_kernel(const float* __restrict__ q, int ld_q, int n_heads, int dh,
+                                    int s_k, const T* __restrict__ bk, int bk_rows, int R_pad,
+                                    const double* __restrict__ theta, float scale,
+                                    const int* __restrict__ t_dev, void* __restrict__ uw,
+                                    int layout, int split) {
+  pdl_launch();
+  if (!split) pdl_wait();
+  query_absorb_body<T>(q, ld_q, n_heads, dh, s_k, bk, bk_rows, R_pad, theta, scale, t_dev, uw, layout,
+                       blockIdx.x, blockIdx.y, blockIdx.z);
+}
+
+// The latent append (both sides) and the query absorption of one layer in one
+// launch: both read only the GEMV output (and t), and the score kernel needs
+// both, so one grid takes the append off the serial launch chain.  Blocks
+// [0, n_abs) absorb (head, rank block, batch row); the rest append.
+struct AbsorbArgs {
+  const float* q;
+  int ld_q, n_heads, dh, s_k;
+  const void* bk;
+  int bk_rows, R_pad;
+  const double* theta;
+  float scale;
+  void* uw;
+  int layout, gy;
+};
+template <typename T>
+__global__ void append_absorb_kernel(AppendSide k, AppendSide v, int ld_lat, int T_cap,
+                                     const int* __restrict__ t_dev, AbsorbArgs a, int n_abs) {
+  pdl_launch();
+  const int bid = blockIdx.x;
+  if (bid < n_abs) {
+    const int i = bid % a.n_heads, rest = bid / a.n_heads;
+    query_absorb_body<T>(a.q, a.ld_q, a.n_heads, a.dh, a.s_k, reinterpret_cast<const T*>(a.bk), a.bk_rows,
+                         a.R_pad, a.theta, a.scale, t_dev, a.uw, a.layout, i, rest % a.gy, rest / a.gy);
+    return;
+  }
+  pdl_wait();  // the GEMV's latents and the step position
+  extern __shared__ double qsm[];
+  const int r = bid - n_abs, gs = k.G + v.G;
+  const int gi = r % gs, b = r / gs;
+  const bool is_k = gi < k.G;
+  const AppendSide& s = is_k ? k : v;
+  const int g = is_k ? gi : gi - k.G;
+  const int t = *t_dev;
+  if (s.bits == 16)
+    append_raw_body<T>(s.lat, ld_lat, s.G, s.ranks, s.lat_off, reinterpret_cast<T*>(s.rows), s.R_pad, T_cap, t,
+                       g, b);
+  else
+    append_quant_body(s.lat, ld_lat, s.G, s.bits, s.ranks, s.lat_off, reinterpret_cast<uint8_t*>(s.rows),
+                      s.scales, s.zps, s.scales64, s.zps64, s.R_pad, T_cap, t, g, b, qsm);
 }
 
 // ---------------------------------------------------------------------------
@@ -1473,6 +1525,48 @@ int palu_query_absorb(int dtype, const float* q, int B, int ld_q, int n_heads, i
     PALU_CK(launch_k(query_absorb_kernel<float>, dim3(grid), dim3(256), smem, S(stream), q, ld_q,
                      n_heads, head_dim, s_k, (const float*)bk, bk_rows, R_pad, theta, scale, t_dev,
                      uw, layout, pdl_split()));
+  PALU_LAUNCHED();
+  return PALU_OK;
+}
+
+int palu_append_absorb(int dtype, int bits_k, int bits_v, const float* lat_k, const float* lat_v, int B,
+                       int ld_lat, int G_k, int G_v, const int* ranks_k, const int* lat_off_k,
+                       const int* ranks_v, const int* lat_off_v, void* rows_k, float* scales_k,
+                       float* zps_k, double* scales64_k, int64_t* zps64_k, void* rows_v, float* scales_v,
+                       float* zps_v, double* scales64_v, int64_t* zps64_v, int R_pad_k, int R_pad_v,
+                       int T_cap, const float* q, int ld_q, int n_heads, int head_dim, int s_k,
+                       const void* bk, int bk_rows, const double* theta, float scale, void* uw, int layout,
+                       const int* t_dev, void* stream) {
+  PALU_REQUIRE(B > 0 && G_k > 0 && G_v > 0 && R_pad_k > 0 && R_pad_v > 0 && T_cap > 0,
+               "palu_append_absorb: bad sizes");
+  PALU_REQUIRE(bk_rows >= R_pad_k, "palu_append_absorb: bk has %d rows < R_pad %d", bk_rows, R_pad_k);
+  PALU_REQUIRE(head_dim % 2 == 0, "rotary embedding requires an even head_dim");
+  PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k, n_heads);
+  PALU_REQUIRE(layout >= 0 && layout <= 3, "palu_append_absorb: layout must be 0..3");
+  size_t smem = ((size_t)head_dim + 32 * ((size_t)head_dim + 1)) * sizeof(float) +
+                (size_t)head_dim * sizeof(double);
+  for (int side = 0; side < 2; ++side) {
+    const int bits = side ? bits_v : bits_k, R_pad = side ? R_pad_v : R_pad_k;
+    if (bits == 16) continue;
+    PALU_REQUIRE(bits == 2 || bits == 3 || bits == 4 || bits == 8,
+                 "bits must be one of (2, 3, 4, 8), got %d", bits);
+    PALU_REQUIRE(R_pad % 32 == 0, "quantised rows need R_pad %% 32 == 0 (got %d)", R_pad);
+    const size_t need = (size_t)(R_pad + 64) * sizeof(double) + R_pad;
+    if (need > smem) smem = need;
+  }
+  const AppendSide k{bits_k, G_k, R_pad_k, lat_k, ranks_k, lat_off_k, rows_k,
+                     scales_k, zps_k, scales64_k, zps64_k};
+  const AppendSide v{bits_v, G_v, R_pad_v, lat_v, ranks_v, lat_off_v, rows_v,
+                     scales_v, zps_v, scales64_v, zps64_v};
+  const int gy = (R_pad_k + 31) / 32;
+  const AbsorbArgs a{q, ld_q, n_heads, head_dim, s_k, bk, bk_rows, R_pad_k, theta, scale, uw, layout, gy};
+  const int n_abs = n_heads * gy * B, n_app = (G_k + G_v) * B;
+  if (dtype == PALU_DTYPE_BF16)
+    PALU_CK(launch_k(append_absorb_kernel<bf16>, dim3(n_abs + n_app), dim3(256), smem, S(stream), k, v, ld_lat,
+                     T_cap, t_dev, a, n_abs));
+  else
+    PALU_CK(launch_k(append_absorb_kernel<float>, dim3(n_abs + n_app), dim3(256), smem, S(stream), k, v, ld_lat,
+                     T_cap, t_dev, a, n_abs));
   PALU_LAUNCHED();
   return PALU_OK;
 }
