@@ -583,7 +583,7 @@ class _Session:
         n1 = int(L.w1.shape[0])
         sk_sum = sum(L.key_ranks)
         qd = L.qdim if L.qdim else d
-        _lib.call("palu_gemv", code, _ptr(L.w1), n1, d, _ptr(x), B, d, _ptr(y), self.n1, 0, st)
+        self._proj(code, L.w1, n1, d, x, y, st)
         yp = y.data_ptr()
         # attention.py:343-347 + _GroupStore.append (:248-255), both sides in one launch
         # (PALU_APPEND_SPLIT=1: one launch per side, for A/B timing)
@@ -642,8 +642,7 @@ class _Session:
                       V.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab), _ptr(self.t_dev),
                       _ptr(self.logits), self.ld_logits, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev),
                       _ptr(self.ctx), self.ko, _ptr(self.ws_fused), self.score_sms, st)
-            _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
-                      _ptr(x), d, 0, st)
+            self._proj(code, L.woT, d, L.ko_pad, self.ctx, x, st)
             return
         if self.tc_layers[li]:
             _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
@@ -672,8 +671,25 @@ class _Session:
                       B, n, L.s_v, V.G, V.r_pad, _ptr(L.ranks_v_dev), _ptr(L.o_off_dev), V.cap,
                       _ptr(self.logits), self.ld_logits, self.planes[li], self.plane,
                       _ptr(self.t_dev), self.n_chunks, _ptr(self.ws), _ptr(self.ctx), self.ko, st)
-        _lib.call("palu_gemv", code, _ptr(L.woT), d, L.ko_pad, _ptr(self.ctx), B, self.ko,
-                  _ptr(self.x), d, 0, st)
+        self._proj(code, L.woT, d, L.ko_pad, self.ctx, self.x, st)
+
+    def _proj(self, code, W, N: int, K: int, xt, yt, st: int):
+        """y[:, :N] = x[:, :K] @ W[:N, :K]^T (attention.py:344-347, 430, 361).
+
+        Decode batches (B < 16) stream the weights once through palu_gemv.  For
+        B >= 16 the projection is a plain GEMM and goes to cuBLAS (bf16 weights,
+        x split into bf16 hi + lo rows, fp32 output: ~16 mantissa bits of x):
+        palu_gemv would re-stream the weights once per 2-4 batch rows."""
+        B = self.B
+        if B >= 16 and code == _lib.DTYPE_BF16:
+            torch = _torch()
+            xs = xt[:, :K]
+            hi = xs.to(torch.bfloat16)
+            lo = (xs - hi.float()).to(torch.bfloat16)
+            out = torch.mm(torch.cat([hi, lo]), W[:N, :K].t(), out_dtype=torch.float32)
+            torch.add(out[:B], out[B:], out=yt[:, :N])
+        else:
+            _lib.call("palu_gemv", code, _ptr(W), N, K, _ptr(xt), B, xt.shape[1], _ptr(yt), yt.shape[1], 0, st)
 
     def launch_step(self):
         """All layers + t += 1 on the current stream (graph-capturable)."""

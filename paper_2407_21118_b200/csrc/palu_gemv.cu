@@ -210,11 +210,12 @@ static int stream_nb(const bf16* W, int N, int K, const float* x, int B, int ldx
 }  // namespace tc
 
 // Returns PALU_EUNSUPPORTED when the shape is not streamable (the caller then
-// uses the warp-per-row kernel): K a multiple of 2048 up to 16384, batch <= 8.
+// uses the warp-per-row kernel): K a multiple of 2048 up to 16384, batch <= 256
+// (more than MAXB rows stream the weights once per MAXB-row chunk).
 int gemv_stream(const bf16* W, int N, int K, const float* x, int B, int ldx, float* y, int ldy,
                 int acc, cudaStream_t st) {
   using namespace tc;
-  if (K % 2048 != 0 || K > 16384 || B > 8 || ldx % 4 != 0) return PALU_EUNSUPPORTED;
+  if (K % 2048 != 0 || K > 16384 || B > 256 || ldx % 4 != 0) return PALU_EUNSUPPORTED;
   switch (K / 2048) {
     case 1: return stream_nb<1>(W, N, K, x, B, ldx, y, ldy, acc, st);
     case 2: return stream_nb<2>(W, N, K, x, B, ldx, y, ldy, acc, st);

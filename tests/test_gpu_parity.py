@@ -640,3 +640,25 @@ def test_batched_prefill_llama_shape_bf16(P):
     assert rel_err(ya, yb) < 5e-3
     print(f"prefill 1024 tokens x 2 layers: batched {t1 - t0:.3f} s, stepwise {t2 - t1:.3f} s")
     assert t1 - t0 < t2 - t1
+
+
+def test_batched_projection_matches_gemv(P):
+    """B >= 16: the step's projections run as cuBLAS GEMMs on bf16 hi + lo
+    rows of x (attention._Session._proj); they agree with the streaming
+    palu_gemv on the same weights and inputs."""
+    import torch
+    from paper_2407_21118_b200 import _lib
+    from paper_2407_21118_b200.attention import _Session, _ptr, _stream
+    from paper_2407_21118_b200.harness import synthetic_engine
+    _, fused, cache = synthetic_engine(layers=1, batch=16, context=600, extra=8, seed=3)
+    s = _Session(fused, cache, use_graph=False)
+    L = fused.layers[0]
+    x = torch.randn(16, s.d, device="cuda")
+    y_mm = torch.zeros(16, s.n1, device="cuda")
+    y_gv = torch.zeros(16, s.n1, device="cuda")
+    n1 = int(L.w1.shape[0])
+    s._proj(fused.dtype_code, L.w1, n1, s.d, x, y_mm, _stream())
+    _lib.call("palu_gemv", fused.dtype_code, _ptr(L.w1), n1, s.d, _ptr(x), 16, s.d, _ptr(y_gv), s.n1, 0,
+              _stream())
+    torch.cuda.synchronize()
+    assert rel_err(y_mm[:, :n1].double().cpu().numpy(), y_gv[:, :n1].double().cpu().numpy()) < 1e-5
