@@ -47,10 +47,11 @@ __device__ __forceinline__ void pdl_enter() {
 // A kernel K starts once its predecessor P executed launch_dependents: if P
 // waits first (pdl_enter), everything before P has completed; if P is split,
 // only what precedes P's own wait is guaranteed.  In the step order
-//   gemv (split) -> append K+V (enter) -> absorb (split) -> score (split)
-//   -> value (split) -> merge (enter) -> gemv (split)
-// score and value start once the layer's first GEMV completed, while the
-// append of row t may still run.  Rule: every thread that reads a latent row,
+//   gemv (split) -> append K+V + absorb (split: one grid; append blocks wait
+//   first, absorb blocks before reading q) -> score (split) -> value (split)
+//   -> merge (enter) -> gemv (split)
+// score and value may start while the append of row t still runs.  Rule:
+// every thread that reads a latent row,
 // scale or zero point of the NEWEST token (row t) executes pdl_wait() first
 // (griddepcontrol.wait returns after the whole predecessor chain completed).
 // Rows < t were written by earlier steps and may be read before the wait:
