@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--rank-k", type=int, default=256)
     ap.add_argument("--rank-v", type=int, default=256)
     ap.add_argument("--zero-keys", action="store_true", help="zero the key latents (data-power test)")
+    ap.add_argument("--bits", type=int, default=16)
     a = ap.parse_args()
     import torch
 
@@ -35,7 +36,7 @@ def main():
 
     _lib.load()
     w, f, c = synthetic_engine(layers=1, batch=1, context=a.context, extra=64, rank_k=a.rank_k,
-                               rank_v=a.rank_v)
+                               rank_v=a.rank_v, bits=a.bits)
     if a.zero_keys:
         for K, _ in c._stores:
             K.rows.zero_()
