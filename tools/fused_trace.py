@@ -72,9 +72,6 @@ def main():
         ph = np.array([[us(tr[i, c]) for c in (495, 496, 497, 498)] for i in value])
         print("value setup done / first TMA / first stage landed / ring wrapped (median us):",
               np.median(ph, axis=0).round(2), "vs end", round(float(np.median([us(tr[i, 1]) for i in value])), 1))
-        fa = np.array([[us(tr[i, c]) for c in (489, 490, 491)] for i in value])
-        print("group A first sub-block: loads issued / max done / P ready (median us):",
-              np.median(fa, axis=0).round(2))
         ev = np.array([us(tr[i, 1]) for i in value])
         sm = np.array([tr[i, 2] for i in value])
         print("end by SM parity: even", np.median(ev[sm % 2 == 0]).round(1), "odd", np.median(ev[sm % 2 == 1]).round(1))
