@@ -1,6 +1,6 @@
 #!/bin/bash
 # score epilogue: parity subset, per-unit trace (diagnostic build), bench A/B
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 TAG=${1:-x}
 timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "quantized_keys or fused or medium or c1 or tcgen05_score" 2>&1 | tail -2

@@ -1,7 +1,7 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 300 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -1
-for a in "" "--rank-k 128 --rank-v 384 --bits 16,4" "--batch 4 --context 16384"; do
+for a in "" "--rank-k 128 --rank-v 384" "--rank-k 128 --rank-v 384 --bits 16,4" "--bits 4"; do
   bash tools/ab_lib.sh abtmp/head/libpalu_b200.so paper_2407_21118_b200/libpalu_b200.so $a
-done 2>&1 | tee gpurun_out/r2_gemv2.txt
+done 2>&1 | tee gpurun_out/r2_gate.txt

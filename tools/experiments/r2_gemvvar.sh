@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 run() { v=$(env "$@" timeout 150 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), round(d['roofline']['per_kernel_ms']['palu_gemv']*1e3,2))"); echo "$*: $v"; }
 for rep in 1 2; do

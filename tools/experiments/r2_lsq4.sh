@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "norope" 2>&1 | tail -1
 run() { v=$(env "$@" timeout 150 python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-baseline --rope off --bits 4 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['value'],1), round(d['roofline']['per_kernel_ms']['palu_latent_score_tc']*1e3,1))"); echo "$*: $v"; }

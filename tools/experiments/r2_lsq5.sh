@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 200 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "norope" 2>&1 | tail -1
 PALU_PARITY_LOG=gpurun_out/r02_parity_lsq.jsonl timeout 600 python -m pytest tests/test_gpu_long_parity.py -q -m gpu -x -k "norope_r256_int4" 2>&1 | tail -1

@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:"latent_score_q|value_q_kernel" -c 2 -o gpurun_out/prof_lsq python bench.py --steps 1 --warmup 3 --no-cpu --no-e2e --no-baseline --layers 2 --rope off --bits 4 > /dev/null 2>&1
 python profiles/ncu_summary.py gpurun_out/prof_lsq.ncu-rep > gpurun_out/prof_lsq.txt 2>&1

@@ -1,6 +1,6 @@
 #!/bin/bash
 # packed-key hand-off relay: parity + bench
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 timeout 400 python -m pytest tests/test_gpu_parity.py -q -m gpu -x 2>&1 | tail -2
 for v in "int4:--bits 4" "int2:--bits 2" "k4v4p:--rank-k 128 --rank-v 384 --bits 4" "norope_int4:--rope off --bits 4" "k16v4:--rank-k 128 --rank-v 384 --bits 16,4" "default:"; do

@@ -1,5 +1,5 @@
 #!/bin/bash
-cd "$(dirname "$0")/.."
+cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 for m in 0 1 3; do
   echo "== PALU_VALUE_DIAG=$m"
