@@ -174,6 +174,16 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
                        void* stream);
+/*
+ * palu_rope_score_tc that also brings l2_prefetch[0, l2_prefetch_bytes) into
+ * L2 with an evict-last policy while it runs (the tensor-bound score leaves
+ * HBM bandwidth idle): the host passes the layer's wo_fused^T, which the
+ * output GEMV then reads from L2.  The latent streams load evict-first.
+ */
+int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const float* zps, int B,
+                          int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
+                          const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
+                          const void* l2_prefetch, long long l2_prefetch_bytes, void* stream);
 
 /*
  * Fused RoPE score + softmax + value path (attention.py:433-446, 350-362 up

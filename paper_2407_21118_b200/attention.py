@@ -35,6 +35,8 @@ FP_BITS = 16
 _APPEND_SPLIT = os.environ.get("PALU_APPEND_SPLIT") == "1"  # A/B diagnostics only
 # PALU_APPEND_ABSORB=0: separate append and absorb launches (A/B diagnostics only)
 _APPEND_ABSORB = os.environ.get("PALU_APPEND_ABSORB", "1") != "0"
+# PALU_L2PF=1: L2 prefetch of the output projection during the score (measured slower; A/B)
+_L2PF = os.environ.get("PALU_L2PF") == "1"
 SUPPORTED_BITS = (2, 3, 4, 8)
 DTYPES = ("float32", "bfloat16")
 
@@ -645,9 +647,15 @@ class _Session:
             self._proj(code, L.woT, d, L.ko_pad, self.ctx, x, st)
             return
         if self.tc_layers[li]:
-            _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
-                      n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
-                      _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
+            if _L2PF:  # the output projection's weights ride into L2 during the score
+                _lib.call("palu_rope_score_tc_pf", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
+                          n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
+                          _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, _ptr(L.woT),
+                          L.woT.numel() * L.woT.element_size(), st)
+            else:
+                _lib.call("palu_rope_score_tc", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
+                          n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),
+                          _ptr(self.t_dev), _ptr(self.logits), self.ld_logits, st)
         else:
             _lib.call("palu_rope_score", code, K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps),
                       B, n, dh, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw), _ptr(f.theta_dev),

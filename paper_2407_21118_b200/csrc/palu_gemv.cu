@@ -65,16 +65,19 @@ gemv_stream_kernel(const __grid_constant__ CUtensorMap map_w, const bf16* __rest
   if (warp == GS_WARPS) {
     // ---------------- producer: contiguous row chunks of W ----------------
     if (lane == 0) {
+      const uint64_t pol_first = policy_evict_first();
       Ring rg;
       for (int c = 0; c < nchunks; ++c, rg.next(GS_SLOTS)) {
         const int row = r0 + c * rpc;
         const int nr = min(rpc, r1 - row);
         mbar_wait(&empty[rg.slot], rg.phase ^ 1);
         mbar_expect_tx(&full[rg.slot], (uint32_t)(nr * row_bytes));
-        // one 2-D tensor box per weight row (W viewed as 256-byte rows)
+        // one 2-D tensor box per weight row (W viewed as 256-byte rows); the
+        // weights are read once per step: evict-first (an L2 hit on rows the
+        // score kernel prefetched demotes them)
         for (int r = 0; r < nr; ++r)
-          tma_load_2d(&map_w, &full[rg.slot], ring + rg.slot * GS_CHUNK + r * row_bytes, 0,
-                      (int)((size_t)(row + r) * (row_bytes / 256)));
+          tma_load_2d_hint(&map_w, &full[rg.slot], ring + rg.slot * GS_CHUNK + r * row_bytes, 0,
+                           (int)((size_t)(row + r) * (row_bytes / 256)), pol_first);
       }
     }
     return;  // the producer takes no part in the reductions below

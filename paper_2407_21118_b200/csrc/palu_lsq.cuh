@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         }
       };
       prefetch(i0 + LQ_PF);
+      const uint64_t pol_first = policy_evict_first();  // codes are read once
       Ring rg;
       for (int i = i0; i < i1; ++i, rg.next(p.raw_slots)) {
         prefetch(i + 1 + LQ_PF);
@@ -151,8 +152,8 @@ __global__ void __launch_bounds__(LQ_THREADS, 1) latent_score_q_kernel(const LQP
         mbar_wait(&rempty[rg.slot], rg.phase ^ 1);
         mark(8, i - i0);
         mbar_expect_tx(&rfull[rg.slot], (uint32_t)RB);
-        bulk_load(raw + (size_t)rg.slot * RB, p.codes + ((size_t)bg * p.T_cap + tile * TILE_M) * p.row_bytes,
-                  (uint32_t)RB, &rfull[rg.slot]);
+        bulk_load_hint(raw + (size_t)rg.slot * RB, p.codes + ((size_t)bg * p.T_cap + tile * TILE_M) * p.row_bytes,
+                       (uint32_t)RB, &rfull[rg.slot], pol_first);
       }
     }
   } else if (warp == 1) {

@@ -42,6 +42,11 @@ struct Params {
   int pf_dist;  // L2 prefetch distance in work items (0 = off)
   int pdl_split;  // 0: wait for the predecessor at entry (A/B diagnostics)
   const float2* rope_tab;  // [n_tab + 128][64]
+  // weights of a later kernel (the layer's output projection) to bring into
+  // L2 with an evict-last policy while this tensor-bound kernel leaves HBM
+  // bandwidth idle; the latent streams load evict-first
+  const uint8_t* l2pf;
+  long long l2pf_bytes;
   const int* t_dev;
   float* logits;
   unsigned long long* trace;  // diagnostics only (PALU_FUSED_TRACE): [CTA][TRACE_STRIDE]
@@ -164,13 +169,14 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
     // shift and a LOP3: 0x43004300 | ((w >> BITS k) & mask)
     constexpr uint32_t MASK = BITS == 4 ? 0x000F000Fu : 0x00030003u;
     constexpr int NV = 2 * BITS / 4;  // uint4 loads per row per k-block (32 B int4, 16 B int2)
+    const uint64_t pol = policy_evict_first();  // codes are read once: keep L2 for the logits
     uint4 nx[RPL][2], cu[RPL][2];
     auto load4 = [&](int kb) {
 #pragma unroll
       for (int rr = 0; rr < RPL; ++rr)
 #pragma unroll
         for (int q = 0; q < NV; ++q)
-          nx[rr][q] = ok[rr] ? __ldg(reinterpret_cast<const uint4*>(rowp[rr] + kb * 8 * BITS) + q)
+          nx[rr][q] = ok[rr] ? ldg128_hint(reinterpret_cast<const uint4*>(rowp[rr] + kb * 8 * BITS) + q, pol)
                              : make_uint4(0u, 0u, 0u, 0u);
     };
     load4(0);
@@ -378,9 +384,19 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         }
       pdl_wait();
       int cur = -1, nloads = 0, it = 0, pst = 0, pph = 0;
+      const uint64_t pol_first = policy_evict_first(), pol_last = policy_evict_last();
+      // this CTA's slice of the L2 prefetch, one 32 KB piece per item
+      constexpr long long PF_PIECE = 32768;
+      const long long pf_share = ((p.l2pf_bytes + gridDim.x - 1) / gridDim.x + PF_PIECE - 1) / PF_PIECE * PF_PIECE;
+      long long pf_at = (long long)blockIdx.x * pf_share;
+      const long long pf_end = min(p.l2pf_bytes, pf_at + pf_share);
       ItemPos ip_(i0, n_super, p.G);
       for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
         const int bg = ip_.bg, st = ip_.st;
+        if (p.l2pf != nullptr && pf_at < pf_end) {
+          bulk_prefetch_l2_hint(p.l2pf + pf_at, (uint32_t)min(PF_PIECE, pf_end - pf_at), pol_last);
+          pf_at += PF_PIECE;
+        }
         if (bg != cur) {
           if (nloads > 0) mbar_wait(uw_empty, (nloads - 1) & 1);
           if (leader) mbar_expect_tx(uw_full, 2 * kblocks * units * UWB);
@@ -410,7 +426,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[pst], pph ^ 1);
           if (leader) mbar_expect_tx(&full[pst], 2 * H_STAGE_BYTES);
-          tma_load_2d_pair(&map_h, &full[pst], s_h + pst * H_STAGE_BYTES, kb * KB, h_row);
+          tma_load_2d_pair_hint(&map_h, &full[pst], s_h + pst * H_STAGE_BYTES, kb * KB, h_row, pol_first);
           if (++pst == p.stages) {
             pst = 0;
             pph ^= 1;
@@ -1167,6 +1183,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
     // so it streams every sub-unit back to back, bounded by the ring
     if (lane == 0 && vp.bits == 16) {
       prefetch_map(&map_v);
+      const uint64_t pol_first = policy_evict_first();  // H_v is read once; keep L2 for the weights
       int ctr = 0;
       bool waited = false;
       Ring rg;
@@ -1197,8 +1214,8 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
             if (vtr != nullptr && ctr == 0) vtr[496] = gtimer();  // first TMA issue
             mbar_expect_tx(&full[st], V_STAGE);
             const int row = u.bg * p.T_cap + c0 + blk * TILE_M;
-            tma_load_2d(&map_v, &full[st], ring + st * V_STAGE, j * 128, row);
-            tma_load_2d(&map_v, &full[st], ring + st * V_STAGE + V_STAGE / 2, j * 128 + 64, row);
+            tma_load_2d_hint(&map_v, &full[st], ring + st * V_STAGE, j * 128, row, pol_first);
+            tma_load_2d_hint(&map_v, &full[st], ring + st * V_STAGE + V_STAGE / 2, j * 128 + 64, row, pol_first);
           }
       }
     }
@@ -1735,6 +1752,7 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
   const uint32_t tmem = *tslot;
   if (warp == 0) {
     if (lane == 0 && p.bits == 16) {
+      const uint64_t pol_first = policy_evict_first();  // H_k is read once: keep L2 for the logits
       Ring rg;
       for (int i = i0; i < i1; ++i) {
         const int bg = i / ntile, tile = i - bg * ntile;
@@ -1742,8 +1760,8 @@ latent_score_tc_kernel(const __grid_constant__ CUtensorMap map_h, const LSParams
           const int st = rg.slot;
           mbar_wait(&empty[st], rg.phase ^ 1);
           mbar_expect_tx(&full[st], H_STAGE_BYTES);
-          tma_load_2d(&map_h, &full[st], s_h + st * H_STAGE_BYTES, kb * KB,
-                      bg * p.T_cap + tile * TILE_M);
+          tma_load_2d_hint(&map_h, &full[st], s_h + st * H_STAGE_BYTES, kb * KB,
+                           bg * p.T_cap + tile * TILE_M, pol_first);
         }
       }
     }
@@ -1956,6 +1974,14 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
                        int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                        const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
                        void* stream) {
+  return palu_rope_score_tc_pf(bits, hk, scales, zps, B, n_heads, s_k, G, R_pad, T_cap, uw, rope_tab, t_dev,
+                               logits, ld_logits, nullptr, 0, stream);
+}
+
+int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const float* zps, int B,
+                          int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
+                          const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
+                          const void* l2_prefetch, long long l2_prefetch_bytes, void* stream) {
   using namespace palu::tc;
   if (bits != 16 && bits != 2 && bits != 3 && bits != 4 && bits != 8) {
     set_error("palu_rope_score_tc: bits %d unsupported", bits);
@@ -2019,6 +2045,8 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
   // stream through TMA and do better without it (tools/pf_sweep.sh)
   prm.pf_dist = getenv("PALU_TC_PF") ? atoi(getenv("PALU_TC_PF")) : (bits == 16 ? PF_DIST : 3);
   prm.rope_tab = reinterpret_cast<const float2*>(rope_tab);
+  prm.l2pf = reinterpret_cast<const uint8_t*>(l2_prefetch);
+  prm.l2pf_bytes = l2_prefetch ? l2_prefetch_bytes : 0;
   prm.t_dev = t_dev;
   prm.logits = logits;
   prm.trace = nullptr;

@@ -298,6 +298,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       Ring rg;
       bool waited = false;
       int kblk = 0;
+      const uint64_t pol_first = policy_evict_first();  // codes are read once: keep L2 for the logits
       // L2 prefetch cursor VQ_PF blocks ahead of the loads: the HBM latency
       // then overlaps the ring turnaround instead of gating it
       VQIter pit(i0, i1, n_super);
@@ -362,8 +363,8 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
           mark(8 + min(kblk++, 47));
           // a block of one (sequence, group) is one contiguous range of the cache
           mbar_expect_tx(&rfull[rg.slot], RB);
-          bulk_load(raw + (size_t)rg.slot * RS, p.codes + ((size_t)bg * p.T_cap + t0) * p.row_bytes,
-                    (uint32_t)RB, &rfull[rg.slot]);
+          bulk_load_hint(raw + (size_t)rg.slot * RS, p.codes + ((size_t)bg * p.T_cap + t0) * p.row_bytes,
+                    (uint32_t)RB, &rfull[rg.slot], pol_first);
           rg.next(p.raw_slots);
         }
       }

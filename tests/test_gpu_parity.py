@@ -624,6 +624,9 @@ def test_batched_prefill_llama_shape_bf16(P):
     fused = P.build_fused(w, dec, cfg, dtype="bfloat16")
     toks = po.random_matrix(1024, 4096, 701) * 0.5
     import torch
+    # warm both paths (cuBLAS handles, lazy module loads) before timing them
+    palu_prefill(w, dec, cfg, toks[:16], fused=fused, batched=True)
+    palu_prefill(w, dec, cfg, toks[:16], fused=fused, batched=False)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     fast = palu_prefill(w, dec, cfg, toks, fused=fused, batched=True)
