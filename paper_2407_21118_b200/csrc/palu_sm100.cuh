@@ -296,6 +296,14 @@ __device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint3
       "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
       : "memory");
 }
+__device__ __forceinline__ void stg_hint(float* dst, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(dst), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ float2 ldg64_cg_hint(const void* src, uint64_t pol) {
+  float2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(v.x), "=f"(v.y) : "l"(src), "l"(pol));
+  return v;
+}
 // read-only 16-byte global load with an L2 eviction policy
 __device__ __forceinline__ uint4 ldg128_hint(const void* src, uint64_t pol) {
   uint4 v;

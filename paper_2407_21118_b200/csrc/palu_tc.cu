@@ -545,6 +545,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     const int jh = (warp - 2) >> 2;  // which 32 of the 64 frequencies
     const int delta = q * 32 + lane; // token row inside this SM's tile
     constexpr int CH = 8;            // frequencies per epilogue chunk (TMEM loads of 8 columns)
+    const uint64_t pol_keep = policy_evict_last();
     float2 cd2[16], sd2[16];         // cos/sin(delta th_j) for j pairs (2i, 2i + 1)
     {
       const float4* off =
@@ -680,8 +681,8 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             // head 2h + 1; UH 1: columns 0..63 u_j (leader), 64..127 w_j (peer)
             const int head0 = g * p.s_k + UH * h;
             float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
-            lg[0] = v0 * sq;
-            if (UH == 2) lg[p.ld_logits] = v1 * sq;
+            stg_hint(lg, v0 * sq, pol_keep);  // read by the value kernel next: keep in L2
+            if (UH == 2) stg_hint(lg + p.ld_logits, v1 * sq, pol_keep);
           }
           if (kTrace && p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == units - 1 &&
               it < TRACE_STRIDE - 8)
@@ -1304,6 +1305,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
       // the sub-block's logits (thread = token pairs 2 ta + 256 i); the next
       // sub-block's are loaded while this one is processed
       constexpr int NP = V_SUB / 256;
+      const uint64_t pol_drop = policy_evict_first();  // the logits are dead after this read
       float2 x[NP][V_HP], xn[NP][V_HP];
       // no value-dependent masking in the prefetch (an op on a loaded register
       // waits for the load); the masks are applied where the values are used
@@ -1314,7 +1316,7 @@ __device__ void value_role(const CUtensorMap& map_v, const Params& p, const VPar
 #pragma unroll
           for (int h = 0; h < V_HP; ++h) {
             float2 v = make_float2(0.f, 0.f);
-            if (h < s_v && t < nt) v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
+            if (h < s_v && t < nt) v = ldg64_cg_hint(lg + (size_t)h * p.ld_logits + t, pol_drop);
             dst[i][h] = v;
           }
         }

@@ -516,6 +516,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
       const float* lg = p.logits + ((size_t)b * p.n_heads + g * p.s) * p.ld_logits + c0;
       const float* sc = p.scales + (size_t)bg * p.T_cap + c0;
       const float* zp = p.zps + (size_t)bg * p.T_cap + c0;
+      const uint64_t pol_drop = policy_evict_first();  // the logits are dead after this read
       float2 x[V_HP], xn[V_HP], sv, svn, zv, zvn;
       // the sub-block's logits, scales and zero points; the next sub-block's
       // are in flight while this one runs
@@ -527,7 +528,7 @@ value_q_kernel(const __grid_constant__ CUtensorMap map_c, const VQParams p) {
 #pragma unroll
         for (int h = 0; h < V_HP; ++h) {
           float2 v = make_float2(0.f, 0.f);
-          if (h < p.s && t < nt) v = __ldcg(reinterpret_cast<const float2*>(lg + (size_t)h * p.ld_logits + t));
+          if (h < p.s && t < nt) v = ldg64_cg_hint(lg + (size_t)h * p.ld_logits + t, pol_drop);
           dst[h] = v;
         }
         sd = make_float2(1.f, 1.f);
