@@ -195,10 +195,19 @@ def test_cache_exports_match_oracle(P, golden):
     _, cache = P.palu_decode(w, dec, cfg, case["tokens"], bits=4)
     q = cache.layers[0].k_groups[0].quantized_latent()
     assert q.bits == 4 and q.codes.shape == (case["T"], 3)
-    ref_codes = g[f"c{ci}_L0_k0_codes"]
-    # fp32 latents vs the reference's fp64 ones may move a boundary code by one
-    assert np.mean(q.codes == ref_codes) > 0.9
-    assert np.max(np.abs(q.codes.astype(int) - ref_codes.astype(int))) <= 1
+    # every stored group: fp32 latents vs the reference's fp64 ones could move
+    # a boundary code by one; bound such flips at 1 % (measured: 0)
+    checked = 0
+    for li in range(len(case["layers"])):
+        for gi, grp in enumerate(cache.layers[li].k_groups):
+            key = f"c{ci}_L{li}_k{gi}_codes"
+            if key not in g.files:
+                continue
+            codes = grp.quantized_latent().codes
+            assert np.mean(codes != g[key]) <= 0.01, key
+            assert np.max(np.abs(codes.astype(int) - g[key].astype(int))) <= 1, key
+            checked += 1
+    assert checked > 0
 
 
 def test_validation_errors(P, golden):
