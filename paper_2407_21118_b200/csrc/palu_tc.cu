@@ -774,7 +774,10 @@ constexpr uint32_t IDESC_LS = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(1
 constexpr int V_TMEM_COLS = 128;
 constexpr int V_PF = 0;     // L2 prefetch distance of the value stream (128-token blocks)
 constexpr int V_SUB = 512;  // tokens per P sub-block (double-buffered)
-constexpr int V_HEAD_START = 2;  // H_v stages issued before the first logits have arrived
+#ifndef PALU_V_HEAD_START
+#define PALU_V_HEAD_START 2
+#endif
+constexpr int V_HEAD_START = PALU_V_HEAD_START;  // H_v stages issued before the first logits have arrived
 
 __device__ __forceinline__ uint32_t ld_acquire_u32(const int* p) {
   uint32_t v;
