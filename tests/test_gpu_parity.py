@@ -201,7 +201,7 @@ def test_cache_exports_match_oracle(P, golden):
     for li in range(len(case["layers"])):
         for gi, grp in enumerate(cache.layers[li].k_groups):
             key = f"c{ci}_L{li}_k{gi}_codes"
-            if key not in g.files:
+            if key not in g:
                 continue
             codes = grp.quantized_latent().codes
             assert np.mean(codes != g[key]) <= 0.01, key
