@@ -14,6 +14,15 @@ constexpr int KB = 64;         // bf16 per 128-byte swizzled row
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32 + 64;    // score kernel: + 2 converter warps
 constexpr int THREADS_Q = 64 + EPI_WARPS * 32 + 128;  // packed keys: + 4 converter warps
+// standalone score kernel: epilogue warps (4 TMEM lane quarters x SCORE_EPI / 4
+// frequency slices); the fused score+value kernel keeps EPI_WARPS
+#ifndef PALU_SCORE_EPI_WARPS
+#define PALU_SCORE_EPI_WARPS 8
+#endif
+constexpr int SCORE_EPI = PALU_SCORE_EPI_WARPS;
+static_assert(SCORE_EPI == 8 || SCORE_EPI == 16, "score epilogue: 8 or 16 warps");
+constexpr int THREADS_S = 64 + SCORE_EPI * 32 + 64;
+constexpr int THREADS_SQ = 64 + SCORE_EPI * 32 + 128;
 constexpr int H_STAGE_BYTES = TILE_M * 128;  // 16 KB per (tile, k-block)
 constexpr int UW_KB_BYTES = N_CTA * 128;     // 32 KB per k-block
 constexpr int SMEM_LIMIT = 232448;           // 227 KB opt-in
@@ -206,6 +215,21 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float* v) {
                : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+  static_assert(N == 4 || N == 8 || N == 16, "tmem_ldn: 4, 8 or 16 columns");
+  if constexpr (N == 4) tmem_ld4(taddr, v);
+  else if constexpr (N == 8) tmem_ld8(taddr, v);
+  else tmem_ld16(taddr, v);
 }
 __device__ __forceinline__ void tmem_wait_ld() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");

@@ -62,9 +62,10 @@ constexpr int TRACE_STRIDE = 512;
 constexpr int SU = 8;  // score trace marks per accumulator unit
 // score epilogue shared memory: the cross-warp reduction buffer, then per
 // epilogue warp two (cos/sin base half-row 256 B, lane scales 128 B) buffers
-constexpr int EPI_RED_BYTES = 4 * 2 * 128 * 4;
+constexpr int EPI_MAXW = SCORE_EPI > EPI_WARPS ? SCORE_EPI : EPI_WARPS;
+constexpr int EPI_RED_BYTES = 4 * (EPI_MAXW / 4 - 1) * 2 * 128 * 4;
 constexpr int EPI_STAGE_BYTES = 2 * 256 + 2 * 128;
-constexpr int SCORE_FIXED_BYTES = 512 + EPI_RED_BYTES + EPI_WARPS * EPI_STAGE_BYTES;
+constexpr int SCORE_FIXED_BYTES = 512 + EPI_RED_BYTES + EPI_MAXW * EPI_STAGE_BYTES;
 
 // Profiling modes that skip MMAs or barrier waits (results invalid) exist only
 // in diagnostic builds (-DPALU_DIAG); the product library ignores the knobs.
@@ -297,7 +298,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
 // short ranks (r <= 128: 8 MMAs per unit) the accumulator must be quad-
 // buffered to cover the ~1 us from a unit's last MMA issue to its epilogue
 // (tools/score_trace.py: 2 slots left the tensor pipe ~45 % idle at r 128).
-template <int UH, int NCONV>
+template <int UH, int NCONV, int EW>
 __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUtensorMap& map_uw,
                                            const Params& p, uint8_t* smem) {
   constexpr int NSLOT = UH == 2 ? 2 : 4;
@@ -343,7 +344,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     }
     for (int a = 0; a < NSLOT; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 2 * EPI_WARPS);
+      mbar_init(&tempty[a], 2 * EW);
     }
     mbar_init(uw_full, 1);
     mbar_init(uw_empty, 1);
@@ -519,13 +520,16 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
                        : "memory");
         }
     }
-  } else if (warp >= 2 + EPI_WARPS) {
+  } else if (warp >= 2 + EW) {
     // ---------------- quantised keys: converter warps (both SMs) ----------------
     if (p.bits != 16) {
       // the newest token's codes and zero point come from this step's latent
       // append: wait for the predecessor chain before the first code load
       pdl_wait();
-      const int cl = (warp - 2 - EPI_WARPS) * 32 + lane;  // the SM tile's row(s) of this lane
+      const int cl = (warp - 2 - EW) * 32 + lane;  // the SM tile's row(s) of this lane
+      // 16 epilogue warps leave ~96 registers: the 2-row converter build is
+      // compiled out there (the host sends packed keys to the 4-warp build)
+      if constexpr (EW == 16 && NCONV == 2) __trap();
       Ring rg;
       ItemPos ip_(i0, n_super, p.G);
       for (int i = i0; i < i1; ++i, ip_.next(n_super, p.G)) {
@@ -542,16 +546,18 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
   } else {
     // ---------------- epilogue (both SMs): cos/sin-weighted row reduction ----------------
     const int q = warp & 3;          // TMEM lane quarter
-    const int jh = (warp - 2) >> 2;  // which 32 of the 64 frequencies
+    constexpr int JH = EW / 4;       // frequency slices
+    constexpr int FPW = 64 / JH;     // frequencies per warp
+    const int jh = (warp - 2) >> 2;  // which FPW of the 64 frequencies
     const int delta = q * 32 + lane; // token row inside this SM's tile
-    constexpr int CH = 8;            // frequencies per epilogue chunk (TMEM loads of 8 columns)
+    constexpr int CH = JH == 2 ? 8 : 4;  // frequencies per epilogue chunk (TMEM loads of CH columns)
     const uint64_t pol_keep = policy_evict_last();
-    float2 cd2[16], sd2[16];         // cos/sin(delta th_j) for j pairs (2i, 2i + 1)
+    float2 cd2[FPW / 2], sd2[FPW / 2];  // cos/sin(delta th_j) for j pairs (2i, 2i + 1)
     {
       const float4* off =
-          reinterpret_cast<const float4*>(p.rope_tab + (size_t)(p.n_tab + delta) * 64 + jh * 32);
+          reinterpret_cast<const float4*>(p.rope_tab + (size_t)(p.n_tab + delta) * 64 + jh * FPW);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
+      for (int i = 0; i < FPW / 2; ++i) {
         const float4 v = off[i];
         cd2[i] = make_float2(v.x, v.y);
         sd2[i] = make_float2(v.z, v.w);
@@ -565,9 +571,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     // memory with cp.async one item ahead.
     uint8_t* eb = reinterpret_cast<uint8_t*>(red) + EPI_RED_BYTES + (warp - 2) * EPI_STAGE_BYTES;
     auto stage_item = [&](int buf, int tile_, int bg_) {
-      if (lane < 16)
+      if (lane < FPW / 2)
         cp_async16(eb + buf * 256 + lane * 16,
-                   reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile_ * 64 + jh * 32) + lane);
+                   reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile_ * 64 + jh * FPW) + lane);
       if (p.bits != 16) {
         const int tq = tile_ * TILE_M + delta;
         if (tq < T_rows) cp_async4(eb + 512 + buf * 128 + lane * 4, p.scales + (size_t)bg_ * p.T_cap + tq);
@@ -612,7 +618,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         for (int hp = 0; hp < UH; ++hp) acc2[hp] = make_float2(0.f, 0.f);
         if ((mode & 1) == 0)
 #pragma unroll
-        for (int jc = 0; jc < 32 / CH; ++jc) {
+        for (int jc = 0; jc < FPW / CH; ++jc) {
           // this chunk's accumulator columns (u_j at col, w_j at col + 64) for
           // every head of the unit, then cos/sin((t0 + delta) th_j) = base (x)
           // offset for its CH frequencies while the loads are in flight
@@ -622,9 +628,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
           float u[UH][CH], w[UH][CH];
 #pragma unroll
           for (int hp = 0; hp < UH; ++hp) {
-            const uint32_t col = slot * SLOT_COLS + hp * 128 + jh * 32 + jc * CH;
-            tmem_ld8(lane_base + col, u[hp]);
-            tmem_ld8(lane_base + col + 64, w[hp]);
+            const uint32_t col = slot * SLOT_COLS + hp * 128 + jh * FPW + jc * CH;
+            tmem_ldn<CH>(lane_base + col, u[hp]);
+            tmem_ldn<CH>(lane_base + col + 64, w[hp]);
           }
           float2 c2[CH / 2], s2[CH / 2];
 #pragma unroll
@@ -636,7 +642,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             s2[k] = ffma2(bsn, cd2[jc * (CH / 2) + k], fmul2(bc, sd2[jc * (CH / 2) + k]));
           }
           tmem_wait_ld();
-          if (jc == 32 / CH - 1) {
+          if (jc == FPW / CH - 1) {
             // every accumulator column this warp reads is in registers: hand
             // the slot back before the last FMAs and the cross-warp exchange
             fence_before();
@@ -665,16 +671,21 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         // in flight, and reuse at u + 4 waits (through the MMA) for every
         // warp's release of u + 2, issued after its reads of u
         const int xb = unit & 3;
-        float* r = red + xb * UH * TILE_M;
-        if (jh == 1) {
-          r[delta] = v[0];
-          if (UH == 2) r[TILE_M + delta] = v[1];
-          named_bar_arrive(1 + xb, EPI_WARPS * 32);
+        float* r = red + xb * (JH - 1) * UH * TILE_M;
+        if (jh != 0) {
+          r[(jh - 1) * UH * TILE_M + delta] = v[0];
+          if (UH == 2) r[((jh - 1) * UH + 1) * TILE_M + delta] = v[1];
+          named_bar_arrive(1 + xb, EW * 32);
         } else {
-          named_bar_sync(1 + xb, EPI_WARPS * 32);
+          named_bar_sync(1 + xb, EW * 32);
           if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 8 + SU * unit] = clock64();
-          const uint32_t ra = smem_u32(r + delta);
-          const float v0 = v[0] + lds32f(ra), v1 = UH == 2 ? v[1] + lds32f(ra + TILE_M * 4) : 0.f;
+          float v0 = v[0], v1 = v[1];
+#pragma unroll
+          for (int k = 0; k < JH - 1; ++k) {
+            const uint32_t ra = smem_u32(r + k * UH * TILE_M + delta);
+            v0 += lds32f(ra);
+            if (UH == 2) v1 += lds32f(ra + TILE_M * 4);
+          }
           const int t = tile * TILE_M + delta;
           if (t < T_rows) {
             // UH 2: D columns 0..127 = head 2h (leader's UW rows), 128..255 =
@@ -714,7 +725,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 // registers), 4 for packed keys (2 left the int4-key score at 173 us vs 156
 // with 4; the 12-warp build gets 128 registers)
 template <int UH, int NCONV>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + EPI_WARPS * 32 + NCONV * 32, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + SCORE_EPI * 32 + NCONV * 32, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
   // setup overlaps the query absorb; only the UW loads read its output
@@ -727,7 +738,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  score_role<UH, NCONV>(map_h, map_uw, p, smem);
+  score_role<UH, NCONV, SCORE_EPI>(map_h, map_uw, p, smem);
 }
 
 // ===========================================================================
@@ -1521,7 +1532,7 @@ rope_attend_tc_kernel(const __grid_constant__ CUtensorMap map_h,
     p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 2] = smid_u32();
   }
   if ((int)(blockIdx.x >> 1) < p.score_pairs) {
-    score_role<2, 2>(map_h, map_uw, p, smem);
+    score_role<2, 2, EPI_WARPS>(map_h, map_uw, p, smem);
   } else {
     const int vcta = (int)blockIdx.x - 2 * p.score_pairs;
     value_role(map_v, p, vp, smem, vcta, (int)gridDim.x - 2 * p.score_pairs);
@@ -2011,6 +2022,8 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
   // one, tools/score_trace.py; kept as an option)
   const int uh = getenv("PALU_SCORE_UH") ? atoi(getenv("PALU_SCORE_UH")) : 2;
   PALU_REQUIRE(uh == 1 || uh == 2, "PALU_SCORE_UH must be 1 or 2");
+  PALU_REQUIRE(SCORE_EPI == 8 || uh == 2 || bits == 16,
+               "PALU_SCORE_UH=1 with packed keys needs the 8-warp score epilogue build");
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, uh == 2 ? TILE_M : 64);
   if (rc) return rc;
   const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + SCORE_FIXED_BYTES;
@@ -2067,13 +2080,13 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
     g_trace_ctas = sms & ~1;
   }
   if (uh == 1)
-    PALU_CK(launch_k(rope_score_tc_kernel<1, 2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+    PALU_CK(launch_k(rope_score_tc_kernel<1, 2>, dim3(sms & ~1), dim3(THREADS_S), smem, (cudaStream_t)stream,
                      map_h, map_uw, prm));
   else if (bits != 16)
-    PALU_CK(launch_k(rope_score_tc_kernel<2, 4>, dim3(sms & ~1), dim3(THREADS_Q), smem,
+    PALU_CK(launch_k(rope_score_tc_kernel<2, 4>, dim3(sms & ~1), dim3(THREADS_SQ), smem,
                      (cudaStream_t)stream, map_h, map_uw, prm));
   else
-    PALU_CK(launch_k(rope_score_tc_kernel<2, 2>, dim3(sms & ~1), dim3(THREADS), smem, (cudaStream_t)stream,
+    PALU_CK(launch_k(rope_score_tc_kernel<2, 2>, dim3(sms & ~1), dim3(THREADS_S), smem, (cudaStream_t)stream,
                      map_h, map_uw, prm));
   PALU_LAUNCHED();
   return PALU_OK;
