@@ -502,8 +502,10 @@ def main():
 
     # --- live per-kernel timing for the roofline (same warm state) ------
     prof = sess.profile_step()
-    if "palu_rope_score_tc_pf" in prof:  # the score entry that also prefetches the output weights
-        prof["palu_rope_score_tc"] = prof.pop("palu_rope_score_tc_pf")
+    rep_used = "palu_rope_score_tc_rep" in prof  # K reconstructed once per KV head (GQA)
+    for alias in ("palu_rope_score_tc_pf", "palu_rope_score_tc_rep"):  # other rope score entries
+        if alias in prof:
+            prof["palu_rope_score_tc"] = prof.pop(alias)
     cache.t += 1
     torch.cuda.synchronize()
 
@@ -548,7 +550,8 @@ def main():
         if score_name in prof:
             break
     score_ms = statistics.mean(prof[score_name])
-    flops = 2.0 * T1 * (NH // shards) * args.rank_k * DH * args.batch  # reconstruction
+    rec_heads = (args.kv_heads if rep_used else NH) // shards  # heads whose K is reconstructed
+    flops = 2.0 * T1 * rec_heads * args.rank_k * DH * args.batch  # reconstruction
     k_bytes = T1 * k_tok * args.batch
     v_bytes = T1 * v_tok * args.batch
     achieved_tf = flops / (score_ms * 1e-3) / 1e12
@@ -556,7 +559,9 @@ def main():
     sv_name = next((k for k in ("palu_value_tc", "palu_softmax_value") if k in prof), None)
     sv_ms = statistics.mean(prof[sv_name]) if sv_name else 0.0
     latent_total = k_bytes + v_bytes
-    if args.rope == "off":  # no reconstruction: the score kernel streams H_k (HBM-bound)
+    # rope off: no reconstruction, the score kernel streams H_k (HBM-bound);
+    # GQA with K rebuilt once per KV head: the key stream outlasts the MMAs
+    if args.rope == "off" or k_bytes / (hbm * 1e9) > flops / (tf_burst * 1e12):
         achieved_gbs = k_bytes / (score_ms * 1e-3) / 1e9
         roofline_head = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm, "unit": "GB/s",
                          "frac": achieved_gbs / hbm, "traffic": None,

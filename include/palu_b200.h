@@ -122,6 +122,8 @@ int palu_pack_rows(const uint8_t* codes, int rows, int cols, int bits, uint8_t* 
  * bk: [G][bk_rows][s_k*d_h] in `dtype` (rows >= rank zero, bk_rows >= R_pad).
  * layout 0: uw fp32 [B][n][R_pad][d_h]  (cols j < h: u_j, j >= h: w_{j-h})
  * layout 1: uw bf16 [B][G][s_k*d_h][R_pad] (K-major rows, tcgen05 B operand)
+ * layout 4: uw float [B][n][d_h] = scale x RoPE_t(q) only (replicated-B groups,
+ *           palu_rope_score_tc_rep)
  * layouts 2/3: as 1 with the rank order permuted for int4 / int2 keys on the
  *   tcgen05 path (groups of 8 / 16: rank k at position k < G/2 ? 2k : 2k-G+1)
  */
@@ -184,6 +186,21 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
                           int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
                           const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
                           const void* l2_prefetch, long long l2_prefetch_bytes, void* stream);
+/*
+ * Replicated-B groups (GQA as its MHA-equivalent layer: the s = n_heads / G
+ * query heads of a group share one KV head's B_k columns):
+ * reconstruct K = H B once per KV head on the tensor pipe, RoPE each key pair
+ * in the epilogue and dot it with the group's rotated queries -- the same
+ * logits as palu_rope_score_tc with 1/s of the accumulator traffic.
+ * bkt: bf16 [B][G][128][R_pad], row c = column c of the group's KV-head B_k
+ * (rank order as the cache); qrot: float [B][n_heads][128] = scale x
+ * RoPE_t(q) (palu_append_absorb layout 4).  Raw bf16 keys, head_dim 128,
+ * n_heads / G == 4, R_pad % 64 == 0 and <= 256.  Replaces the per-head
+ * reconstruction of attention.py:433-444 for such groups.
+ */
+int palu_rope_score_tc_rep(const void* hk, int B, int n_heads, int G, int R_pad, int T_cap, const void* bkt,
+                           const float* qrot, const float* rope_tab, const int* t_dev, float* logits,
+                           int ld_logits, void* stream);
 
 /*
  * Fused RoPE score + softmax + value path (attention.py:433-446, 350-362 up

@@ -46,6 +46,7 @@ SIGNATURES = {
     "palu_rope_score_tc_splits": (i32, [i32, i32]),
     "palu_rope_score_tc": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, p]),
     "palu_rope_score_tc_pf": (i32, [i32, p, p, p, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, p, i64, p]),
+    "palu_rope_score_tc_rep": (i32, [p, i32, i32, i32, i32, i32, p, p, p, p, p, i32, p]),
     "palu_rope_attend_workspace": (sz, [i32, i32, i32, i32, i32]),
     "palu_rope_attend_tc": (i32, [p, p, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, i32, p, p, p,
                                   i32, p, i32, p]),

@@ -37,6 +37,9 @@ _APPEND_SPLIT = os.environ.get("PALU_APPEND_SPLIT") == "1"  # A/B diagnostics on
 _APPEND_ABSORB = os.environ.get("PALU_APPEND_ABSORB", "1") != "0"
 # PALU_L2PF=1: L2 prefetch of the output projection during the score (measured slower; A/B)
 _L2PF = os.environ.get("PALU_L2PF") == "1"
+# replicated-B key groups (GQA as its MHA-equivalent layer): reconstruct K once
+# per KV head (palu_rope_score_tc_rep); PALU_GQA_REP=0 keeps the per-head path
+_GQA_REP = os.environ.get("PALU_GQA_REP", "1") != "0"
 SUPPORTED_BITS = (2, 3, 4, 8)
 DTYPES = ("float32", "bfloat16")
 
@@ -559,6 +562,24 @@ class _Session:
                          for (K, V) in c._stores)
             self.ws_fused = torch.zeros(nbytes // 4 + 1, dtype=torch.float32, device=dev)
         self.score_sms = int(os.environ.get("PALU_SCORE_SMS", "0"))
+        # replicated-B groups: every query head of a key group uses the same
+        # B_k columns (one KV head); the score reconstructs K = H B once per
+        # group and dots the rotated keys with the group's 4 rotated queries
+        self.rep_bkt = [None] * len(fused.layers)
+        self.qrot = None
+        for li, L in enumerate(fused.layers):
+            K = c._stores[li][0]
+            if not (self.tc_layers[li] and not self.fused_layers[li] and _GQA_REP and K.bits == FP_BITS
+                    and L.s_k == 4 and self.dh == 128 and _APPEND_ABSORB and not _APPEND_SPLIT):
+                continue
+            bk = L.bk[:, :K.r_pad]  # [G][R_pad][s_k d_h]
+            blocks = bk.reshape(bk.shape[0], K.r_pad, L.s_k, self.dh)
+            if not bool((blocks == blocks[:, :, :1]).all()):
+                continue
+            bkt = blocks[:, :, 0].transpose(1, 2).contiguous()  # [G][d_h][R_pad]
+            self.rep_bkt[li] = bkt.unsqueeze(0).expand(self.B, -1, -1, -1).contiguous()
+            if self.qrot is None:
+                self.qrot = torch.zeros(self.B * self.n * self.dh, dtype=torch.float32, device=dev)
         self.uw_bf = None
         self.rope_tab = None
         if any(self.tc_layers):
@@ -594,6 +615,8 @@ class _Session:
         # matches the converter's code order for int4 / int2 keys)
         if self.fused_layers[li]:
             uw_ptr, layout = _ptr(self.uw_bf), 1
+        elif self.rep_bkt[li] is not None:
+            uw_ptr, layout = _ptr(self.qrot), 4  # rotated queries only
         elif self.tc_layers[li]:
             uw_ptr, layout = _ptr(self.uw_bf), {4: 2, 2: 3}.get(K.bits, 1)
         else:
@@ -646,7 +669,11 @@ class _Session:
                       _ptr(self.ctx), self.ko, _ptr(self.ws_fused), self.score_sms, st)
             self._proj(code, L.woT, d, L.ko_pad, self.ctx, x, st)
             return
-        if self.tc_layers[li]:
+        if self.rep_bkt[li] is not None:
+            _lib.call("palu_rope_score_tc_rep", _ptr(K.rows), B, n, K.G, K.r_pad, K.cap,
+                      _ptr(self.rep_bkt[li]), _ptr(self.qrot), _ptr(self.rope_tab), _ptr(self.t_dev),
+                      _ptr(self.logits), self.ld_logits, st)
+        elif self.tc_layers[li]:
             if _L2PF:  # the output projection's weights ride into L2 during the score
                 _lib.call("palu_rope_score_tc_pf", K.bits, _ptr(K.rows), _ptr(K.scales), _ptr(K.zps), B,
                           n, L.s_k, K.G, K.r_pad, K.cap, _ptr(self.uw_bf), _ptr(self.rope_tab),

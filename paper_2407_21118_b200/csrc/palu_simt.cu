@@ -352,6 +352,21 @@ __device__ __forceinline__ void query_absorb_body(const float* __restrict__ q, i
     csn[j] = cs;
     csn[half + j] = sn;
   }
+  if (layout == 4) {
+    // replicated-B groups (GQA as its MHA-equivalent layer): the score kernel
+    // reconstructs K = H B once per KV head, so only the rotated query is
+    // needed: uw = float [B][n_heads][dh] = scale x RoPE_pos(q) (fp64 angles)
+    pdl_wait();  // q comes from the preceding GEMV
+    __syncthreads();
+    float* out = reinterpret_cast<float*>(uw) + ((size_t)b * n_heads + i) * dh;
+    for (int j = threadIdx.x; j < half; j += blockDim.x) {
+      const double cs = csn[j], sn = csn[half + j];
+      const double lo = qh[j], hi = qh[j + half];
+      out[j] = scale * (float)(lo * cs - hi * sn);
+      out[j + half] = scale * (float)(lo * sn + hi * cs);
+    }
+    return;
+  }
   const int width = s_k * dh;
   const T* bg = bk + ((size_t)g * bk_rows + k0) * width + (size_t)p * dh;
   constexpr int V = 16 / (int)sizeof(T);
@@ -1542,7 +1557,7 @@ int palu_append_absorb(int dtype, int bits_k, int bits_v, const float* lat_k, co
   PALU_REQUIRE(bk_rows >= R_pad_k, "palu_append_absorb: bk has %d rows < R_pad %d", bk_rows, R_pad_k);
   PALU_REQUIRE(head_dim % 2 == 0, "rotary embedding requires an even head_dim");
   PALU_REQUIRE(s_k >= 1 && n_heads % s_k == 0, "group size %d does not divide %d heads", s_k, n_heads);
-  PALU_REQUIRE(layout >= 0 && layout <= 3, "palu_append_absorb: layout must be 0..3");
+  PALU_REQUIRE(layout >= 0 && layout <= 4, "palu_append_absorb: layout must be 0..4");
   size_t smem = ((size_t)head_dim + 32 * ((size_t)head_dim + 1)) * sizeof(float) +
                 (size_t)head_dim * sizeof(double);
   for (int side = 0; side < 2; ++side) {
@@ -1558,7 +1573,7 @@ int palu_append_absorb(int dtype, int bits_k, int bits_v, const float* lat_k, co
                      scales_k, zps_k, scales64_k, zps64_k};
   const AppendSide v{bits_v, G_v, R_pad_v, lat_v, ranks_v, lat_off_v, rows_v,
                      scales_v, zps_v, scales64_v, zps64_v};
-  const int gy = (R_pad_k + 31) / 32;
+  const int gy = layout == 4 ? 1 : (R_pad_k + 31) / 32;  // layout 4: rotated query rows only
   const AbsorbArgs a{q, ld_q, n_heads, head_dim, s_k, bk, bk_rows, R_pad_k, theta, scale, uw, layout, gy};
   const int n_abs = n_heads * gy * B, n_app = (G_k + G_v) * B;
   if (dtype == PALU_DTYPE_BF16)

@@ -56,16 +56,24 @@ struct Params {
   const uint8_t* codes;
   const float* scales;
   const float* zps;
+  // replicated-B groups (QH > 1): scale x RoPE(q) rows, float [B][n_heads][128]
+  const float* qrot;
 };
 
 constexpr int TRACE_STRIDE = 512;
 constexpr int SU = 8;  // score trace marks per accumulator unit
 // score epilogue shared memory: the cross-warp reduction buffer, then per
 // epilogue warp two (cos/sin base half-row 256 B, lane scales 128 B) buffers
+// (+ for replicated-B groups two buffers of the QH rotated query slices)
 constexpr int EPI_MAXW = SCORE_EPI > EPI_WARPS ? SCORE_EPI : EPI_WARPS;
-constexpr int EPI_RED_BYTES = 4 * (EPI_MAXW / 4 - 1) * 2 * 128 * 4;
-constexpr int EPI_STAGE_BYTES = 2 * 256 + 2 * 128;
-constexpr int SCORE_FIXED_BYTES = 512 + EPI_RED_BYTES + EPI_MAXW * EPI_STAGE_BYTES;
+constexpr int epi_red_bytes(int nout) { return 4 * (EPI_MAXW / 4 - 1) * (nout < 2 ? 2 : nout) * 128 * 4; }
+constexpr int epi_stage_bytes(int qh) { return 2 * 256 + 2 * 128 + (qh > 1 ? 2 * qh * 256 : 0); }
+constexpr int score_fixed_bytes(int nout, int qh) {
+  return 512 + epi_red_bytes(nout) + EPI_MAXW * epi_stage_bytes(qh);
+}
+constexpr int EPI_RED_BYTES = epi_red_bytes(2);
+constexpr int EPI_STAGE_BYTES = epi_stage_bytes(1);
+constexpr int SCORE_FIXED_BYTES = score_fixed_bytes(2, 1);
 
 // Profiling modes that skip MMAs or barrier waits (results invalid) exist only
 // in diagnostic builds (-DPALU_DIAG); the product library ignores the knobs.
@@ -298,7 +306,7 @@ __device__ __forceinline__ void convert_tile(const PP& p, uint8_t* s_h, uint64_t
 // short ranks (r <= 128: 8 MMAs per unit) the accumulator must be quad-
 // buffered to cover the ~1 us from a unit's last MMA issue to its epilogue
 // (tools/score_trace.py: 2 slots left the tensor pipe ~45 % idle at r 128).
-template <int UH, int NCONV, int EW>
+template <int UH, int NCONV, int EW, int QH = 1>
 __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUtensorMap& map_uw,
                                            const Params& p, uint8_t* smem) {
   constexpr int NSLOT = UH == 2 ? 2 : 4;
@@ -569,8 +577,13 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     // item (L2 latency under the HBM stream; tools/score_trace.py at r_k 128:
     // the tensor pipe idled behind it), so this warp stages them into shared
     // memory with cp.async one item ahead.
-    uint8_t* eb = reinterpret_cast<uint8_t*>(red) + EPI_RED_BYTES + (warp - 2) * EPI_STAGE_BYTES;
-    auto stage_item = [&](int buf, int tile_, int bg_) {
+    // QH > 1 (replicated-B groups, UH 1): the accumulator holds K = H B of the
+    // group's one KV head (cols j: dim j, j + 64: dim j + 64); the epilogue
+    // rotates each pair and dots it with the QH query heads' rotated rows
+    static_assert(QH == 1 || UH == 1, "replicated-B groups use N128 units");
+    constexpr int NOUT = UH * QH;  // logits per lane per unit
+    uint8_t* eb = reinterpret_cast<uint8_t*>(red) + epi_red_bytes(NOUT) + (warp - 2) * epi_stage_bytes(QH);
+    auto stage_item = [&](int buf, int tile_, int bg_, int qbuf) {
       if (lane < FPW / 2)
         cp_async16(eb + buf * 256 + lane * 16,
                    reinterpret_cast<const float4*>(p.rope_tab + (size_t)tile_ * 64 + jh * FPW) + lane);
@@ -578,13 +591,26 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         const int tq = tile_ * TILE_M + delta;
         if (tq < T_rows) cp_async4(eb + 512 + buf * 128 + lane * 4, p.scales + (size_t)bg_ * p.T_cap + tq);
       }
+      if (QH > 1 && qbuf >= 0) {
+        // [hh][FPW lo dims | FPW hi dims] of this warp's frequency slice
+#pragma unroll
+        for (int c = lane; c < QH * 2 * FPW / 4; c += 32) {
+          const int hh = c / (FPW / 2), part = c % (FPW / 2);
+          const int dim = (part < FPW / 4 ? part * 4 : 64 + (part - FPW / 4) * 4) + jh * FPW;
+          cp_async16(eb + 768 + qbuf * QH * 256 + c * 16, p.qrot + ((size_t)bg_ * QH + hh) * 128 + dim);
+        }
+      }
       cp_async_commit();
     };
     // quantised keys: the newest token's scale comes from this step's append
     pdl_wait();
     int unit = 0, it = 0;
+    // QH > 1: the query slices change only with (b, g) -- restaged into the
+    // idle buffer when the next item moves to another group
+    int q_use = 0, q_next = 0, q_bg0 = -1, q_bg1 = -1;
     ItemPos ip_(i0, n_super, p.G), nx(i0, n_super, p.G);
-    if (i0 < i1) stage_item(0, 2 * nx.st + (int)rank, nx.bg);
+    if (i0 < i1) stage_item(0, 2 * nx.st + (int)rank, nx.bg, 0);
+    q_bg0 = nx.bg;
     nx.next(n_super, p.G);
     for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
       const int bg = ip_.bg, st = ip_.st;
@@ -594,6 +620,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 10 + SU * unit] = clock64();
       cp_async_wait_all();
       __syncwarp();
+      q_use = q_next;
       if (kTrace && p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 && SU * unit + 11 < TRACE_STRIDE)
         p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 11 + SU * unit] = clock64();
       const uint32_t base_addr = smem_u32(eb) + (uint32_t)(it & 1) * 256u;
@@ -602,7 +629,13 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
       if (p.bits != 16 && tile * TILE_M + delta < T_rows)
         sq = lds32f(smem_u32(eb) + 512u + (uint32_t)(it & 1) * 128u + (uint32_t)lane * 4u);
       if (i + 1 < i1) {  // the other buffer was consumed an item ago
-        stage_item((it + 1) & 1, 2 * nx.st + (int)rank, nx.bg);
+        int qbuf = -1;
+        if (QH > 1 && (q_use ? q_bg1 : q_bg0) != nx.bg) {
+          qbuf = q_use ^ 1;  // idle since the item before this one
+          if (qbuf) q_bg1 = nx.bg; else q_bg0 = nx.bg;
+        }
+        q_next = qbuf >= 0 ? qbuf : q_use;
+        stage_item((it + 1) & 1, 2 * nx.st + (int)rank, nx.bg, qbuf);
         nx.next(n_super, p.G);
       }
       for (int h = 0; h < units; ++h, ++unit) {
@@ -613,9 +646,9 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
         mbar_wait(&tfull[slot], (unit / NSLOT) & 1);
         fence_after();
         if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 6 + SU * unit] = clock64();
-        float2 acc2[UH];
+        float2 acc2[NOUT];
 #pragma unroll
-        for (int hp = 0; hp < UH; ++hp) acc2[hp] = make_float2(0.f, 0.f);
+        for (int o = 0; o < NOUT; ++o) acc2[o] = make_float2(0.f, 0.f);
         if ((mode & 1) == 0)
 #pragma unroll
         for (int jc = 0; jc < FPW / CH; ++jc) {
@@ -649,51 +682,71 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
             __syncwarp();
             if (lane == 0) mbar_arrive_leader(&tempty[slot]);
           }
+          if constexpr (QH == 1) {
 #pragma unroll
-          for (int hp = 0; hp < UH; ++hp)
+            for (int hp = 0; hp < UH; ++hp)
+#pragma unroll
+              for (int k = 0; k < CH / 2; ++k) {
+                acc2[hp] = ffma2(c2[k], make_float2(u[hp][2 * k], u[hp][2 * k + 1]), acc2[hp]);
+                acc2[hp] = ffma2(s2[k], make_float2(w[hp][2 * k], w[hp][2 * k + 1]), acc2[hp]);
+              }
+          } else {
+            const uint32_t qb = smem_u32(eb) + 768u + (uint32_t)q_use * (QH * 256u);
 #pragma unroll
             for (int k = 0; k < CH / 2; ++k) {
-              acc2[hp] = ffma2(c2[k], make_float2(u[hp][2 * k], u[hp][2 * k + 1]), acc2[hp]);
-              acc2[hp] = ffma2(s2[k], make_float2(w[hp][2 * k], w[hp][2 * k + 1]), acc2[hp]);
+              // RoPE of the key pair (dims j, j + 64) for frequencies j, j + 1
+              const float2 lo = make_float2(u[0][2 * k], u[0][2 * k + 1]);
+              const float2 hi = make_float2(w[0][2 * k], w[0][2 * k + 1]);
+              const float2 t = fmul2(s2[k], hi);
+              const float2 klo = ffma2(c2[k], lo, make_float2(-t.x, -t.y));
+              const float2 khi = ffma2(s2[k], lo, fmul2(c2[k], hi));
+              const uint32_t jo = (uint32_t)(jc * CH + 2 * k) * 4u;
+#pragma unroll
+              for (int hh = 0; hh < QH; ++hh) {
+                const float2 ql = lds64f(qb + (uint32_t)hh * (2u * FPW * 4u) + jo);
+                const float2 qh = lds64f(qb + (uint32_t)hh * (2u * FPW * 4u) + FPW * 4u + jo);
+                acc2[hh] = ffma2(klo, ql, acc2[hh]);
+                acc2[hh] = ffma2(khi, qh, acc2[hh]);
+              }
             }
+          }
         }
         if (mode & 1) {  // diagnostics: no math, release the slot at once
           fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive_leader(&tempty[slot]);
         }
-        float v[2] = {0.f, 0.f};
+        float v[NOUT];
 #pragma unroll
-        for (int hp = 0; hp < UH; ++hp) v[hp] = acc2[hp].x + acc2[hp].y;
+        for (int o = 0; o < NOUT; ++o) v[o] = acc2[o].x + acc2[o].y;
         if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 7 + SU * unit] = clock64();
         // exchange buffer and named barrier rotate over 4 units: a warp hands
         // the slot back before this exchange, so unit u + 2 may already be
         // in flight, and reuse at u + 4 waits (through the MMA) for every
         // warp's release of u + 2, issued after its reads of u
         const int xb = unit & 3;
-        float* r = red + xb * (JH - 1) * UH * TILE_M;
+        float* r = red + xb * (JH - 1) * NOUT * TILE_M;
         if (jh != 0) {
-          r[(jh - 1) * UH * TILE_M + delta] = v[0];
-          if (UH == 2) r[((jh - 1) * UH + 1) * TILE_M + delta] = v[1];
+#pragma unroll
+          for (int o = 0; o < NOUT; ++o) r[((jh - 1) * NOUT + o) * TILE_M + delta] = v[o];
           named_bar_arrive(1 + xb, EW * 32);
         } else {
           named_bar_sync(1 + xb, EW * 32);
           if (tr) p.trace[(size_t)blockIdx.x * TRACE_STRIDE + 8 + SU * unit] = clock64();
-          float v0 = v[0], v1 = v[1];
 #pragma unroll
-          for (int k = 0; k < JH - 1; ++k) {
-            const uint32_t ra = smem_u32(r + k * UH * TILE_M + delta);
-            v0 += lds32f(ra);
-            if (UH == 2) v1 += lds32f(ra + TILE_M * 4);
-          }
+          for (int k = 0; k < JH - 1; ++k)
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o) v[o] += lds32f(smem_u32(r + (k * NOUT + o) * TILE_M + delta));
           const int t = tile * TILE_M + delta;
           if (t < T_rows) {
             // UH 2: D columns 0..127 = head 2h (leader's UW rows), 128..255 =
             // head 2h + 1; UH 1: columns 0..63 u_j (leader), 64..127 w_j (peer)
-            const int head0 = g * p.s_k + UH * h;
+            // QH > 1: the group's query heads g QH .. g QH + QH - 1
+            const int head0 = (g * p.s_k + UH * h) * QH;
             float* lg = p.logits + ((size_t)b * p.n_heads + head0) * p.ld_logits + t;
-            stg_hint(lg, v0 * sq, pol_keep);  // read by the value kernel next: keep in L2
-            if (UH == 2) stg_hint(lg + p.ld_logits, v1 * sq, pol_keep);
+#pragma unroll
+            for (int o = 0; o < NOUT; ++o)  // read by the value kernel next: keep in L2
+              stg_hint(lg + (size_t)o * p.ld_logits, v[o] * sq, pol_keep);
           }
           if (kTrace && p.trace != nullptr && p.ready != nullptr && warp == 2 && lane == 0 && h == units - 1 &&
               it < TRACE_STRIDE - 8)
@@ -724,7 +777,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
 // NCONV converter warps: 2 for raw bf16 keys (idle; 10 warps keep 168
 // registers), 4 for packed keys (2 left the int4-key score at 173 us vs 156
 // with 4; the 12-warp build gets 128 registers)
-template <int UH, int NCONV>
+template <int UH, int NCONV, int QH = 1>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(64 + SCORE_EPI * 32 + NCONV * 32, 1)
 rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
                      const __grid_constant__ CUtensorMap map_uw, const Params p) {
@@ -738,7 +791,7 @@ rope_score_tc_kernel(const __grid_constant__ CUtensorMap map_h,
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  score_role<UH, NCONV, SCORE_EPI>(map_h, map_uw, p, smem);
+  score_role<UH, NCONV, SCORE_EPI, QH>(map_h, map_uw, p, smem);
 }
 
 // ===========================================================================
@@ -1994,16 +2047,20 @@ int palu_rope_score_tc(int bits, const void* hk, const float* scales, const floa
                                logits, ld_logits, nullptr, 0, stream);
 }
 
-int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const float* zps, int B,
-                          int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
-                          const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
-                          const void* l2_prefetch, long long l2_prefetch_bytes, void* stream) {
+// qh > 1: replicated-B groups (uw = the static K-major B^T of each group's KV
+// head, [B][G][128][R_pad]; qrot = scale x RoPE(q) rows), s_k = 1 per group
+static int rope_score_impl(int bits, const void* hk, const float* scales, const float* zps, int B,
+                           int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
+                           const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
+                           const void* l2_prefetch, long long l2_prefetch_bytes, const float* qrot, int qh,
+                           void* stream) {
   using namespace palu::tc;
   if (bits != 16 && bits != 2 && bits != 3 && bits != 4 && bits != 8) {
     set_error("palu_rope_score_tc: bits %d unsupported", bits);
     return PALU_EUNSUPPORTED;
   }
-  if (!palu_rope_score_tc_splits(s_k, R_pad) || G * s_k != n_heads) {
+  if (qh > 1 ? (s_k != 1 || R_pad % KB != 0 || R_pad > 256 || G * qh != n_heads)
+             : (!palu_rope_score_tc_splits(s_k, R_pad) || G * s_k != n_heads)) {
     set_error("palu_rope_score_tc: unsupported shape (R_pad %d, s_k %d)", R_pad, s_k);
     return PALU_EUNSUPPORTED;
   }
@@ -2020,13 +2077,15 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
   // heads per accumulator unit: 1 (quad-buffered N128) for short ranks
   // (UH 1 measured slower at r 128: an N128 pair-MMA costs as much as an N256
   // one, tools/score_trace.py; kept as an option)
-  const int uh = getenv("PALU_SCORE_UH") ? atoi(getenv("PALU_SCORE_UH")) : 2;
+  const int uh = qh > 1 ? 1 : (getenv("PALU_SCORE_UH") ? atoi(getenv("PALU_SCORE_UH")) : 2);
   PALU_REQUIRE(uh == 1 || uh == 2, "PALU_SCORE_UH must be 1 or 2");
+  PALU_REQUIRE(qh == 1 || (qh == 4 && bits == 16 && qrot != nullptr && ((uintptr_t)qrot & 15) == 0),
+               "palu_rope_score_tc_rep: 4 query heads per KV head, raw bf16 keys, aligned rotated queries");
   PALU_REQUIRE(SCORE_EPI == 8 || uh == 2 || bits == 16,
                "PALU_SCORE_UH=1 with packed keys needs the 8-warp score epilogue build");
   rc = make_map_2d(&map_uw, uw, R_pad, (uint64_t)B * G * s_k * 128, KB, uh == 2 ? TILE_M : 64);
   if (rc) return rc;
-  const int fixed = kblocks * (s_k / 2) * HEAD_BYTES + SCORE_FIXED_BYTES;
+  const int fixed = kblocks * s_k * (HEAD_BYTES / 2) + (qh > 1 ? score_fixed_bytes(qh, qh) : SCORE_FIXED_BYTES);
   int stages = (SMEM_LIMIT - fixed) / H_STAGE_BYTES;
   if (stages > 12) stages = 12;
   PALU_REQUIRE(stages >= kblocks, "tc: not enough shared memory (%d stages)", stages);
@@ -2038,6 +2097,8 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
     PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_LIMIT));
     PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_LIMIT));
+    PALU_CK(cudaFuncSetAttribute(rope_score_tc_kernel<1, 2, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  SMEM_LIMIT));
     attr = true;
   }
@@ -2073,13 +2134,17 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
   prm.codes = reinterpret_cast<const uint8_t*>(hk);
   prm.scales = scales;
   prm.zps = zps;
+  prm.qrot = qrot;
   if (getenv("PALU_SCORE_TRACE")) {  // diagnostics: per-head-pair timeline (tools/score_trace.py)
     if (!g_trace) PALU_CK(cudaMalloc(&g_trace, (size_t)1024 * TRACE_STRIDE * 8));
     PALU_CK(cudaMemsetAsync(g_trace, 0, (size_t)1024 * TRACE_STRIDE * 8, (cudaStream_t)stream));
     prm.trace = g_trace;
     g_trace_ctas = sms & ~1;
   }
-  if (uh == 1)
+  if (qh > 1)
+    PALU_CK(launch_k(rope_score_tc_kernel<1, 2, 4>, dim3(sms & ~1), dim3(THREADS_S), smem,
+                     (cudaStream_t)stream, map_h, map_uw, prm));
+  else if (uh == 1)
     PALU_CK(launch_k(rope_score_tc_kernel<1, 2>, dim3(sms & ~1), dim3(THREADS_S), smem, (cudaStream_t)stream,
                      map_h, map_uw, prm));
   else if (bits != 16)
@@ -2090,6 +2155,21 @@ int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const f
                      map_h, map_uw, prm));
   PALU_LAUNCHED();
   return PALU_OK;
+}
+
+int palu_rope_score_tc_pf(int bits, const void* hk, const float* scales, const float* zps, int B,
+                          int n_heads, int s_k, int G, int R_pad, int T_cap, const void* uw,
+                          const float* rope_tab, const int* t_dev, float* logits, int ld_logits,
+                          const void* l2_prefetch, long long l2_prefetch_bytes, void* stream) {
+  return rope_score_impl(bits, hk, scales, zps, B, n_heads, s_k, G, R_pad, T_cap, uw, rope_tab, t_dev, logits,
+                         ld_logits, l2_prefetch, l2_prefetch_bytes, nullptr, 1, stream);
+}
+
+int palu_rope_score_tc_rep(const void* hk, int B, int n_heads, int G, int R_pad, int T_cap, const void* bkt,
+                           const float* qrot, const float* rope_tab, const int* t_dev, float* logits,
+                           int ld_logits, void* stream) {
+  return rope_score_impl(16, hk, nullptr, nullptr, B, n_heads, 1, G, R_pad, T_cap, bkt, rope_tab, t_dev, logits,
+                         ld_logits, nullptr, 0, qrot, G > 0 ? n_heads / G : 0, stream);
 }
 
 // ---- fused score + softmax + value ------------------------------------------

@@ -155,7 +155,8 @@ def run_case(P, *, T, n_layers=2, rk=256, rv=256, bits=16, hadamard=False, rope=
     rec = dict(case=name, T=T, layers=n_layers, rank_k=rk, rank_v=rv, kv_heads=gqa_kv or None,
                bits=list(bits) if isinstance(bits, tuple) else bits, hadamard=hadamard, rope=rope,
                rope_base=base, rel_l2=errs, code_mismatches=mism,
-               score_kernel=("tcgen05" if any(sess.tc_layers) else
+               score_kernel=("tcgen05_rep" if any(x is not None for x in getattr(sess, "rep_bkt", [])) else
+                             "tcgen05" if any(sess.tc_layers) else
                              "latent_score_tc" if any(sess.ls_tc_layers) else "simt"),
                value_kernel="tcgen05" if any(sess.value_tc_layers) else "simt",
                oracle_s_per_step=round(t_or / steps, 2))

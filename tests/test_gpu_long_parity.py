@@ -72,6 +72,8 @@ def test_gqa_long_context_step_matches_oracle(P, case):
     rec["tol"] = TOL
     log_result(rec)
     torch.cuda.empty_cache()
+    # raw bf16 keys: K reconstructed once per KV head (palu_rope_score_tc_rep)
+    assert rec["score_kernel"] == "tcgen05_rep", rec
     assert rec["code_mismatches"] == 0, rec
     assert max(rec["rel_l2"]) < TOL, rec
 

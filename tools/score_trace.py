@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--rank-v", type=int, default=256)
     ap.add_argument("--zero-keys", action="store_true", help="zero the key latents (data-power test)")
     ap.add_argument("--bits", type=int, default=16)
+    ap.add_argument("--kv-heads", type=int, default=0, help="GQA replicated-B layer (Mistral: 8)")
     a = ap.parse_args()
     import torch
 
@@ -36,7 +37,8 @@ def main():
 
     _lib.load()
     w, f, c = synthetic_engine(layers=1, batch=1, context=a.context, extra=64, rank_k=a.rank_k,
-                               rank_v=a.rank_v, bits=a.bits)
+                               rank_v=a.rank_v, bits=a.bits, kv_heads=a.kv_heads,
+                               rope_base=1e6 if a.kv_heads else 10000.0)
     if a.zero_keys:
         for K, _ in c._stores:
             K.rows.zero_()
