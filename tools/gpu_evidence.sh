@@ -3,7 +3,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 rm -f gpurun_out/r02_parity_final.jsonl
-PALU_PARITY_LOG=gpurun_out/r02_parity_final.jsonl timeout 2400 python -m pytest tests -q -m gpu 2>&1 | tail -3 > gpurun_out/r02_pytest_gpu.txt
+PALU_PARITY_LOG=gpurun_out/r02_parity_final.jsonl timeout 2400 python -m pytest tests -q -m gpu -rf 2>&1 | tail -6 > gpurun_out/r02_pytest_gpu.txt
 cat gpurun_out/r02_pytest_gpu.txt
 timeout 900 python bench.py > gpurun_out/r2_fin_default.log 2>&1; tail -1 gpurun_out/r2_fin_default.log > gpurun_out/r2_fin_default.json
 timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/r2_fin_reference.log 2>&1; tail -1 gpurun_out/r2_fin_reference.log > gpurun_out/r2_fin_reference.json
