@@ -71,8 +71,6 @@ constexpr int epi_stage_bytes(int qh) { return 2 * 256 + 2 * 128 + (qh > 1 ? 2 *
 constexpr int score_fixed_bytes(int nout, int qh) {
   return 512 + epi_red_bytes(nout) + EPI_MAXW * epi_stage_bytes(qh);
 }
-constexpr int EPI_RED_BYTES = epi_red_bytes(2);
-constexpr int EPI_STAGE_BYTES = epi_stage_bytes(1);
 constexpr int SCORE_FIXED_BYTES = score_fixed_bytes(2, 1);
 
 // Profiling modes that skip MMAs or barrier waits (results invalid) exist only
@@ -613,7 +611,7 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
     q_bg0 = nx.bg;
     nx.next(n_super, p.G);
     for (int i = i0; i < i1; ++i, ++it, ip_.next(n_super, p.G)) {
-      const int bg = ip_.bg, st = ip_.st;
+      const int st = ip_.st;
       const int b = ip_.b, g = ip_.g;
       const int tile = 2 * st + (int)rank;
       if (kTrace && p.trace != nullptr && p.ready == nullptr && warp == 2 && lane == 0 && SU * unit + 11 < TRACE_STRIDE)
