@@ -690,21 +690,29 @@ __device__ __forceinline__ void score_role(const CUtensorMap& map_h, const CUten
               }
           } else {
             const uint32_t qb = smem_u32(eb) + 768u + (uint32_t)q_use * (QH * 256u);
+            static_assert(CH % 4 == 0, "query slices are read 4 frequencies at a time");
 #pragma unroll
-            for (int k = 0; k < CH / 2; ++k) {
-              // RoPE of the key pair (dims j, j + 64) for frequencies j, j + 1
-              const float2 lo = make_float2(u[0][2 * k], u[0][2 * k + 1]);
-              const float2 hi = make_float2(w[0][2 * k], w[0][2 * k + 1]);
-              const float2 t = fmul2(s2[k], hi);
-              const float2 klo = ffma2(c2[k], lo, make_float2(-t.x, -t.y));
-              const float2 khi = ffma2(s2[k], lo, fmul2(c2[k], hi));
-              const uint32_t jo = (uint32_t)(jc * CH + 2 * k) * 4u;
+            for (int k4 = 0; k4 < CH / 4; ++k4) {
+              // RoPE of the key pairs (dims j, j + 64) for frequencies j .. j + 3
+              float2 klo[2], khi[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int k = 2 * k4 + e;
+                const float2 lo = make_float2(u[0][2 * k], u[0][2 * k + 1]);
+                const float2 hi = make_float2(w[0][2 * k], w[0][2 * k + 1]);
+                const float2 t = fmul2(s2[k], hi);
+                klo[e] = ffma2(c2[k], lo, make_float2(-t.x, -t.y));
+                khi[e] = ffma2(s2[k], lo, fmul2(c2[k], hi));
+              }
+              const uint32_t jo = (uint32_t)(jc * CH + 4 * k4) * 4u;
 #pragma unroll
               for (int hh = 0; hh < QH; ++hh) {
-                const float2 ql = lds64f(qb + (uint32_t)hh * (2u * FPW * 4u) + jo);
-                const float2 qh = lds64f(qb + (uint32_t)hh * (2u * FPW * 4u) + FPW * 4u + jo);
-                acc2[hh] = ffma2(klo, ql, acc2[hh]);
-                acc2[hh] = ffma2(khi, qh, acc2[hh]);
+                const float4 ql = lds128f(qb + (uint32_t)hh * (2u * FPW * 4u) + jo);
+                const float4 qh = lds128f(qb + (uint32_t)hh * (2u * FPW * 4u) + FPW * 4u + jo);
+                acc2[hh] = ffma2(klo[0], make_float2(ql.x, ql.y), acc2[hh]);
+                acc2[hh] = ffma2(khi[0], make_float2(qh.x, qh.y), acc2[hh]);
+                acc2[hh] = ffma2(klo[1], make_float2(ql.z, ql.w), acc2[hh]);
+                acc2[hh] = ffma2(khi[1], make_float2(qh.z, qh.w), acc2[hh]);
               }
             }
           }
