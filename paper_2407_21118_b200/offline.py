@@ -102,7 +102,7 @@ def fuse_hadamard_gpu(layer, device=None) -> RotatedLayer:
     dev = device or torch.device("cuda")
     groups, dims = [], []
     for g in layer.groups:
-        h = torch.from_numpy(hadamard(g.rank).data).to(dev)
+        h = torch.tensor(np.asarray(hadamard(g.rank).data), device=dev)  # copy: the Matrix view is read-only
         a = torch.from_numpy(np.ascontiguousarray(as_array(g.a))).to(dev, torch.float64)
         b = torch.from_numpy(np.ascontiguousarray(as_array(g.b))).to(dev, torch.float64)
         groups.append(GroupFactors(Matrix.wrap((a @ h).cpu().numpy()), Matrix.wrap((h.T @ b).cpu().numpy()),
