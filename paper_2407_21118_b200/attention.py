@@ -572,11 +572,9 @@ class _Session:
             if not (self.tc_layers[li] and not self.fused_layers[li] and _GQA_REP and K.bits == FP_BITS
                     and L.s_k == 4 and self.dh == 128 and _APPEND_ABSORB and not _APPEND_SPLIT):
                 continue
-            bk = L.bk[:, :K.r_pad]  # [G][R_pad][s_k d_h]
-            blocks = bk.reshape(bk.shape[0], K.r_pad, L.s_k, self.dh)
-            if not bool((blocks == blocks[:, :, :1]).all()):
+            bkt = replicated_key_operand(L.bk, K.r_pad, L.s_k, self.dh)
+            if bkt is None:
                 continue
-            bkt = blocks[:, :, 0].transpose(1, 2).contiguous()  # [G][d_h][R_pad]
             self.rep_bkt[li] = bkt.unsqueeze(0).expand(self.B, -1, -1, -1).contiguous()
             if self.qrot is None:
                 self.qrot = torch.zeros(self.B * self.n * self.dh, dtype=torch.float32, device=dev)
@@ -802,6 +800,24 @@ class _Session:
             torch.cuda.current_stream().wait_stream(s)
             self.graph = g
         self.graph.replay()
+
+
+def replicated_key_operand(bk, r_pad: int, s_k: int, dh: int):
+    """B_k of every group as the reconstruct-once score's B operand, or None.
+
+    bk: [G][rows >= r_pad][s_k * dh] (the fused B_k blocks, one d_h block per
+    query head of the group).  When every head block of every group is the
+    same (GQA as its MHA-equivalent layer: one KV head per group, SURVEY
+    7.2-10), returns bf16/fp32 [G][dh][r_pad] with row c = column c of the
+    group's KV-head block (K-major for tcgen05); otherwise None.
+    """
+    b = bk[:, :r_pad]
+    if b.shape[-1] != s_k * dh:
+        return None
+    blocks = b.reshape(b.shape[0], r_pad, s_k, dh)
+    if not bool((blocks == blocks[:, :, :1]).all()):
+        return None
+    return blocks[:, :, 0].transpose(1, 2).contiguous()
 
 
 def _session(fused, cache, score_kernel=None) -> _Session:
